@@ -1,0 +1,139 @@
+"""CPU oracle -- TEST INFRASTRUCTURE ONLY.
+
+A plain double-precision C implementation (``oracle/oracle.c``) of the two
+batch-reduction operations of TurboTransformers (arXiv 2010.05680, PAPER.md
+§4.1.2 l.313-317, Eq. 1 l.406-409, kernel names l.765), loaded with ctypes.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s
+``cpu_baseline`` / ``--impl reference`` legs may import this package.  It
+shares no code with ``paper_2010_05680_b200/`` and imports nothing from it.
+
+Parity: every function here is pinned by ``tests/test_oracle_pins.py``
+(closed forms, invariants, exhaustive decoder checks, brute force against
+mpmath, independent library routines); none is "parity unpinned".
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+import threading
+
+import numpy as np
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "oracle.c")
+_LIB_PATH = os.path.join(_HERE, "liboracle.so")
+_lock = threading.Lock()
+_lib = None
+
+DTYPE_CODE = {torch.float32: 0, torch.float16: 1, torch.bfloat16: 2}
+
+_i64 = ctypes.c_int64
+_vp = ctypes.c_void_p
+
+
+def build(force: bool = False) -> str:
+    """Compile oracle.c with gcc (plain -O2, no fast-math) into liboracle.so."""
+    stale = (not os.path.exists(_LIB_PATH)) or os.path.getmtime(_LIB_PATH) < os.path.getmtime(_SRC)
+    if force or stale:
+        tmp = _LIB_PATH + f".{os.getpid()}.tmp"
+        subprocess.check_call(
+            ["gcc", "-O2", "-fno-fast-math", "-ffp-contract=off", "-std=c11", "-fPIC",
+             "-shared", "-o", tmp, _SRC, "-lm"])
+        os.replace(tmp, _LIB_PATH)
+    return _LIB_PATH
+
+
+def _load():
+    global _lib
+    with _lock:
+        if _lib is None:
+            lib = ctypes.CDLL(build())
+            lib.tto_widen.argtypes = [_vp, ctypes.c_int, _i64, _vp]
+            lib.tto_softmax_masked.argtypes = [_vp, ctypes.c_int, _vp, _i64, _i64, _i64, _i64,
+                                               ctypes.c_float, _vp]
+            lib.tto_add_bias_layernorm.argtypes = [_vp, _vp, _vp, _vp, _vp, ctypes.c_int, _i64,
+                                                   _i64, ctypes.c_float, _vp]
+            lib.tto_layernorm_onepass_eq1.argtypes = [_vp, _vp, _vp, ctypes.c_int, _i64, _i64,
+                                                      ctypes.c_float, _vp]
+            for f in (lib.tto_widen, lib.tto_softmax_masked, lib.tto_add_bias_layernorm,
+                      lib.tto_layernorm_onepass_eq1):
+                f.restype = ctypes.c_int
+            _lib = lib
+    return _lib
+
+
+def _host(t: torch.Tensor) -> torch.Tensor:
+    if t.dtype not in DTYPE_CODE:
+        raise TypeError(f"oracle: unsupported dtype {t.dtype}")
+    return t.detach().to("cpu").contiguous()
+
+
+def _ptr(t: torch.Tensor):
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def widen(t: torch.Tensor) -> torch.Tensor:
+    """Exact storage-dtype -> float64 widening by the oracle's own bit decoders."""
+    src = _host(t)
+    out = torch.empty(src.shape, dtype=torch.float64)
+    rc = _load().tto_widen(_ptr(src), DTYPE_CODE[src.dtype], src.numel(), _ptr(out))
+    assert rc == 0
+    return out
+
+
+def softmax_masked(scores: torch.Tensor, lengths, scale: float) -> torch.Tensor:
+    """Masked softmax over the last dim of [B,H,Sq,Sk]; returns float64.
+
+    Key columns j >= clamp(lengths[b], 0, Sk) are +0.0 (DESIGN R1-R3)."""
+    if scores.dim() != 4:
+        raise ValueError("scores must be [B,H,Sq,Sk]")
+    src = _host(scores)
+    B, H, Sq, Sk = src.shape
+    lens = torch.as_tensor(np.asarray(lengths, dtype=np.int32) if not torch.is_tensor(lengths)
+                           else lengths.detach().to("cpu", torch.int32)).contiguous()
+    if lens.numel() != B:
+        raise ValueError("lengths must have B entries")
+    out = torch.empty((B, H, Sq, Sk), dtype=torch.float64)
+    rc = _load().tto_softmax_masked(_ptr(src), DTYPE_CODE[src.dtype], _ptr(lens), B, H, Sq, Sk,
+                                    ctypes.c_float(scale), _ptr(out))
+    assert rc == 0
+    return out
+
+
+def softmax_rows(rows: torch.Tensor, row_lengths, scale: float) -> torch.Tensor:
+    """Masked softmax of R independent rows [R, Sk], each with its own valid
+    length (B=R, H=Sq=1).  Used to check sampled rows of full-size runs."""
+    R, Sk = rows.shape
+    return softmax_masked(rows.reshape(R, 1, 1, Sk), row_lengths, scale).reshape(R, Sk)
+
+
+def add_bias_layernorm(x, residual, bias, gamma, beta, eps: float) -> torch.Tensor:
+    """LayerNorm((x + bias) + residual) * gamma + beta over the last dim; float64."""
+    xs, rs, bs, gs, be = (_host(t) for t in (x, residual, bias, gamma, beta))
+    if not (xs.dtype == rs.dtype == bs.dtype == gs.dtype == be.dtype):
+        raise TypeError("all LayerNorm operands share one dtype (DESIGN R11)")
+    hidden = xs.shape[-1]
+    rows = xs.numel() // hidden if hidden else 0
+    if rs.shape != xs.shape or bs.numel() != hidden or gs.numel() != hidden or be.numel() != hidden:
+        raise ValueError("shape mismatch")
+    out = torch.empty(xs.shape, dtype=torch.float64)
+    rc = _load().tto_add_bias_layernorm(_ptr(xs), _ptr(rs), _ptr(bs), _ptr(gs), _ptr(be),
+                                        DTYPE_CODE[xs.dtype], rows, hidden, ctypes.c_float(eps),
+                                        _ptr(out))
+    assert rc == 0
+    return out
+
+
+def layernorm_onepass_eq1(x, gamma, beta, eps: float) -> torch.Tensor:
+    """The paper's one-pass variance form (Eq. 1 RHS), plain LN, float64."""
+    xs, gs, be = (_host(t) for t in (x, gamma, beta))
+    hidden = xs.shape[-1]
+    rows = xs.numel() // hidden if hidden else 0
+    out = torch.empty(xs.shape, dtype=torch.float64)
+    rc = _load().tto_layernorm_onepass_eq1(_ptr(xs), _ptr(gs), _ptr(be), DTYPE_CODE[xs.dtype],
+                                           rows, hidden, ctypes.c_float(eps), _ptr(out))
+    assert rc == 0
+    return out
