@@ -1,0 +1,16 @@
+"""B200-native batch-reduction kernels of TurboTransformers (arXiv 2010.05680).
+
+The product is ``libtt.so`` (C ABI in ``include/tt.h``): in-place masked
+attention softmax and fused add-bias + residual + LayerNorm, hand-written for
+sm_100a.  This package is its thin ctypes binding; names follow the C ABI.
+"""
+from ._lib import (  # noqa: F401
+    EXPORTS, TT_ERROR_CUDA, TT_ERROR_INVALID_VALUE, TT_ERROR_NOT_SUPPORTED, TT_MAX_LN_HIDDEN,
+    TT_MAX_SOFTMAX_COLS, TT_SUCCESS, TTError, layernorm_plan, lib, softmax_plan, status_string,
+    tt_add_bias_layernorm, tt_add_bias_layernorm_raw, tt_add_bias_layernorm_staged,
+    tt_softmax_masked, tt_softmax_masked_raw, tt_softmax_masked_staged, version)
+
+__all__ = [
+    "tt_softmax_masked", "tt_add_bias_layernorm", "tt_softmax_masked_staged",
+    "tt_add_bias_layernorm_staged", "softmax_plan", "layernorm_plan", "TTError", "lib",
+]

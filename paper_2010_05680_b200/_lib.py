@@ -1,0 +1,204 @@
+"""ctypes binding of libtt.so (contract: include/tt.h).
+
+Argument marshalling only: every step of both operations runs in the CUDA
+kernels behind the C ABI.  There is no fallback of any kind -- if libtt.so is
+missing or fails to load, every call raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libtt.so")
+
+TT_SUCCESS = 0
+TT_ERROR_INVALID_VALUE = 1
+TT_ERROR_NOT_SUPPORTED = 2
+TT_ERROR_CUDA = 3
+TT_MAX_SOFTMAX_COLS = 32768
+TT_MAX_LN_HIDDEN = 32768
+
+DTYPE_CODE = {torch.float32: 0, torch.float16: 1, torch.bfloat16: 2}
+_SUFFIX = {torch.float32: "f32", torch.float16: "f16", torch.bfloat16: "bf16"}
+
+# Every symbol include/tt.h declares (checked by tests/test_abi.py).
+EXPORTS = (
+    "tt_softmax_masked_f32", "tt_softmax_masked_f16", "tt_softmax_masked_bf16",
+    "tt_add_bias_layernorm_f32", "tt_add_bias_layernorm_f16", "tt_add_bias_layernorm_bf16",
+    "tt_softmax_masked_staged", "tt_add_bias_layernorm_staged",
+    "tt_status_string", "tt_last_cuda_error", "tt_version",
+    "tt_softmax_masked_plan", "tt_add_bias_layernorm_plan",
+)
+
+
+class TTError(RuntimeError):
+    def __init__(self, status: int, what: str):
+        self.status = status
+        super().__init__(f"{what}: {status_string(status)}"
+                         + (f" (cudaError {lib().tt_last_cuda_error()})" if status == TT_ERROR_CUDA
+                            else ""))
+
+
+_i64, _vp, _f, _i = ctypes.c_int64, ctypes.c_void_p, ctypes.c_float, ctypes.c_int
+_lib = None
+_lock = threading.Lock()
+
+
+def lib() -> ctypes.CDLL:
+    """Load libtt.so once.  Raises if the CUDA library is missing."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise RuntimeError(
+                    f"libtt.so not found at {LIB_PATH}: build it with "
+                    "`python -m paper_2010_05680_b200.build` (there is no CPU fallback)")
+            L = ctypes.CDLL(LIB_PATH)
+            sm = [_vp, _vp, _i64, _i64, _i64, _i64, _f, _vp]
+            ln = [_vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _f, _vp]
+            for s in ("f32", "f16", "bf16"):
+                getattr(L, f"tt_softmax_masked_{s}").argtypes = sm
+                getattr(L, f"tt_add_bias_layernorm_{s}").argtypes = ln
+            L.tt_softmax_masked_staged.argtypes = [_i, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _i64,
+                                                   _f, _vp]
+            L.tt_add_bias_layernorm_staged.argtypes = [_i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
+                                                       _vp, _i64, _i64, _f, _vp]
+            L.tt_softmax_masked_plan.argtypes = [_i, _i64, _i64, _i64, _i64, ctypes.c_char_p, _i]
+            L.tt_add_bias_layernorm_plan.argtypes = [_i, _i64, _i64, ctypes.c_char_p, _i]
+            L.tt_status_string.argtypes = [_i]
+            L.tt_status_string.restype = ctypes.c_char_p
+            for name in EXPORTS:
+                if name != "tt_status_string":
+                    getattr(L, name).restype = _i
+            _lib = L
+    return _lib
+
+
+def status_string(s: int) -> str:
+    return lib().tt_status_string(int(s)).decode()
+
+
+def version() -> int:
+    return lib().tt_version()
+
+
+def _stream_ptr(stream) -> int:
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return int(stream.cuda_stream) if hasattr(stream, "cuda_stream") else int(stream)
+
+
+def _check(status: int, what: str):
+    if status != TT_SUCCESS:
+        raise TTError(status, what)
+
+
+def _dev(t: torch.Tensor, name: str):
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+
+
+# --------------------------------------------------------------------- softmax
+def tt_softmax_masked(scores: torch.Tensor, lengths: torch.Tensor, scale: float, stream=None):
+    """In place: scores[b,h,i,:] <- masked softmax (tt_softmax_masked_{f32,f16,bf16})."""
+    _dev(scores, "scores")
+    _dev(lengths, "lengths")
+    if scores.dim() != 4:
+        raise ValueError("scores must be [B, H, Sq, Sk]")
+    if lengths.dtype != torch.int32 or lengths.numel() != scores.shape[0]:
+        raise ValueError("lengths must be int32[B]")
+    B, H, Sq, Sk = scores.shape
+    fn = getattr(lib(), f"tt_softmax_masked_{_SUFFIX[scores.dtype]}")
+    _check(fn(scores.data_ptr(), lengths.data_ptr(), B, H, Sq, Sk, float(scale),
+              _stream_ptr(stream)), fn.__name__)
+    return scores
+
+
+def tt_softmax_masked_raw(dtype: torch.dtype, scores_ptr: int, lengths_ptr: int, B: int, H: int,
+                          Sq: int, Sk: int, scale: float, stream_ptr: int = 0) -> int:
+    """Pointer-level call; returns the tt_status (used by the ABI tests)."""
+    fn = getattr(lib(), f"tt_softmax_masked_{_SUFFIX[dtype]}")
+    return fn(scores_ptr, lengths_ptr, B, H, Sq, Sk, float(scale), stream_ptr)
+
+
+def tt_softmax_masked_staged(host_scores: torch.Tensor, host_lengths: torch.Tensor,
+                             dev_scores: torch.Tensor, dev_lengths: torch.Tensor, scale: float,
+                             stream=None):
+    """H2D copy, kernel, D2H copy on one stream (host buffers pinned)."""
+    _dev(dev_scores, "dev_scores")
+    _dev(dev_lengths, "dev_lengths")
+    if host_scores.is_cuda or host_lengths.is_cuda:
+        raise ValueError("host_* must be host tensors")
+    if host_scores.shape != dev_scores.shape or host_scores.dtype != dev_scores.dtype:
+        raise ValueError("host/device scores mismatch")
+    B, H, Sq, Sk = dev_scores.shape
+    _check(lib().tt_softmax_masked_staged(DTYPE_CODE[dev_scores.dtype], host_scores.data_ptr(),
+                                          host_lengths.data_ptr(), dev_scores.data_ptr(),
+                                          dev_lengths.data_ptr(), B, H, Sq, Sk, float(scale),
+                                          _stream_ptr(stream)), "tt_softmax_masked_staged")
+    return host_scores
+
+
+def softmax_plan(dtype: torch.dtype, B: int, H: int, Sq: int, Sk: int) -> str:
+    buf = ctypes.create_string_buffer(128)
+    _check(lib().tt_softmax_masked_plan(DTYPE_CODE[dtype], B, H, Sq, Sk, buf, 128),
+           "tt_softmax_masked_plan")
+    return buf.value.decode()
+
+
+# ------------------------------------------------------------------- layernorm
+def tt_add_bias_layernorm(out: torch.Tensor, x: torch.Tensor, residual: torch.Tensor,
+                          bias: torch.Tensor, gamma: torch.Tensor, beta: torch.Tensor,
+                          eps: float, stream=None):
+    """out <- LayerNorm((x + bias) + residual) * gamma + beta (tt_add_bias_layernorm_*)."""
+    for t, n in ((out, "out"), (x, "x"), (residual, "residual"), (bias, "bias"),
+                 (gamma, "gamma"), (beta, "beta")):
+        _dev(t, n)
+        if t.dtype != x.dtype:
+            raise ValueError("all operands share one dtype")
+    hidden = x.shape[-1]
+    rows = x.numel() // hidden if hidden else 0
+    if out.shape != x.shape or residual.shape != x.shape:
+        raise ValueError("out, x, residual must have the same shape")
+    if bias.numel() != hidden or gamma.numel() != hidden or beta.numel() != hidden:
+        raise ValueError("bias, gamma, beta must have `hidden` elements")
+    fn = getattr(lib(), f"tt_add_bias_layernorm_{_SUFFIX[x.dtype]}")
+    _check(fn(out.data_ptr(), x.data_ptr(), residual.data_ptr(), bias.data_ptr(),
+              gamma.data_ptr(), beta.data_ptr(), rows, hidden, float(eps), _stream_ptr(stream)),
+           fn.__name__)
+    return out
+
+
+def tt_add_bias_layernorm_raw(dtype: torch.dtype, out: int, x: int, residual: int, bias: int,
+                              gamma: int, beta: int, rows: int, hidden: int, eps: float,
+                              stream_ptr: int = 0) -> int:
+    fn = getattr(lib(), f"tt_add_bias_layernorm_{_SUFFIX[dtype]}")
+    return fn(out, x, residual, bias, gamma, beta, rows, hidden, float(eps), stream_ptr)
+
+
+def tt_add_bias_layernorm_staged(host_out, host_x, host_residual, dev_out, dev_x, dev_residual,
+                                 bias, gamma, beta, eps: float, stream=None):
+    for t, n in ((dev_out, "dev_out"), (dev_x, "dev_x"), (dev_residual, "dev_residual"),
+                 (bias, "bias"), (gamma, "gamma"), (beta, "beta")):
+        _dev(t, n)
+    hidden = dev_x.shape[-1]
+    rows = dev_x.numel() // hidden if hidden else 0
+    _check(lib().tt_add_bias_layernorm_staged(
+        DTYPE_CODE[dev_x.dtype], host_out.data_ptr(), host_x.data_ptr(), host_residual.data_ptr(),
+        dev_out.data_ptr(), dev_x.data_ptr(), dev_residual.data_ptr(), bias.data_ptr(),
+        gamma.data_ptr(), beta.data_ptr(), rows, hidden, float(eps), _stream_ptr(stream)),
+        "tt_add_bias_layernorm_staged")
+    return host_out
+
+
+def layernorm_plan(dtype: torch.dtype, rows: int, hidden: int) -> str:
+    buf = ctypes.create_string_buffer(128)
+    _check(lib().tt_add_bias_layernorm_plan(DTYPE_CODE[dtype], rows, hidden, buf, 128),
+           "tt_add_bias_layernorm_plan")
+    return buf.value.decode()

@@ -1,0 +1,274 @@
+// common.cuh -- vector I/O, dtype packing and group reductions shared by the
+// softmax and LayerNorm kernels (sm_100a only).
+//
+// Design: a "group" of G consecutive threads owns one row.
+//   G in {4, 8, 16, 32}  : sub-warp / warp groups, reductions are register
+//                          butterflies (SHFL.BFLY) or one CREDUX for the
+//                          warp-wide max -- no shared memory, no barrier.
+//   G in {64 .. 1024}    : a whole CTA owns one row (long rows); warp partials
+//                          go through shared memory with ONE barrier per batch
+//                          of R rows (the paper's "one synchronization for X
+//                          elements").
+// Each group processes R rows at once so independent loads, shuffles and
+// MUFU ops interleave (the paper's warpAllReduceSum_XElem ILP, l.374-383).
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <stdint.h>
+
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ != 1000)
+#error "libtt is written for sm_100a only (-gencode arch=compute_100a,code=sm_100a)"
+#endif
+
+namespace tt {
+
+// ----------------------------------------------------------------------------
+// Raw vectors of VB bytes (VB in {2, 4, 8, 16, 32}); 32-byte accesses compile
+// to LDG.E.256 / STG.E.256 on sm_100a.
+// ----------------------------------------------------------------------------
+template <int VB>
+struct Raw {
+    static constexpr int W = VB >= 4 ? VB / 4 : 1;
+    uint32_t w[W];
+};
+
+// Streaming load: bypass L1 (each byte is used once by one thread).
+template <int VB>
+__device__ __forceinline__ void ld_stream(const void* p, Raw<VB>& r) {
+    if constexpr (VB == 32) {
+        asm volatile(
+            "ld.global.L1::no_allocate.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+            : "=r"(r.w[0]), "=r"(r.w[1]), "=r"(r.w[2]), "=r"(r.w[3]), "=r"(r.w[4]),
+              "=r"(r.w[5]), "=r"(r.w[6]), "=r"(r.w[7])
+            : "l"(p));
+    } else if constexpr (VB == 16) {
+        asm volatile("ld.global.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(r.w[0]), "=r"(r.w[1]), "=r"(r.w[2]), "=r"(r.w[3])
+                     : "l"(p));
+    } else if constexpr (VB == 8) {
+        asm volatile("ld.global.L1::no_allocate.v2.u32 {%0,%1}, [%2];"
+                     : "=r"(r.w[0]), "=r"(r.w[1])
+                     : "l"(p));
+    } else if constexpr (VB == 4) {
+        asm volatile("ld.global.L1::no_allocate.u32 %0, [%1];" : "=r"(r.w[0]) : "l"(p));
+    } else {
+        static_assert(VB == 2, "VB");
+        unsigned short h;
+        asm volatile("ld.global.L1::no_allocate.u16 %0, [%1];" : "=h"(h) : "l"(p));
+        r.w[0] = h;
+    }
+}
+
+// Read-only parameter load (bias / gamma / beta): cached in L1, shared by all
+// rows of the CTA.  Caller guarantees no overlap with any written buffer.
+template <int VB>
+__device__ __forceinline__ void ld_param(const void* p, Raw<VB>& r) {
+    if constexpr (VB == 32) {
+        asm("ld.global.nc.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+            : "=r"(r.w[0]), "=r"(r.w[1]), "=r"(r.w[2]), "=r"(r.w[3]), "=r"(r.w[4]),
+              "=r"(r.w[5]), "=r"(r.w[6]), "=r"(r.w[7])
+            : "l"(p));
+    } else if constexpr (VB == 16) {
+        asm("ld.global.nc.v4.u32 {%0,%1,%2,%3}, [%4];"
+            : "=r"(r.w[0]), "=r"(r.w[1]), "=r"(r.w[2]), "=r"(r.w[3])
+            : "l"(p));
+    } else if constexpr (VB == 8) {
+        asm("ld.global.nc.v2.u32 {%0,%1}, [%2];" : "=r"(r.w[0]), "=r"(r.w[1]) : "l"(p));
+    } else if constexpr (VB == 4) {
+        asm("ld.global.nc.u32 %0, [%1];" : "=r"(r.w[0]) : "l"(p));
+    } else {
+        unsigned short h;
+        asm("ld.global.nc.u16 %0, [%1];" : "=h"(h) : "l"(p));
+        r.w[0] = h;
+    }
+}
+
+template <int VB>
+__device__ __forceinline__ void st_stream(void* p, const Raw<VB>& r) {
+    if constexpr (VB == 32) {
+        asm volatile(
+            "st.global.L1::no_allocate.v8.u32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p),
+            "r"(r.w[0]), "r"(r.w[1]), "r"(r.w[2]), "r"(r.w[3]), "r"(r.w[4]), "r"(r.w[5]),
+            "r"(r.w[6]), "r"(r.w[7])
+            : "memory");
+    } else if constexpr (VB == 16) {
+        asm volatile("st.global.L1::no_allocate.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p),
+                     "r"(r.w[0]), "r"(r.w[1]), "r"(r.w[2]), "r"(r.w[3])
+                     : "memory");
+    } else if constexpr (VB == 8) {
+        asm volatile("st.global.L1::no_allocate.v2.u32 [%0], {%1,%2};" ::"l"(p), "r"(r.w[0]),
+                     "r"(r.w[1])
+                     : "memory");
+    } else if constexpr (VB == 4) {
+        asm volatile("st.global.L1::no_allocate.u32 [%0], %1;" ::"l"(p), "r"(r.w[0]) : "memory");
+    } else {
+        unsigned short h = (unsigned short)r.w[0];
+        asm volatile("st.global.L1::no_allocate.u16 [%0], %1;" ::"l"(p), "h"(h) : "memory");
+    }
+}
+
+// ----------------------------------------------------------------------------
+// dtype <-> fp32.  Narrowing is round-to-nearest-even (DESIGN R12).
+// ----------------------------------------------------------------------------
+template <typename T>
+struct Elem;
+
+template <>
+struct Elem<float> {
+    static __device__ __forceinline__ float to_f(float v) { return v; }
+    static __device__ __forceinline__ float from_f(float v) { return v; }
+    template <int VB>
+    static __device__ __forceinline__ void unpack(const Raw<VB>& r, float* f) {
+#pragma unroll
+        for (int i = 0; i < VB / 4; ++i) f[i] = __uint_as_float(r.w[i]);
+    }
+    template <int VB>
+    static __device__ __forceinline__ void pack(const float* f, Raw<VB>& r) {
+#pragma unroll
+        for (int i = 0; i < VB / 4; ++i) r.w[i] = __float_as_uint(f[i]);
+    }
+};
+
+template <>
+struct Elem<__half> {
+    static __device__ __forceinline__ float to_f(__half v) { return __half2float(v); }
+    static __device__ __forceinline__ __half from_f(float v) { return __float2half_rn(v); }
+    template <int VB>
+    static __device__ __forceinline__ void unpack(const Raw<VB>& r, float* f) {
+        if constexpr (VB == 2) {
+            f[0] = __half2float(__ushort_as_half((unsigned short)r.w[0]));
+        } else {
+#pragma unroll
+            for (int i = 0; i < VB / 4; ++i) {
+                __half2 h = *reinterpret_cast<const __half2*>(&r.w[i]);
+                float2 t = __half22float2(h);
+                f[2 * i] = t.x;
+                f[2 * i + 1] = t.y;
+            }
+        }
+    }
+    template <int VB>
+    static __device__ __forceinline__ void pack(const float* f, Raw<VB>& r) {
+        if constexpr (VB == 2) {
+            r.w[0] = __half_as_ushort(__float2half_rn(f[0]));
+        } else {
+#pragma unroll
+            for (int i = 0; i < VB / 4; ++i) {
+                __half2 h = __floats2half2_rn(f[2 * i], f[2 * i + 1]);
+                r.w[i] = *reinterpret_cast<const uint32_t*>(&h);
+            }
+        }
+    }
+};
+
+template <>
+struct Elem<__nv_bfloat16> {
+    static __device__ __forceinline__ float to_f(__nv_bfloat16 v) { return __bfloat162float(v); }
+    static __device__ __forceinline__ __nv_bfloat16 from_f(float v) {
+        return __float2bfloat16_rn(v);
+    }
+    template <int VB>
+    static __device__ __forceinline__ void unpack(const Raw<VB>& r, float* f) {
+        if constexpr (VB == 2) {
+            f[0] = __uint_as_float(r.w[0] << 16);
+        } else {
+#pragma unroll
+            for (int i = 0; i < VB / 4; ++i) {
+                f[2 * i] = __uint_as_float(r.w[i] << 16);
+                f[2 * i + 1] = __uint_as_float(r.w[i] & 0xffff0000u);
+            }
+        }
+    }
+    template <int VB>
+    static __device__ __forceinline__ void pack(const float* f, Raw<VB>& r) {
+        if constexpr (VB == 2) {
+            r.w[0] = __bfloat16_as_ushort(__float2bfloat16_rn(f[0]));
+        } else {
+#pragma unroll
+            for (int i = 0; i < VB / 4; ++i) {
+                __nv_bfloat162 h = __floats2bfloat162_rn(f[2 * i], f[2 * i + 1]);
+                r.w[i] = *reinterpret_cast<const uint32_t*>(&h);
+            }
+        }
+    }
+};
+
+// ----------------------------------------------------------------------------
+// Scalar helpers
+// ----------------------------------------------------------------------------
+__device__ __forceinline__ float ex2_approx(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+// Warp-wide f32 max in one instruction (CREDUX.MAX.F32.NAN, sm_100a only).
+__device__ __forceinline__ float warp_max_redux(float v) {
+    float m;
+    asm volatile("redux.sync.max.NaN.f32 %0, %1, 0xffffffff;" : "=f"(m) : "f"(v));
+    return m;
+}
+
+// ----------------------------------------------------------------------------
+// Group all-reduce of R independent values (one per row in flight).
+// For G <= 32 the whole group is inside one warp; for G > 32 the group is the
+// CTA and `smem` must hold R * (G / 32) floats (distinct buffer per call site).
+// ----------------------------------------------------------------------------
+template <int G, int R>
+__device__ __forceinline__ void group_max(float (&v)[R], float* smem) {
+    if constexpr (G >= 32) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) v[r] = warp_max_redux(v[r]);
+    } else {
+#pragma unroll
+        for (int o = G / 2; o > 0; o >>= 1) {
+#pragma unroll
+            for (int r = 0; r < R; ++r) v[r] = fmaxf(v[r], __shfl_xor_sync(0xffffffffu, v[r], o));
+        }
+    }
+    if constexpr (G > 32) {
+        constexpr int NW = G / 32;
+        const int warp = threadIdx.x >> 5;
+        if ((threadIdx.x & 31) == 0) {
+#pragma unroll
+            for (int r = 0; r < R; ++r) smem[r * NW + warp] = v[r];
+        }
+        __syncthreads();
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            float m = smem[r * NW];
+#pragma unroll
+            for (int w = 1; w < NW; ++w) m = fmaxf(m, smem[r * NW + w]);
+            v[r] = m;
+        }
+    }
+}
+
+template <int G, int R>
+__device__ __forceinline__ void group_sum(float (&v)[R], float* smem) {
+    constexpr int GW = G < 32 ? G : 32;
+#pragma unroll
+    for (int o = GW / 2; o > 0; o >>= 1) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) v[r] += __shfl_xor_sync(0xffffffffu, v[r], o);
+    }
+    if constexpr (G > 32) {
+        constexpr int NW = G / 32;
+        const int warp = threadIdx.x >> 5;
+        if ((threadIdx.x & 31) == 0) {
+#pragma unroll
+            for (int r = 0; r < R; ++r) smem[r * NW + warp] = v[r];
+        }
+        __syncthreads();
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            float s = 0.f;
+#pragma unroll
+            for (int w = 0; w < NW; ++w) s += smem[r * NW + w];
+            v[r] = s;
+        }
+    }
+}
+
+}  // namespace tt

@@ -1,0 +1,25 @@
+// launch.h -- internal interface between the C ABI (tt_api.cu) and the kernel
+// translation units.  Not installed; the public contract is include/tt.h.
+#pragma once
+
+#include <cuda_runtime_api.h>
+#include <stdint.h>
+
+namespace tt {
+
+// dtype codes: 0 = fp32, 1 = fp16, 2 = bf16.
+// *supported is set false (and nothing launched) when no tier fits.
+cudaError_t softmax_launch(int dtype, void* scores, const int32_t* lengths, int64_t nrows,
+                           int64_t rows_per_batch, int64_t Sk, float scale, cudaStream_t stream,
+                           bool* supported);
+const char* softmax_tier_name(int dtype, int64_t Sk);
+
+// vec_bytes: widest vector width (bytes) that every operand's alignment and
+// the row pitch allow (host-computed in tt_api.cu).
+cudaError_t layernorm_launch(int dtype, void* out, const void* x, const void* residual,
+                             const void* bias, const void* gamma, const void* beta, int64_t rows,
+                             int64_t hidden, float eps, int vec_bytes, cudaStream_t stream,
+                             bool* supported);
+const char* layernorm_tier_name(int dtype, int64_t hidden, int vec_bytes);
+
+}  // namespace tt

@@ -1,0 +1,233 @@
+// layernorm.cu -- fused add-bias + residual + LayerNorm over [rows, hidden]
+// (TurboTransformers' AddBiasLayerNorm; fusion of everything
+// between two GEMMs, l.302; LayerNorm "calculates the mean and variance",
+// l.316; variance per Eq. 1 l.406-409).
+//
+// One group of G threads owns one row:
+//   LN-1  v_k = (x_k + bias_k) + residual_k in fp32, held in registers
+//   LN-2  mean = sum(v) / N, then var = sum((v - mean)^2) / N: two register
+//         butterflies over the SAME registers (one extra shuffle round, zero
+//         extra HBM bytes).  The paper's one-pass E(x^2) - E(x)^2 (Eq. 1 RHS)
+//         saves that round but loses ~3 digits in fp32 when |mean| >> std
+//         (DESIGN R9, offset test), so it is not used.
+//   LN-3  y_k = (v_k - mean) * rsqrt(var + eps) * gamma_k + beta_k, RNE
+//         narrowing, vector store.  `out` may alias x or residual exactly:
+//         every element of a row is loaded before any element is stored.
+#include "common.cuh"
+#include "launch.h"
+
+namespace tt {
+
+template <typename T, int VB, int G, int NV, int R, int NT>
+__global__ void __launch_bounds__(NT)
+    ln_rows_kernel(T* out, const T* x, const T* residual, const T* __restrict__ bias,
+                   const T* __restrict__ gamma, const T* __restrict__ beta, int64_t rows,
+                   int hidden, float eps) {
+    constexpr int VE = VB / (int)sizeof(T);
+    constexpr int GPB = NT / G;
+    constexpr int NWG = G > 32 ? G / 32 : 1;
+    __shared__ float red_a[G > 32 ? R * NWG : 1];
+    __shared__ float red_b[G > 32 ? R * NWG : 1];
+
+    const int q = threadIdx.x % G;
+    const int gi = threadIdx.x / G;
+    const int64_t base = (int64_t)blockIdx.x * GPB * R;
+    const int nvec = hidden / VE;
+    const float invN = 1.0f / (float)hidden;
+
+    int64_t off[R];
+    bool live[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int64_t row = base + (int64_t)r * GPB + gi;
+        live[r] = row < rows;
+        off[r] = (live[r] ? row : 0) * (int64_t)hidden;
+    }
+
+    // ---- LN-1: v = (x + bias) + residual
+    float v[R][NV][VE];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+#pragma unroll
+        for (int k = 0; k < NV; ++k) {
+            const int vi = q + k * G;
+            if (live[r] && vi < nvec) {
+                Raw<VB> wx, wr;
+                ld_stream<VB>(x + off[r] + vi * VE, wx);
+                ld_stream<VB>(residual + off[r] + vi * VE, wr);
+                float fr[VE];
+                Elem<T>::template unpack<VB>(wx, v[r][k]);
+                Elem<T>::template unpack<VB>(wr, fr);
+                Raw<VB> wb;
+                ld_param<VB>(bias + vi * VE, wb);
+                float fb[VE];
+                Elem<T>::template unpack<VB>(wb, fb);
+#pragma unroll
+                for (int e = 0; e < VE; ++e) v[r][k][e] = (v[r][k][e] + fb[e]) + fr[e];
+            } else {
+#pragma unroll
+                for (int e = 0; e < VE; ++e) v[r][k][e] = 0.f;
+            }
+        }
+    }
+
+    // ---- LN-2: mean, then centred second moment
+    float mean[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        float a = 0.f;
+#pragma unroll
+        for (int k = 0; k < NV; ++k)
+#pragma unroll
+            for (int e = 0; e < VE; ++e) a += v[r][k][e];
+        mean[r] = a;
+    }
+    group_sum<G, R>(mean, red_a);
+    float var[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        mean[r] *= invN;
+        float a = 0.f;
+#pragma unroll
+        for (int k = 0; k < NV; ++k) {
+            const int vi = q + k * G;
+            if (vi < nvec) {
+#pragma unroll
+                for (int e = 0; e < VE; ++e) {
+                    const float d = v[r][k][e] - mean[r];
+                    a = fmaf(d, d, a);
+                }
+            }
+        }
+        var[r] = a;
+    }
+    group_sum<G, R>(var, red_b);
+
+    // ---- LN-3: normalise, affine, store
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        if (!live[r]) continue;
+        const float rstd = rsqrtf(var[r] * invN + eps);
+#pragma unroll
+        for (int k = 0; k < NV; ++k) {
+            const int vi = q + k * G;
+            if (vi < nvec) {
+                Raw<VB> wg, wb;
+                ld_param<VB>(gamma + vi * VE, wg);
+                ld_param<VB>(beta + vi * VE, wb);
+                float fg[VE], fb[VE], y[VE];
+                Elem<T>::template unpack<VB>(wg, fg);
+                Elem<T>::template unpack<VB>(wb, fb);
+#pragma unroll
+                for (int e = 0; e < VE; ++e) y[e] = fmaf((v[r][k][e] - mean[r]) * rstd, fg[e], fb[e]);
+                Raw<VB> wy;
+                Elem<T>::template pack<VB>(y, wy);
+                st_stream<VB>(out + off[r] + vi * VE, wy);
+            }
+        }
+    }
+}
+
+namespace {
+
+template <typename T, int VB, int G, int NV, int R, int NT>
+cudaError_t launch_ln(void* out, const void* x, const void* res, const void* bias,
+                      const void* gamma, const void* beta, int64_t rows, int hidden, float eps,
+                      cudaStream_t st) {
+    constexpr int GPB = NT / G;
+    const int64_t rows_per_cta = (int64_t)GPB * R;
+    const int64_t grid = (rows + rows_per_cta - 1) / rows_per_cta;
+    if (grid > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
+    ln_rows_kernel<T, VB, G, NV, R, NT><<<(unsigned)grid, NT, 0, st>>>(
+        static_cast<T*>(out), static_cast<const T*>(x), static_cast<const T*>(res),
+        static_cast<const T*>(bias), static_cast<const T*>(gamma), static_cast<const T*>(beta),
+        rows, hidden, eps);
+    return cudaGetLastError();
+}
+
+using LnFn = cudaError_t (*)(void*, const void*, const void*, const void*, const void*,
+                             const void*, int64_t, int, float, cudaStream_t);
+
+struct LnTier {
+    int vb;        // vector bytes
+    int ve;        // elements per vector
+    int capacity;  // G * NV * VE: largest hidden
+    LnFn fn;
+    const char* name;
+};
+
+#define TT_LN_TIER(T, TN, VB, G, NV, R, NT)                                                \
+    LnTier {                                                                               \
+        VB, (VB) / (int)sizeof(T), (G) * (NV) * ((VB) / (int)sizeof(T)),                   \
+            &launch_ln<T, VB, G, NV, R, NT>,                                               \
+            "ln_rows<" TN ",V" #VB ",G" #G ",NV" #NV ",R" #R ",T" #NT ">"                 \
+    }
+
+// Main tiers use 16- or 32-byte vectors; the scalar tiers (VB = sizeof(T))
+// only serve hidden sizes whose row pitch is not a multiple of 16 bytes.
+// NVC = CTA-tier vectors per thread (NV * VE = 32 registers of row data);
+// NVS = scalar CTA tier (VE = 1).
+#define TT_LN_TABLE(T, TN, SB, NVC32, NVC16)                                               \
+    static const LnTier kLn_##TN[] = {                                                     \
+        TT_LN_TIER(T, #TN, 16, 4, 1, 2, 256),   TT_LN_TIER(T, #TN, 16, 8, 1, 2, 256),       \
+        TT_LN_TIER(T, #TN, 16, 16, 1, 2, 256),  TT_LN_TIER(T, #TN, 16, 32, 1, 2, 256),      \
+        TT_LN_TIER(T, #TN, 16, 32, 2, 2, 256),  TT_LN_TIER(T, #TN, 16, 32, 3, 1, 256),      \
+        TT_LN_TIER(T, #TN, 16, 32, 4, 1, 256),  TT_LN_TIER(T, #TN, 16, 32, 6, 1, 256),      \
+        TT_LN_TIER(T, #TN, 16, 32, 8, 1, 256),  TT_LN_TIER(T, #TN, 32, 4, 1, 2, 256),       \
+        TT_LN_TIER(T, #TN, 32, 8, 1, 2, 256),   TT_LN_TIER(T, #TN, 32, 16, 1, 2, 256),      \
+        TT_LN_TIER(T, #TN, 32, 32, 1, 2, 256),  TT_LN_TIER(T, #TN, 32, 32, 2, 1, 256),      \
+        TT_LN_TIER(T, #TN, 32, 32, 3, 1, 256),  TT_LN_TIER(T, #TN, 32, 32, 4, 1, 256),      \
+        TT_LN_TIER(T, #TN, 16, 128, NVC16, 1, 128), TT_LN_TIER(T, #TN, 16, 256, NVC16, 1, 256), \
+        TT_LN_TIER(T, #TN, 16, 512, NVC16, 1, 512), TT_LN_TIER(T, #TN, 16, 1024, NVC16, 1, 1024), \
+        TT_LN_TIER(T, #TN, 32, 128, NVC32, 1, 128), TT_LN_TIER(T, #TN, 32, 256, NVC32, 1, 256), \
+        TT_LN_TIER(T, #TN, 32, 512, NVC32, 1, 512), TT_LN_TIER(T, #TN, 32, 1024, NVC32, 1, 1024), \
+        TT_LN_TIER(T, #TN, SB, 32, 1, 1, 256),  TT_LN_TIER(T, #TN, SB, 32, 4, 1, 256),      \
+        TT_LN_TIER(T, #TN, SB, 32, 16, 1, 256), TT_LN_TIER(T, #TN, SB, 256, 16, 1, 256),    \
+        TT_LN_TIER(T, #TN, SB, 1024, 32, 1, 1024),                                         \
+    };
+
+TT_LN_TABLE(float, f32, 4, 4, 8)
+TT_LN_TABLE(__half, f16, 2, 2, 4)
+TT_LN_TABLE(__nv_bfloat16, bf16, 2, 2, 4)
+
+template <size_t N>
+const LnTier* pick_from(const LnTier (&tab)[N], int64_t hidden, int vec_bytes) {
+    const LnTier* best = nullptr;
+    for (size_t i = 0; i < N; ++i) {
+        const LnTier& t = tab[i];
+        if (t.vb > vec_bytes || hidden % t.ve != 0 || hidden > t.capacity) continue;
+        // least padding first (fewest idle lanes), then the widest vector
+        if (!best || t.capacity < best->capacity ||
+            (t.capacity == best->capacity && t.vb > best->vb))
+            best = &t;
+    }
+    return best;
+}
+
+const LnTier* pick_dtype(int dtype, int64_t hidden, int vec_bytes) {
+    switch (dtype) {
+        case 0: return pick_from(kLn_f32, hidden, vec_bytes);
+        case 1: return pick_from(kLn_f16, hidden, vec_bytes);
+        case 2: return pick_from(kLn_bf16, hidden, vec_bytes);
+        default: return nullptr;
+    }
+}
+
+}  // namespace
+
+const char* layernorm_tier_name(int dtype, int64_t hidden, int vec_bytes) {
+    const LnTier* t = pick_dtype(dtype, hidden, vec_bytes);
+    return t ? t->name : nullptr;
+}
+
+cudaError_t layernorm_launch(int dtype, void* out, const void* x, const void* residual,
+                             const void* bias, const void* gamma, const void* beta, int64_t rows,
+                             int64_t hidden, float eps, int vec_bytes, cudaStream_t stream,
+                             bool* supported) {
+    const LnTier* t = pick_dtype(dtype, hidden, vec_bytes);
+    *supported = t != nullptr;
+    if (!t) return cudaSuccess;
+    return t->fn(out, x, residual, bias, gamma, beta, rows, (int)hidden, eps, stream);
+}
+
+}  // namespace tt

@@ -1,0 +1,253 @@
+// softmax.cu -- in-place masked attention softmax over [B, H, Sq, Sk]
+// (TurboTransformers' ApplyMaskAndSoftmax; batch reduction
+// "Softmax calculates summation and maximum", §4.1.2 l.316).
+//
+// One group of G threads owns one row:
+//   SM-1  b = row / (H*Sq);  L = clamp(lengths[b], 0, Sk)
+//   SM-2  vector-load the valid prefix j < L only (masked bytes never read),
+//         t_j = x_j * (scale * log2 e) in fp32
+//   SM-3  m = max t_j   (per-lane max, then CREDUX / butterfly / CTA merge)
+//   SM-4  e_j = 2^(t_j - m) computed ONCE and kept in registers; s = sum e_j
+//   SM-5  y_j = e_j / s for j < L, +0.0 for L <= j < Sk; RNE narrow; vector store
+// Every element is read at most once and written exactly once: the row lives
+// in registers between the load and the store, so no smem staging or online
+// (m, s) rescaling is needed up to TT_MAX_SOFTMAX_COLS (CTA tier).
+//
+// Rows of any length: a row starts at an arbitrary element offset, so each row
+// is split into an unaligned head (< VE elements, scalar), an aligned body of
+// VB-byte vectors and a tail (< VE elements, scalar).
+#include "common.cuh"
+#include "launch.h"
+
+namespace tt {
+
+constexpr float kLog2e = 1.4426950408889634f;
+
+template <typename T, int VB, int G, int NV, int R, int NT>
+__global__ void __launch_bounds__(NT) softmax_rows_kernel(T* __restrict__ scores,
+                                                          const int32_t* __restrict__ lengths,
+                                                          int64_t nrows, int64_t rows_per_batch,
+                                                          int Sk, float c) {
+    constexpr int VE = VB / (int)sizeof(T);          // elements per vector
+    constexpr int HI = (VE - 1 + G - 1) / G;         // head / tail iterations per lane
+    constexpr int GPB = NT / G;                      // groups per CTA
+    constexpr int NWG = G > 32 ? G / 32 : 1;         // warps per group (CTA tier)
+    __shared__ float red_max[G > 32 ? R * NWG : 1];
+    __shared__ float red_sum[G > 32 ? R * NWG : 1];
+
+    const int q = threadIdx.x % G;
+    const int gi = threadIdx.x / G;
+    const int64_t base = (int64_t)blockIdx.x * GPB * R;
+
+    T* p[R];
+    int Lr[R], hd[R], nv[R];
+    bool live[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int64_t row = base + (int64_t)r * GPB + gi;
+        live[r] = row < nrows;
+        const int64_t rr = live[r] ? row : 0;
+        p[r] = scores + rr * (int64_t)Sk;
+        const int mis = (int)((reinterpret_cast<uintptr_t>(p[r]) & (VB - 1)) / sizeof(T));
+        hd[r] = mis ? min(VE - mis, Sk) : 0;
+        nv[r] = (Sk - hd[r]) / VE;
+        int L = live[r] ? __ldg(lengths + rr / rows_per_batch) : 0;
+        Lr[r] = min(max(L, 0), Sk);
+    }
+
+    // ---- SM-2: load the valid prefix, scaled into the log2 domain
+    float v[R][NV][VE];
+    float hv[R][HI], tv[R][HI];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+#pragma unroll
+        for (int k = 0; k < NV; ++k) {
+            const int vi = q + k * G;
+            const int j0 = hd[r] + vi * VE;
+            if (vi < nv[r] && j0 < Lr[r]) {
+                Raw<VB> w;
+                ld_stream<VB>(p[r] + j0, w);
+                Elem<T>::template unpack<VB>(w, v[r][k]);
+#pragma unroll
+                for (int e = 0; e < VE; ++e)
+                    v[r][k][e] = (j0 + e < Lr[r]) ? v[r][k][e] * c : -INFINITY;
+            } else {
+#pragma unroll
+                for (int e = 0; e < VE; ++e) v[r][k][e] = -INFINITY;
+            }
+        }
+        const int tl0 = hd[r] + nv[r] * VE;
+#pragma unroll
+        for (int i = 0; i < HI; ++i) {
+            const int jh = q + i * G;
+            hv[r][i] = (jh < hd[r] && jh < Lr[r]) ? Elem<T>::to_f(p[r][jh]) * c : -INFINITY;
+            const int jt = tl0 + q + i * G;
+            tv[r][i] = (jt < Sk && jt < Lr[r]) ? Elem<T>::to_f(p[r][jt]) * c : -INFINITY;
+        }
+    }
+
+    // ---- SM-3: row max
+    float m[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        float a = -INFINITY;
+#pragma unroll
+        for (int k = 0; k < NV; ++k)
+#pragma unroll
+            for (int e = 0; e < VE; ++e) a = fmaxf(a, v[r][k][e]);
+#pragma unroll
+        for (int i = 0; i < HI; ++i) a = fmaxf(a, fmaxf(hv[r][i], tv[r][i]));
+        m[r] = a;
+    }
+    group_max<G, R>(m, red_max);
+
+    // ---- SM-4: exponentiate once, sum
+    float s[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const float mm = (m[r] == -INFINITY) ? 0.f : m[r];  // empty row: keep e = 0
+        float a = 0.f;
+#pragma unroll
+        for (int k = 0; k < NV; ++k)
+#pragma unroll
+            for (int e = 0; e < VE; ++e) {
+                v[r][k][e] = ex2_approx(v[r][k][e] - mm);
+                a += v[r][k][e];
+            }
+#pragma unroll
+        for (int i = 0; i < HI; ++i) {
+            hv[r][i] = ex2_approx(hv[r][i] - mm);
+            tv[r][i] = ex2_approx(tv[r][i] - mm);
+            a += hv[r][i] + tv[r][i];
+        }
+        s[r] = a;
+    }
+    group_sum<G, R>(s, red_sum);
+
+    // ---- SM-5: normalise valid keys, +0.0 for padding keys, store every column
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        if (!live[r]) continue;
+        const float inv = 1.0f / s[r];
+#pragma unroll
+        for (int k = 0; k < NV; ++k) {
+            const int vi = q + k * G;
+            if (vi < nv[r]) {
+                const int j0 = hd[r] + vi * VE;
+                float y[VE];
+#pragma unroll
+                for (int e = 0; e < VE; ++e) y[e] = (j0 + e < Lr[r]) ? v[r][k][e] * inv : 0.f;
+                Raw<VB> w;
+                Elem<T>::template pack<VB>(y, w);
+                st_stream<VB>(p[r] + j0, w);
+            }
+        }
+        const int tl0 = hd[r] + nv[r] * VE;
+#pragma unroll
+        for (int i = 0; i < HI; ++i) {
+            const int jh = q + i * G;
+            if (jh < hd[r]) p[r][jh] = Elem<T>::from_f(jh < Lr[r] ? hv[r][i] * inv : 0.f);
+            const int jt = tl0 + q + i * G;
+            if (jt < Sk) p[r][jt] = Elem<T>::from_f(jt < Lr[r] ? tv[r][i] * inv : 0.f);
+        }
+    }
+}
+
+// ----------------------------------------------------------------------------
+// Tier table.  Selection is by (dtype, Sk) only; per-row lengths only shorten
+// the reads.  See DESIGN.md §5 for the choice of each entry.
+// ----------------------------------------------------------------------------
+namespace {
+
+template <typename T, int VB, int G, int NV, int R, int NT>
+cudaError_t launch_softmax(void* scores, const int32_t* lengths, int64_t nrows, int64_t rpb,
+                           int Sk, float scale, cudaStream_t st) {
+    constexpr int GPB = NT / G;
+    const int64_t rows_per_cta = (int64_t)GPB * R;
+    const int64_t grid = (nrows + rows_per_cta - 1) / rows_per_cta;
+    if (grid > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
+    softmax_rows_kernel<T, VB, G, NV, R, NT><<<(unsigned)grid, NT, 0, st>>>(
+        static_cast<T*>(scores), lengths, nrows, rpb, Sk, scale * kLog2e);
+    return cudaGetLastError();
+}
+
+using SoftmaxFn = cudaError_t (*)(void*, const int32_t*, int64_t, int64_t, int, float,
+                                  cudaStream_t);
+
+struct SoftmaxTier {
+    int max_cols;  // largest Sk this tier handles for its dtype
+    SoftmaxFn fn;
+    const char* name;
+};
+
+#define TT_SM_TIER(T, TN, VB, G, NV, R, NT)                                                 \
+    SoftmaxTier {                                                                           \
+        (G) * (NV) * ((VB) / (int)sizeof(T)), &launch_softmax<T, VB, G, NV, R, NT>,        \
+            "softmax_rows<" TN ",V" #VB ",G" #G ",NV" #NV ",R" #R ",T" #NT ">"            \
+    }
+
+// Ordered by max_cols; the first tier that fits is used.  Short rows use
+// 16-byte vectors so that more lanes carry bytes; rows of >= 256 B use
+// 32-byte vectors (LDG.256).  Sub-warp groups handle many short rows per
+// warp; R = 2 rows per group in flight doubles the memory-level parallelism.
+template <typename T>
+struct SoftmaxTable;
+
+#define TT_SM_TABLE(T, TN, NVC)                                                             \
+    template <>                                                                             \
+    struct SoftmaxTable<T> {                                                                \
+        static constexpr int N = 13;                                                        \
+        static const SoftmaxTier* tiers() {                                                 \
+            static const SoftmaxTier t[N] = {                                               \
+                TT_SM_TIER(T, TN, 16, 4, 1, 2, 256),     TT_SM_TIER(T, TN, 16, 8, 1, 2, 256),  \
+                TT_SM_TIER(T, TN, 16, 16, 1, 2, 256),    TT_SM_TIER(T, TN, 32, 16, 1, 2, 256), \
+                TT_SM_TIER(T, TN, 32, 32, 1, 2, 256),    TT_SM_TIER(T, TN, 32, 32, 2, 1, 256), \
+                TT_SM_TIER(T, TN, 32, 32, 3, 1, 256),    TT_SM_TIER(T, TN, 32, 32, 4, 1, 256), \
+                TT_SM_TIER(T, TN, 32, 64, NVC, 1, 64),   TT_SM_TIER(T, TN, 32, 128, NVC, 1, 128), \
+                TT_SM_TIER(T, TN, 32, 256, NVC, 1, 256), TT_SM_TIER(T, TN, 32, 512, NVC, 1, 512), \
+                TT_SM_TIER(T, TN, 32, 1024, NVC, 1, 1024),                                 \
+            };                                                                              \
+            return t;                                                                       \
+        }                                                                                   \
+    };
+
+// CTA tiers keep NV * VE = 32 fp32 registers of row data per thread so that a
+// 1024-thread CTA fits the 64-register limit: NVC = 4 (fp32) or 2 (16-bit).
+TT_SM_TABLE(float, "f32", 4)
+TT_SM_TABLE(__half, "f16", 2)
+TT_SM_TABLE(__nv_bfloat16, "bf16", 2)
+
+template <typename T>
+const SoftmaxTier* pick(int64_t Sk) {
+    const SoftmaxTier* t = SoftmaxTable<T>::tiers();
+    for (int i = 0; i < SoftmaxTable<T>::N; ++i)
+        if (Sk <= t[i].max_cols) return &t[i];
+    return nullptr;
+}
+
+const SoftmaxTier* pick_dtype(int dtype, int64_t Sk) {
+    switch (dtype) {
+        case 0: return pick<float>(Sk);
+        case 1: return pick<__half>(Sk);
+        case 2: return pick<__nv_bfloat16>(Sk);
+        default: return nullptr;
+    }
+}
+
+}  // namespace
+
+const char* softmax_tier_name(int dtype, int64_t Sk) {
+    const SoftmaxTier* t = pick_dtype(dtype, Sk);
+    return t ? t->name : nullptr;
+}
+
+cudaError_t softmax_launch(int dtype, void* scores, const int32_t* lengths, int64_t nrows,
+                           int64_t rows_per_batch, int64_t Sk, float scale, cudaStream_t stream,
+                           bool* supported) {
+    const SoftmaxTier* t = pick_dtype(dtype, Sk);
+    *supported = t != nullptr;
+    if (!t) return cudaSuccess;
+    return t->fn(scores, lengths, nrows, rows_per_batch, (int)Sk, scale, stream);
+}
+
+}  // namespace tt

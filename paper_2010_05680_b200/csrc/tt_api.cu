@@ -1,0 +1,268 @@
+// tt_api.cu -- the C ABI of libtt.so (contract: include/tt.h).
+//
+// Host-side validation happens before any CUDA call; the kernels themselves
+// live in softmax.cu / layernorm.cu.  No allocation, no synchronisation, no
+// global state beyond a thread-local last-error slot.
+#include <math.h>
+#include <stdio.h>
+#include <string.h>
+
+#include "../../include/tt.h"
+#include "launch.h"
+
+namespace {
+
+thread_local int g_last_cuda_error = 0;
+
+constexpr int kVersion = 1 * 10000 + 0 * 100 + 0;
+
+int elem_bytes(int dtype) { return dtype == 0 ? 4 : 2; }
+
+bool mul_overflows(int64_t a, int64_t b, int64_t* out) {
+    __int128 p = (__int128)a * (__int128)b;
+    if (p > (__int128)INT64_MAX) return true;
+    *out = (int64_t)p;
+    return false;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+tt_status cuda_status(cudaError_t e) {
+    if (e == cudaSuccess) return TT_SUCCESS;
+    g_last_cuda_error = (int)e;
+    return TT_ERROR_CUDA;
+}
+
+// Byte ranges [a, a+n) and [b, b+m) overlap?
+bool overlaps(const void* a, int64_t n, const void* b, int64_t m) {
+    const uintptr_t pa = reinterpret_cast<uintptr_t>(a), pb = reinterpret_cast<uintptr_t>(b);
+    return pa < pb + (uintptr_t)m && pb < pa + (uintptr_t)n;
+}
+
+// ------------------------------------------------------------------ softmax
+tt_status softmax_validate(int dtype, const void* scores, const int32_t* lengths, int64_t B,
+                           int64_t H, int64_t Sq, int64_t Sk, float scale, bool check_ptrs,
+                           int64_t* nrows_out, bool* empty) {
+    if (dtype < 0 || dtype > 2) return TT_ERROR_INVALID_VALUE;
+    if (B < 0 || H < 0 || Sq < 0 || Sk < 0) return TT_ERROR_INVALID_VALUE;
+    if (!isfinite(scale)) return TT_ERROR_INVALID_VALUE;
+    int64_t bh, nrows, n;
+    if (mul_overflows(B, H, &bh) || mul_overflows(bh, Sq, &nrows) || mul_overflows(nrows, Sk, &n) ||
+        mul_overflows(n, elem_bytes(dtype), &n))
+        return TT_ERROR_INVALID_VALUE;
+    *nrows_out = nrows;
+    *empty = (nrows == 0 || Sk == 0);
+    if (*empty) return TT_SUCCESS;
+    if (check_ptrs) {
+        if (!scores || !lengths) return TT_ERROR_INVALID_VALUE;
+        if (!aligned16(scores) || (reinterpret_cast<uintptr_t>(lengths) & 3u))
+            return TT_ERROR_NOT_SUPPORTED;
+    }
+    if (Sk > TT_MAX_SOFTMAX_COLS) return TT_ERROR_NOT_SUPPORTED;
+    return TT_SUCCESS;
+}
+
+tt_status softmax_any(int dtype, void* scores, const int32_t* lengths, int64_t B, int64_t H,
+                      int64_t Sq, int64_t Sk, float scale, cudaStream_t stream) {
+    int64_t nrows = 0;
+    bool empty = false;
+    tt_status s = softmax_validate(dtype, scores, lengths, B, H, Sq, Sk, scale, true, &nrows, &empty);
+    if (s != TT_SUCCESS || empty) return s;
+    bool supported = false;
+    cudaError_t e = tt::softmax_launch(dtype, scores, lengths, nrows, H * Sq, Sk, scale, stream,
+                                       &supported);
+    if (!supported) return TT_ERROR_NOT_SUPPORTED;
+    return cuda_status(e);
+}
+
+// ---------------------------------------------------------------- layernorm
+int ln_vec_bytes(int dtype, int64_t hidden, const void* const* ptrs, int nptrs) {
+    const int e = elem_bytes(dtype);
+    for (int vb = 32; vb >= e; vb >>= 1) {
+        if ((hidden * e) % vb) continue;
+        bool ok = true;
+        for (int i = 0; i < nptrs; ++i)
+            if (reinterpret_cast<uintptr_t>(ptrs[i]) % (uintptr_t)vb) ok = false;
+        if (ok) return vb;
+    }
+    return e;
+}
+
+tt_status ln_validate(int dtype, const void* out, const void* x, const void* residual,
+                      const void* bias, const void* gamma, const void* beta, int64_t rows,
+                      int64_t hidden, float eps, bool check_ptrs, bool* empty) {
+    if (dtype < 0 || dtype > 2) return TT_ERROR_INVALID_VALUE;
+    if (rows < 0 || hidden < 0) return TT_ERROR_INVALID_VALUE;
+    if (!isfinite(eps) || eps < 0.f) return TT_ERROR_INVALID_VALUE;
+    int64_t n, nb;
+    if (mul_overflows(rows, hidden, &n) || mul_overflows(n, elem_bytes(dtype), &nb))
+        return TT_ERROR_INVALID_VALUE;
+    *empty = (n == 0);
+    if (*empty) return TT_SUCCESS;
+    if (check_ptrs) {
+        const void* ps[6] = {out, x, residual, bias, gamma, beta};
+        for (const void* p : ps)
+            if (!p) return TT_ERROR_INVALID_VALUE;
+        // out may alias x or residual exactly; any partial overlap is rejected,
+        // and the read-only parameters must not overlap anything written.
+        const int64_t pb = hidden * elem_bytes(dtype);
+        if (out != x && overlaps(out, nb, x, nb)) return TT_ERROR_INVALID_VALUE;
+        if (out != residual && overlaps(out, nb, residual, nb)) return TT_ERROR_INVALID_VALUE;
+        const void* params[3] = {bias, gamma, beta};
+        for (const void* p : params)
+            if (overlaps(out, nb, p, pb)) return TT_ERROR_INVALID_VALUE;
+        for (const void* p : ps)
+            if (!aligned16(p)) return TT_ERROR_NOT_SUPPORTED;
+    }
+    if (hidden > TT_MAX_LN_HIDDEN) return TT_ERROR_NOT_SUPPORTED;
+    return TT_SUCCESS;
+}
+
+tt_status ln_any(int dtype, void* out, const void* x, const void* residual, const void* bias,
+                 const void* gamma, const void* beta, int64_t rows, int64_t hidden, float eps,
+                 cudaStream_t stream) {
+    bool empty = false;
+    tt_status s = ln_validate(dtype, out, x, residual, bias, gamma, beta, rows, hidden, eps, true,
+                              &empty);
+    if (s != TT_SUCCESS || empty) return s;
+    const void* ps[6] = {out, x, residual, bias, gamma, beta};
+    const int vb = ln_vec_bytes(dtype, hidden, ps, 6);
+    bool supported = false;
+    cudaError_t e = tt::layernorm_launch(dtype, out, x, residual, bias, gamma, beta, rows, hidden,
+                                         eps, vb, stream, &supported);
+    if (!supported) return TT_ERROR_NOT_SUPPORTED;
+    return cuda_status(e);
+}
+
+void copy_name(const char* name, char* buf, int cap) {
+    if (!buf || cap <= 0) return;
+    snprintf(buf, (size_t)cap, "%s", name ? name : "");
+}
+
+}  // namespace
+
+extern "C" {
+
+tt_status tt_softmax_masked_f32(float* scores, const int32_t* lengths, int64_t B, int64_t H,
+                                int64_t Sq, int64_t Sk, float scale, cudaStream_t stream) {
+    return softmax_any(0, scores, lengths, B, H, Sq, Sk, scale, stream);
+}
+tt_status tt_softmax_masked_f16(void* scores, const int32_t* lengths, int64_t B, int64_t H,
+                                int64_t Sq, int64_t Sk, float scale, cudaStream_t stream) {
+    return softmax_any(1, scores, lengths, B, H, Sq, Sk, scale, stream);
+}
+tt_status tt_softmax_masked_bf16(void* scores, const int32_t* lengths, int64_t B, int64_t H,
+                                 int64_t Sq, int64_t Sk, float scale, cudaStream_t stream) {
+    return softmax_any(2, scores, lengths, B, H, Sq, Sk, scale, stream);
+}
+
+tt_status tt_add_bias_layernorm_f32(float* out, const float* x, const float* residual,
+                                    const float* bias, const float* gamma, const float* beta,
+                                    int64_t rows, int64_t hidden, float eps, cudaStream_t stream) {
+    return ln_any(0, out, x, residual, bias, gamma, beta, rows, hidden, eps, stream);
+}
+tt_status tt_add_bias_layernorm_f16(void* out, const void* x, const void* residual,
+                                    const void* bias, const void* gamma, const void* beta,
+                                    int64_t rows, int64_t hidden, float eps, cudaStream_t stream) {
+    return ln_any(1, out, x, residual, bias, gamma, beta, rows, hidden, eps, stream);
+}
+tt_status tt_add_bias_layernorm_bf16(void* out, const void* x, const void* residual,
+                                     const void* bias, const void* gamma, const void* beta,
+                                     int64_t rows, int64_t hidden, float eps, cudaStream_t stream) {
+    return ln_any(2, out, x, residual, bias, gamma, beta, rows, hidden, eps, stream);
+}
+
+tt_status tt_softmax_masked_staged(int dtype, void* host_scores, const int32_t* host_lengths,
+                                   void* dev_scores, int32_t* dev_lengths, int64_t B, int64_t H,
+                                   int64_t Sq, int64_t Sk, float scale, cudaStream_t stream) {
+    int64_t nrows = 0;
+    bool empty = false;
+    tt_status s = softmax_validate(dtype, dev_scores, dev_lengths, B, H, Sq, Sk, scale, true,
+                                   &nrows, &empty);
+    if (s != TT_SUCCESS || empty) return s;
+    if (!host_scores || !host_lengths) return TT_ERROR_INVALID_VALUE;
+    const size_t bytes = (size_t)(nrows * Sk * elem_bytes(dtype));
+    cudaError_t e = cudaMemcpyAsync(dev_lengths, host_lengths, (size_t)B * sizeof(int32_t),
+                                    cudaMemcpyHostToDevice, stream);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(dev_scores, host_scores, bytes, cudaMemcpyHostToDevice, stream);
+    if (e != cudaSuccess) return cuda_status(e);
+    s = softmax_any(dtype, dev_scores, dev_lengths, B, H, Sq, Sk, scale, stream);
+    if (s != TT_SUCCESS) return s;
+    return cuda_status(
+        cudaMemcpyAsync(host_scores, dev_scores, bytes, cudaMemcpyDeviceToHost, stream));
+}
+
+tt_status tt_add_bias_layernorm_staged(int dtype, void* host_out, const void* host_x,
+                                       const void* host_residual, void* dev_out, void* dev_x,
+                                       void* dev_residual, const void* bias, const void* gamma,
+                                       const void* beta, int64_t rows, int64_t hidden, float eps,
+                                       cudaStream_t stream) {
+    bool empty = false;
+    tt_status s = ln_validate(dtype, dev_out, dev_x, dev_residual, bias, gamma, beta, rows, hidden,
+                              eps, true, &empty);
+    if (s != TT_SUCCESS || empty) return s;
+    if (!host_out || !host_x || !host_residual) return TT_ERROR_INVALID_VALUE;
+    const size_t bytes = (size_t)(rows * hidden * elem_bytes(dtype));
+    cudaError_t e = cudaMemcpyAsync(dev_x, host_x, bytes, cudaMemcpyHostToDevice, stream);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(dev_residual, host_residual, bytes, cudaMemcpyHostToDevice, stream);
+    if (e != cudaSuccess) return cuda_status(e);
+    s = ln_any(dtype, dev_out, dev_x, dev_residual, bias, gamma, beta, rows, hidden, eps, stream);
+    if (s != TT_SUCCESS) return s;
+    return cuda_status(cudaMemcpyAsync(host_out, dev_out, bytes, cudaMemcpyDeviceToHost, stream));
+}
+
+const char* tt_status_string(tt_status s) {
+    switch (s) {
+        case TT_SUCCESS: return "TT_SUCCESS";
+        case TT_ERROR_INVALID_VALUE: return "TT_ERROR_INVALID_VALUE";
+        case TT_ERROR_NOT_SUPPORTED: return "TT_ERROR_NOT_SUPPORTED";
+        case TT_ERROR_CUDA: return "TT_ERROR_CUDA";
+        default: return "TT_UNKNOWN_STATUS";
+    }
+}
+
+int tt_last_cuda_error(void) { return g_last_cuda_error; }
+
+int tt_version(void) { return kVersion; }
+
+tt_status tt_softmax_masked_plan(int dtype, int64_t B, int64_t H, int64_t Sq, int64_t Sk,
+                                 char* buf, int cap) {
+    int64_t nrows = 0;
+    bool empty = false;
+    tt_status s = softmax_validate(dtype, nullptr, nullptr, B, H, Sq, Sk, 1.0f, false, &nrows,
+                                   &empty);
+    if (s != TT_SUCCESS) {
+        copy_name("", buf, cap);
+        return s;
+    }
+    copy_name(empty ? "none" : tt::softmax_tier_name(dtype, Sk), buf, cap);
+    return TT_SUCCESS;
+}
+
+tt_status tt_add_bias_layernorm_plan(int dtype, int64_t rows, int64_t hidden, char* buf, int cap) {
+    bool empty = false;
+    tt_status s = ln_validate(dtype, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, rows,
+                              hidden, 0.f, false, &empty);
+    if (s != TT_SUCCESS) {
+        copy_name("", buf, cap);
+        return s;
+    }
+    if (empty) {
+        copy_name("none", buf, cap);
+        return TT_SUCCESS;
+    }
+    // plan for 256-byte-aligned operands (every cudaMalloc / PyTorch allocation)
+    const int e = elem_bytes(dtype);
+    int vb = e;
+    for (int c = 32; c >= e; c >>= 1)
+        if ((hidden * e) % c == 0) {
+            vb = c;
+            break;
+        }
+    copy_name(tt::layernorm_tier_name(dtype, hidden, vb), buf, cap);
+    return TT_SUCCESS;
+}
+
+}  // extern "C"

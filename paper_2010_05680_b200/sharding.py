@@ -1,0 +1,89 @@
+"""Request-batch sharding across the GPUs of one node.
+
+Rows and requests are independent and neither operation reduces across rows,
+so the multi-GPU path has no data-path collective: every rank derives the same
+batch list from the seed, takes its share, and runs the kernels on its own
+GPU.  NCCL (torch.distributed) carries only per-rank records (checksums,
+byte counts, timings) and the timing barriers.
+"""
+from __future__ import annotations
+
+import hashlib
+import struct
+from typing import Sequence
+
+import torch
+
+
+def lpt_partition(costs: Sequence[int], world: int) -> list:
+    """Greedy longest-processing-time bin packing of batch costs onto `world`
+    ranks.  Deterministic: ties in cost keep the lower batch index first, ties
+    in load go to the lower rank.  Returns, per rank, its batch indices in
+    ascending order."""
+    if world < 1:
+        raise ValueError("world must be >= 1")
+    order = sorted(range(len(costs)), key=lambda i: (-int(costs[i]), i))
+    load = [0] * world
+    parts = [[] for _ in range(world)]
+    for i in order:
+        r = min(range(world), key=lambda k: (load[k], k))
+        parts[r].append(i)
+        load[r] += int(costs[i])
+    return [sorted(p) for p in parts]
+
+
+def contiguous_ranges(nrows: int, world: int) -> list:
+    """Split [0, nrows) into `world` contiguous row ranges, sizes differing by <= 1."""
+    base, extra = divmod(nrows, world)
+    out, start = [], 0
+    for r in range(world):
+        n = base + (1 if r < extra else 0)
+        out.append((start, start + n))
+        start += n
+    return out
+
+
+RECORD_FIELDS = ("digest_lo", "digest_hi", "checksum", "bytes_alg", "rows", "elapsed_us",
+                 "batches", "rank")
+
+
+def tensor_digest(t: torch.Tensor) -> int:
+    """64-bit digest of a tensor's bytes (blake2b over the host copy)."""
+    b = t.detach().contiguous().view(torch.uint8).cpu().numpy().tobytes()
+    return int.from_bytes(hashlib.blake2b(b, digest_size=8).digest(), "little")
+
+
+def combine_digests(digests: Sequence[int]) -> int:
+    h = hashlib.blake2b(digest_size=8)
+    for d in digests:
+        h.update(struct.pack("<Q", d & 0xFFFFFFFFFFFFFFFF))
+    return int.from_bytes(h.digest(), "little")
+
+
+def make_record(digest: int, checksum: float, bytes_alg: int, rows: int, elapsed_us: float,
+                batches: int, rank: int) -> torch.Tensor:
+    """Fixed 64-byte per-rank record (8 float64 slots; the 64-bit digest is
+    split into two exact 32-bit halves)."""
+    return torch.tensor([float(digest & 0xFFFFFFFF), float(digest >> 32), float(checksum),
+                         float(bytes_alg), float(rows), float(elapsed_us), float(batches),
+                         float(rank)], dtype=torch.float64)
+
+
+def record_digest(rec) -> int:
+    return int(rec[0]) | (int(rec[1]) << 32)
+
+
+def gather_records(rec: torch.Tensor, group=None) -> torch.Tensor:
+    """all_gather of the 64-byte records -> [world, 8] on every rank."""
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    out = torch.empty((world, rec.numel()), dtype=rec.dtype, device=rec.device)
+    dist.all_gather_into_tensor(out, rec.reshape(1, -1).contiguous(), group=group)
+    return out
+
+
+def max_over_ranks(value: float, device) -> float:
+    import torch.distributed as dist
+    t = torch.tensor([float(value)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())

@@ -1,0 +1,61 @@
+"""Tolerances for GPU-vs-oracle parity (north_star; R14).
+
+g = GPU output widened to float64, ref = oracle (float64).
+  fp32 softmax   |g - ref| <= 1e-5
+  fp32 LN        |g - ref| <= 1e-4 * max(1, |ref|)
+  fp16 (both)    |g - ref| <= 2e-3 * max(1, |ref|)
+  bf16 softmax   |g - ref| <= 2e-3
+  bf16 LN        |g - ref| <= max(2e-3 * max(1, |ref|), ulp_bf16(ref))
+                 (the literal 2e-3 is below bf16's own rounding of LN outputs
+                 of magnitude > 0.5; DESIGN R14(v))
+  masked softmax positions: bit pattern exactly 0 (+0.0) in every dtype.
+"""
+import torch
+
+
+def ulp_bf16(ref: torch.Tensor) -> torch.Tensor:
+    a = ref.abs().clamp_min(2.0 ** -126)
+    return torch.exp2(torch.floor(torch.log2(a)) - 7)
+
+
+def bound(op: str, dtype, ref: torch.Tensor) -> torch.Tensor:
+    one = torch.ones_like(ref)
+    mag = torch.maximum(one, ref.abs())
+    if op == "softmax":
+        if dtype == torch.float32:
+            return torch.full_like(ref, 1e-5)
+        if dtype == torch.float16:
+            return 2e-3 * mag
+        return torch.full_like(ref, 2e-3)
+    if dtype == torch.float32:
+        return 1e-4 * mag
+    if dtype == torch.float16:
+        return 2e-3 * mag
+    return torch.maximum(2e-3 * mag, ulp_bf16(ref))
+
+
+def assert_close(op: str, dtype, got: torch.Tensor, ref: torch.Tensor, what: str = ""):
+    g = got.detach().to("cpu").to(torch.float64)
+    r = ref.to(torch.float64)
+    assert g.shape == r.shape, (g.shape, r.shape)
+    err = (g - r).abs()
+    b = bound(op, dtype, r)
+    bad = ~(err <= b)  # NaN counts as bad
+    if bad.any():
+        idx = bad.nonzero()[0].tolist()
+        raise AssertionError(
+            f"{what} {op} {dtype}: {int(bad.sum())} of {g.numel()} outside tolerance; first at "
+            f"{idx}: got {g[tuple(idx)].item()!r} ref {r[tuple(idx)].item()!r}; max err "
+            f"{err.nan_to_num(float('inf')).max().item():.3e}")
+    return err.max().item() if err.numel() else 0.0
+
+
+def masked_bits_zero(y: torch.Tensor, lengths) -> bool:
+    """Every padding key column (j >= clamp(L_b, 0, Sk)) holds bit pattern 0."""
+    B, H, Sq, Sk = y.shape
+    lens = torch.as_tensor(lengths, dtype=torch.int64, device=y.device).clamp(0, Sk)
+    cols = torch.arange(Sk, device=y.device)
+    mask = (cols[None, :] >= lens[:, None])[:, None, None, :].expand(B, H, Sq, Sk)
+    ib = torch.int32 if y.dtype == torch.float32 else torch.int16
+    bits = y.view(ib)
+    return bool((bits[mask] == 0).all().item())

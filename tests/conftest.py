@@ -36,3 +36,13 @@ def read_golden(name):
                 continue
             rows.append([c.strip() for c in line.split("|")])
     return rows
+
+
+@pytest.fixture(scope="session")
+def ttlib():
+    """Build libtt.so in-tree if stale (nvcc cross-compiles without a GPU)."""
+    from paper_2010_05680_b200 import build as b
+    b.build()
+    import paper_2010_05680_b200 as tt
+    tt.lib()
+    return tt

@@ -1,0 +1,138 @@
+"""The C-ABI boundary without a GPU: the library loads, exports every symbol
+include/tt.h declares, and rejects bad arguments on the host before any CUDA
+call (so none of these tests touches a device)."""
+import ctypes
+import math
+import os
+import re
+
+import pytest
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+DT = [torch.float32, torch.float16, torch.bfloat16]
+FAKE = 0x10000  # 16-B aligned, never dereferenced: validation fails first
+
+
+def _declared():
+    src = open(os.path.join(ROOT, "include", "tt.h")).read()
+    return set(re.findall(r"TT_API\s+[\w\s\*]+?\b(tt_\w+)\s*\(", src))
+
+
+def test_header_declares_expected_api(ttlib):
+    decl = _declared()
+    assert decl == set(ttlib.EXPORTS), decl ^ set(ttlib.EXPORTS)
+
+
+def test_library_exports_every_declared_symbol(ttlib):
+    L = ttlib.lib()
+    for name in _declared():
+        assert hasattr(L, name), name
+        assert ctypes.cast(getattr(L, name), ctypes.c_void_p).value
+
+
+def test_library_is_sm100a_only():
+    from paper_2010_05680_b200 import build as b
+    import subprocess
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", b.LIB],
+                         capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+    ptx = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-ptx", b.LIB],
+                         capture_output=True, text=True).stdout
+    assert "compute_100." not in ptx.replace("compute_100a", "")
+
+
+def test_status_strings_and_version(ttlib):
+    assert ttlib.status_string(0) == "TT_SUCCESS"
+    assert ttlib.status_string(1) == "TT_ERROR_INVALID_VALUE"
+    assert ttlib.status_string(2) == "TT_ERROR_NOT_SUPPORTED"
+    assert ttlib.status_string(3) == "TT_ERROR_CUDA"
+    assert ttlib.version() >= 10000
+    assert ttlib.lib().tt_last_cuda_error() == 0
+
+
+@pytest.mark.parametrize("dtype", DT)
+def test_softmax_validation(ttlib, dtype):
+    f = ttlib.tt_softmax_masked_raw
+    INV, NS, OK = 1, 2, 0
+    assert f(dtype, 0, 0, 2, 2, 2, 8, 1.0) == INV                 # null pointers
+    assert f(dtype, FAKE, 0, 2, 2, 2, 8, 1.0) == INV              # null lengths
+    assert f(dtype, FAKE, FAKE, -1, 2, 2, 8, 1.0) == INV          # negative dim
+    assert f(dtype, FAKE, FAKE, 2, 2, 2, -8, 1.0) == INV
+    assert f(dtype, FAKE, FAKE, 2, 2, 2, 8, math.inf) == INV      # non-finite scale
+    assert f(dtype, FAKE, FAKE, 2, 2, 2, 8, math.nan) == INV
+    assert f(dtype, FAKE, FAKE, 1 << 40, 1 << 20, 1 << 10, 8, 1.0) == INV   # overflow
+    assert f(dtype, FAKE + 2, FAKE, 2, 2, 2, 8, 1.0) == NS        # misaligned base
+    assert f(dtype, FAKE, FAKE + 1, 2, 2, 2, 8, 1.0) == NS        # misaligned lengths
+    assert f(dtype, FAKE, FAKE, 2, 2, 2, ttlib.TT_MAX_SOFTMAX_COLS + 1, 1.0) == NS
+    # empty problems: success, no CUDA call, null pointers allowed
+    for shape in ((0, 2, 2, 8), (2, 0, 2, 8), (2, 2, 0, 8), (2, 2, 2, 0)):
+        assert f(dtype, 0, 0, *shape, 1.0) == OK
+
+
+@pytest.mark.parametrize("dtype", DT)
+def test_layernorm_validation(ttlib, dtype):
+    f = ttlib.tt_add_bias_layernorm_raw
+    INV, NS, OK = 1, 2, 0
+    e = 4 if dtype == torch.float32 else 2
+    rows, hid = 4, 64
+    n = rows * hid * e
+    out, x, r = FAKE, FAKE + 4 * n, FAKE + 8 * n
+    b, g, be = FAKE + 12 * n, FAKE + 12 * n + 4096, FAKE + 12 * n + 8192
+    ok = (out, x, r, b, g, be)
+    assert f(dtype, 0, x, r, b, g, be, rows, hid, 1e-5) == INV
+    assert f(dtype, out, x, r, b, 0, be, rows, hid, 1e-5) == INV
+    assert f(dtype, *ok, -1, hid, 1e-5) == INV
+    assert f(dtype, *ok, rows, hid, -1e-5) == INV                 # negative eps
+    assert f(dtype, *ok, rows, hid, math.inf) == INV
+    assert f(dtype, *ok, rows, hid, math.nan) == INV
+    assert f(dtype, *ok, 1 << 62, 1 << 10, 1e-5) == INV           # overflow
+    # out partially overlapping x (exact aliasing is allowed, tested on GPU)
+    assert f(dtype, x + 64, x, r, b, g, be, rows, hid, 1e-5) == INV
+    assert f(dtype, r - 64, x, r, b, g, be, rows, hid, 1e-5) == INV
+    # parameters overlapping the output
+    assert f(dtype, out, x, r, out + 16, g, be, rows, hid, 1e-5) == INV
+    assert f(dtype, out + 2, x, r, b, g, be, rows, hid, 1e-5) == NS
+    assert f(dtype, out, x, r, b, g, be + 8, rows, hid, 1e-5) == NS
+    big = 1 << 24  # far-apart fake buffers for the oversized-row check
+    far = tuple(FAKE + i * big for i in range(6))
+    assert f(dtype, *far, rows, ttlib.TT_MAX_LN_HIDDEN + 1, 1e-5) == NS
+    assert f(dtype, 0, 0, 0, 0, 0, 0, 0, hid, 1e-5) == OK
+    assert f(dtype, 0, 0, 0, 0, 0, 0, rows, 0, 1e-5) == OK
+
+
+@pytest.mark.skipif(torch.cuda.is_available(), reason="checks the no-device error path")
+def test_launch_without_device_fails_loudly(ttlib):
+    """With valid arguments and no GPU the call reaches the launch and returns
+    TT_ERROR_CUDA: there is no CPU fallback."""
+    st = ttlib.tt_softmax_masked_raw(torch.float32, FAKE, FAKE, 1, 1, 1, 8, 1.0)
+    assert st == ttlib.TT_ERROR_CUDA
+    assert ttlib.lib().tt_last_cuda_error() != 0
+    with pytest.raises(RuntimeError):
+        import paper_2010_05680_b200._lib as L
+        L._check(st, "x")
+
+
+@pytest.mark.parametrize("dtype,Sk,tier", [
+    (torch.float32, 40, "softmax_rows<f32,V16,G16,NV1,R2,T256>"),
+    (torch.float16, 37, "softmax_rows<f16,V16,G8,NV1,R2,T256>"),
+    (torch.bfloat16, 512, "softmax_rows<bf16,V32,G32,NV1,R2,T256>"),
+    (torch.float16, 491, "softmax_rows<f16,V32,G32,NV1,R2,T256>"),
+    (torch.float32, 500, "softmax_rows<f32,V32,G32,NV2,R1,T256>"),
+    (torch.float32, 4096, "softmax_rows<f32,V32,G128,NV4,R1,T128>"),
+    (torch.bfloat16, 32768, "softmax_rows<bf16,V32,G1024,NV2,R1,T1024>"),
+])
+def test_softmax_tier_plan(ttlib, dtype, Sk, tier):
+    assert ttlib.softmax_plan(dtype, 2, 12, 3, Sk) == tier
+
+
+@pytest.mark.parametrize("dtype,hidden,tier", [
+    (torch.float32, 768, "ln_rows<f32,V32,G32,NV3,R1,T256>"),
+    (torch.float16, 768, "ln_rows<f16,V16,G32,NV3,R1,T256>"),
+    (torch.bfloat16, 1024, "ln_rows<bf16,V32,G32,NV2,R1,T256>"),
+    (torch.float32, 37, "ln_rows<f32,V4,G32,NV4,R1,T256>"),
+    (torch.float16, 16, "ln_rows<f16,V16,G4,NV1,R2,T256>"),
+    (torch.float32, 4096, "ln_rows<f32,V32,G128,NV4,R1,T128>"),
+])
+def test_layernorm_tier_plan(ttlib, dtype, hidden, tier):
+    assert ttlib.layernorm_plan(dtype, 10, hidden) == tier

@@ -1,0 +1,133 @@
+"""GPU parity: tt_add_bias_layernorm_* (CUDA, through the C ABI) vs the fp64 oracle."""
+import pytest
+import torch
+
+import oracle
+import workloads as W
+from _parity import assert_close
+
+pytestmark = pytest.mark.gpu
+DT = [torch.float32, torch.float16, torch.bfloat16]
+
+
+def _run(tt, d, eps, out=None):
+    dd = {k: v.cuda() for k, v in d.items()}
+    o = torch.empty_like(dd["x"]) if out is None else out
+    tt.tt_add_bias_layernorm(o, dd["x"], dd["residual"], dd["bias"], dd["gamma"], dd["beta"], eps)
+    torch.cuda.synchronize()
+    return o
+
+
+def _ref(d, eps):
+    return oracle.add_bias_layernorm(d["x"], d["residual"], d["bias"], d["gamma"], d["beta"], eps)
+
+
+def _check(tt, rows, hidden, dtype, eps=W.EPS_BERT, seed=0, offset=0.0, what=""):
+    d = W.ln_inputs(rows, hidden, dtype, seed=seed, offset=offset)
+    y = _run(tt, d, eps)
+    return assert_close("layernorm", dtype, y, _ref(d, eps), what or f"{rows}x{hidden}")
+
+
+def test_c1_bert_base_b1_s40(ttlib):
+    _check(ttlib, 40, 768, torch.float32, what="C1")
+
+
+@pytest.mark.parametrize("dtype", [torch.float16, torch.float32])
+@pytest.mark.parametrize("S", W.C2.extra["seqs"])
+def test_c2_seq_sweep(ttlib, dtype, S):
+    _check(ttlib, 20 * S, 768, dtype, seed=S, what=f"C2 S={S}")
+
+
+@pytest.mark.parametrize("dtype", [torch.float16, torch.float32])
+def test_c3_rows(ttlib, dtype):
+    S = int(W.c3_lengths().max())
+    _check(ttlib, 64 * S, 768, dtype, seed=3, what="C3")
+
+
+def test_c4_bert_large_full_size_sampled(ttlib):
+    """[32768, 1024] bf16 in bench.py's configuration; oracle on sampled rows."""
+    rows, hidden = 64 * 512, 1024
+    d = W.ln_inputs(rows, hidden, torch.bfloat16, device="cuda", seed=4)
+    out = torch.empty_like(d["x"])
+    ttlib.tt_add_bias_layernorm(out, d["x"], d["residual"], d["bias"], d["gamma"], d["beta"],
+                                W.EPS_BERT)
+    torch.cuda.synchronize()
+    idx = torch.randint(0, rows, (4096,), generator=torch.Generator().manual_seed(4))
+    idx[0], idx[-1] = 0, rows - 1
+    ic = idx.cuda()
+    ref = oracle.add_bias_layernorm(d["x"][ic].cpu(), d["residual"][ic].cpu(), d["bias"].cpu(),
+                                    d["gamma"].cpu(), d["beta"].cpu(), W.EPS_BERT)
+    assert_close("layernorm", torch.bfloat16, out[ic], ref, "C4")
+    assert torch.isfinite(out.float()).all()
+
+
+@pytest.mark.parametrize("dtype", DT)
+@pytest.mark.parametrize("hidden", [1, 2, 3, 16, 37, 64, 100, 128, 256, 384, 512, 640, 768, 1000,
+                                    1024, 1536, 2048, 2056, 3072, 4096, 5000, 8192, 32768])
+def test_hidden_sweep(ttlib, dtype, hidden):
+    rows = 3 if hidden > 4096 else 37
+    _check(ttlib, rows, hidden, dtype, eps=1e-5, seed=hidden)
+
+
+@pytest.mark.parametrize("eps", [1e-12, 1e-5, 0.5])
+@pytest.mark.parametrize("dtype", DT)
+def test_eps_values(ttlib, dtype, eps):
+    _check(ttlib, 64, 768, dtype, eps=eps, seed=11)
+
+
+def test_offset_mean_much_larger_than_std_fp32(ttlib):
+    """x ~ N(0,1) + 64: the paper's one-pass E(x^2)-E(x)^2 fails 1e-4 here in
+    fp32 (DESIGN R9); the two-level register moments must pass."""
+    for hidden in (768, 1024):
+        _check(ttlib, 256, hidden, torch.float32, offset=64.0, seed=64, what="offset 64")
+        _check(ttlib, 256, hidden, torch.float32, offset=1000.0, seed=65, what="offset 1000")
+
+
+@pytest.mark.parametrize("dtype", DT)
+def test_alias_out_x_and_out_residual(ttlib, dtype):
+    d = W.ln_inputs(300, 768, dtype, seed=21)
+    ref = _ref(d, W.EPS_BERT)
+    dd = {k: v.cuda() for k, v in d.items()}
+    x = dd["x"].clone()
+    ttlib.tt_add_bias_layernorm(x, x, dd["residual"], dd["bias"], dd["gamma"], dd["beta"],
+                                W.EPS_BERT)
+    torch.cuda.synchronize()
+    assert_close("layernorm", dtype, x, ref, "out=x")
+    r = dd["residual"].clone()
+    ttlib.tt_add_bias_layernorm(r, dd["x"], r, dd["bias"], dd["gamma"], dd["beta"], W.EPS_BERT)
+    torch.cuda.synchronize()
+    assert_close("layernorm", dtype, r, ref, "out=residual")
+
+
+@pytest.mark.parametrize("dtype", DT)
+def test_gamma_zero_gives_beta_exactly(ttlib, dtype):
+    d = W.ln_inputs(50, 1024, dtype, seed=2)
+    d["gamma"] = torch.zeros_like(d["gamma"])
+    y = _run(ttlib, d, 1e-5)
+    assert torch.equal(y.cpu(), d["beta"].expand(50, 1024))
+
+
+@pytest.mark.parametrize("dtype", DT)
+def test_deterministic_bitwise(ttlib, dtype):
+    d = W.ln_inputs(4096, 768, dtype, seed=5)
+    a = _run(ttlib, d, W.EPS_BERT)
+    b = _run(ttlib, d, W.EPS_BERT)
+    assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("dtype", DT)
+def test_staged_host_buffers(ttlib, dtype):
+    d = W.ln_inputs(40, 768, dtype, seed=8)
+    hx, hr = d["x"].clone().pin_memory(), d["residual"].clone().pin_memory()
+    ho = torch.empty_like(hx).pin_memory()
+    dx, dr, do = (torch.empty_like(hx, device="cuda") for _ in range(3))
+    p = {k: d[k].cuda() for k in ("bias", "gamma", "beta")}
+    ttlib.tt_add_bias_layernorm_staged(ho, hx, hr, do, dx, dr, p["bias"], p["gamma"], p["beta"],
+                                       W.EPS_BERT)
+    torch.cuda.synchronize()
+    assert_close("layernorm", dtype, ho, _ref(d, W.EPS_BERT), "staged")
+
+
+def test_rows_not_multiple_of_cta(ttlib):
+    for rows in (1, 7, 15, 17, 1023, 1025):
+        _check(ttlib, rows, 768, torch.float16, seed=rows)

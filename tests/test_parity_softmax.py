@@ -1,0 +1,210 @@
+"""GPU parity: tt_softmax_masked_* (CUDA, through the C ABI) vs the fp64 oracle.
+
+Small configs are compared element by element on every row; full-size
+configs (C3, C4, C5 batches) in the launch configuration bench.py times are
+compared on seeded row samples, plus properties checked on every row
+(masked bits exactly 0, valid rows sum to 1, no NaN)."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import workloads as W
+from _parity import assert_close, masked_bits_zero
+
+pytestmark = pytest.mark.gpu
+DT = [torch.float32, torch.float16, torch.bfloat16]
+SUM_TOL = {torch.float32: 1e-4, torch.float16: 5e-3, torch.bfloat16: 2e-2}
+
+
+def _run(tt, x_cpu, lens, scale):
+    x = x_cpu.cuda()
+    L = torch.as_tensor(np.asarray(lens, dtype=np.int32)).cuda()
+    tt.tt_softmax_masked(x, L, scale)
+    torch.cuda.synchronize()
+    return x
+
+
+def _full_check(tt, x_cpu, lens, scale, what=""):
+    y = _run(tt, x_cpu, lens, scale)
+    ref = oracle.softmax_masked(x_cpu, lens, scale)
+    assert_close("softmax", x_cpu.dtype, y, ref, what)
+    assert masked_bits_zero(y, lens), what
+    return y
+
+
+def _sampled_check(tt, x_dev, lens, scale, nsample=2048, seed=0, what=""):
+    """In-place call on a device tensor; oracle on a seeded sample of rows."""
+    B, H, Sq, Sk = x_dev.shape
+    nrows = B * H * Sq
+    g = torch.Generator().manual_seed(seed)
+    idx = torch.randint(0, nrows, (min(nsample, nrows),), generator=g)
+    idx[0], idx[-1] = 0, nrows - 1
+    rows_before = x_dev.view(nrows, Sk)[idx.cuda()].cpu()
+    L = torch.as_tensor(np.asarray(lens, dtype=np.int32)).cuda()
+    tt.tt_softmax_masked(x_dev, L, scale)
+    torch.cuda.synchronize()
+    got = x_dev.view(nrows, Sk)[idx.cuda()].cpu()
+    row_lens = np.asarray(lens, dtype=np.int32)[(idx // (H * Sq)).numpy()]
+    ref = oracle.softmax_rows(rows_before, row_lens, scale)
+    assert_close("softmax", x_dev.dtype, got, ref, what)
+    # every row: masked bits, sums, finiteness
+    assert masked_bits_zero(x_dev, lens), what
+    s = x_dev.float().sum(-1)
+    lens_t = torch.as_tensor(np.asarray(lens), device=x_dev.device).clamp(0, Sk)
+    valid = (lens_t > 0)[:, None, None].expand(B, H, Sq)
+    assert torch.isfinite(s).all()
+    assert ((s[valid] - 1).abs() <= SUM_TOL[x_dev.dtype]).all(), what
+    assert (s[~valid] == 0).all()
+
+
+# ----------------------------------------------------------------- C1, C2
+def test_c1_bert_base_b1_s40(ttlib):
+    x = W.scores(1, 12, 40, 40, torch.float32, seed=W.SEED + 1)
+    _full_check(ttlib, x, [40], W.SCALE_BERT, "C1")
+
+
+@pytest.mark.parametrize("dtype", [torch.float16, torch.float32])
+@pytest.mark.parametrize("S", W.C2.extra["seqs"])
+@pytest.mark.parametrize("ragged", [False, True])
+def test_c2_seq_sweep(ttlib, dtype, S, ragged):
+    lens = W.lengths_ragged(20, S) if ragged else W.lengths_full(20, S)
+    if S <= 128:
+        x = W.scores(20, 12, S, S, dtype, seed=W.SEED + 2 + S)
+        _full_check(ttlib, x, lens, W.SCALE_BERT, f"C2 S={S}")
+    else:
+        x = W.scores(20, 12, S, S, dtype, device="cuda", seed=W.SEED + 2 + S)
+        _sampled_check(ttlib, x, lens, W.SCALE_BERT, what=f"C2 S={S}")
+
+
+# ----------------------------------------------------------------- C3, C4, C5
+@pytest.mark.parametrize("dtype", [torch.float16, torch.float32])
+def test_c3_variable_length_batch(ttlib, dtype):
+    lens = W.c3_lengths()
+    S = int(lens.max())
+    x = W.scores(64, 12, S, S, dtype, device="cuda", seed=W.SEED + 3)
+    _sampled_check(ttlib, x, lens, W.SCALE_BERT, nsample=4096, what="C3")
+
+
+@pytest.mark.parametrize("ragged", [False, True])
+def test_c4_bert_large_full_size(ttlib, ragged):
+    lens = W.lengths_ragged(64, 512, seed_offset=4) if ragged else W.lengths_full(64, 512)
+    x = W.scores(64, 16, 512, 512, torch.bfloat16, device="cuda", seed=W.SEED + 4)
+    _sampled_check(ttlib, x, lens, W.SCALE_BERT, nsample=4096, what="C4")
+
+
+@pytest.mark.parametrize("dtype", [torch.float16, torch.bfloat16])
+def test_c5_stream_batches(ttlib, dtype):
+    batches = W.c5_stream()
+    for bi in (0, 17, 63):
+        lens = batches[bi]
+        S = int(lens.max())
+        x = W.scores(64, 12, S, S, dtype, device="cuda", seed=W.SEED + 5 + bi)
+        _sampled_check(ttlib, x, lens, W.SCALE_BERT, nsample=1024, seed=bi, what=f"C5 b{bi}")
+
+
+# ----------------------------------------------------------------- edge cases
+@pytest.mark.parametrize("dtype", DT)
+def test_every_row_length_1_to_160(ttlib, dtype):
+    """Every Sk 1..160: all tiers' head / body / tail splits and group sizes."""
+    for Sk in range(1, 161):
+        B = 3
+        lens = [Sk, max(Sk // 2, 1), 0]
+        x = W.scores(B, 2, 3, Sk, dtype, seed=Sk)
+        _full_check(ttlib, x, lens, W.SCALE_BERT, f"Sk={Sk}")
+
+
+@pytest.mark.parametrize("dtype", DT)
+@pytest.mark.parametrize("Sk", [255, 256, 257, 511, 513, 767, 1000, 1023, 1024, 1025, 2047, 2048,
+                                2049, 4095, 4096, 4099, 8192, 16384, 32768])
+def test_long_rows_and_tier_boundaries(ttlib, dtype, Sk):
+    lens = [Sk, Sk - 1, 1, Sk // 3]
+    x = W.scores(4, 1, 2, Sk, dtype, seed=Sk + 7)
+    _full_check(ttlib, x, lens, W.SCALE_BERT, f"Sk={Sk}")
+
+
+@pytest.mark.parametrize("dtype", DT)
+def test_length_edge_values(ttlib, dtype):
+    Sk = 70
+    lens = [0, -5, 1, 69, 70, 71, 1 << 30, -(1 << 30)]
+    x = W.scores(len(lens), 2, 2, Sk, dtype, seed=3)
+    y = _full_check(ttlib, x, lens, W.SCALE_BERT, "edge lengths")
+    assert (y[0] == 0).all() and (y[1] == 0).all() and (y[7] == 0).all()
+    assert (y[2, :, :, 0] == 1).all()
+
+
+@pytest.mark.parametrize("dtype", DT)
+def test_poison_in_masked_columns_is_never_read(ttlib, dtype):
+    for Sk in (37, 64, 500, 512, 3000):
+        lens = [Sk // 2, 1, Sk, 0]
+        x = W.scores(4, 2, 3, Sk, dtype, seed=Sk)
+        clean = _run(ttlib, x, lens, W.SCALE_BERT)
+        dirty = _run(ttlib, W.poison_masked(x, lens), lens, W.SCALE_BERT)
+        ib = torch.int32 if dtype == torch.float32 else torch.int16
+        assert torch.equal(clean.view(ib), dirty.view(ib)), Sk
+
+
+@pytest.mark.parametrize("dtype", DT)
+def test_peaky_and_scale_variants(ttlib, dtype):
+    Sk = 130
+    lens = [130, 77]
+    x = W.scores(2, 3, 5, Sk, dtype, seed=99, std=40.0)
+    for scale in (W.SCALE_BERT, 1.0, -0.5, 0.0, 1e-3):
+        _full_check(ttlib, x, lens, scale, f"scale={scale}")
+
+
+@pytest.mark.parametrize("dtype", DT)
+def test_deterministic_bitwise(ttlib, dtype):
+    lens = W.c3_lengths(salt=1)
+    S = int(lens.max())
+    x = W.scores(64, 12, S, S, dtype, device="cuda", seed=5)
+    a, b = x.clone(), x.clone()
+    L = torch.as_tensor(lens).cuda()
+    ttlib.tt_softmax_masked(a, L, W.SCALE_BERT)
+    ttlib.tt_softmax_masked(b, L, W.SCALE_BERT)
+    torch.cuda.synchronize()
+    ib = torch.int32 if dtype == torch.float32 else torch.int16
+    assert torch.equal(a.view(ib), b.view(ib))
+
+
+def test_nondefault_stream_and_offset_views(ttlib):
+    """A side stream, and a base pointer 16 B (not 32 B) aligned."""
+    s = torch.cuda.Stream()
+    Sk = 512
+    buf = W.scores(1, 1, 1, 8 + 2 * 3 * Sk, torch.bfloat16, seed=1).reshape(-1).cuda()
+    x = buf[8:].view(2, 1, 3, Sk)  # 16-byte offset
+    assert x.data_ptr() % 32 == 16
+    ref_in = x.cpu()
+    lens = torch.tensor([512, 300], dtype=torch.int32).cuda()
+    with torch.cuda.stream(s):
+        ttlib.tt_softmax_masked(x, lens, 0.125, stream=s)
+    s.synchronize()
+    assert_close("softmax", torch.bfloat16, x, oracle.softmax_masked(ref_in, [512, 300], 0.125))
+    assert (buf[:8].cpu() == W.scores(1, 1, 1, 8 + 2 * 3 * Sk, torch.bfloat16,
+                                      seed=1).reshape(-1)[:8]).all()
+
+
+@pytest.mark.parametrize("dtype", DT)
+def test_staged_host_buffers(ttlib, dtype):
+    lens = np.array([40, 17, 3], dtype=np.int32)
+    x = W.scores(3, 12, 40, 40, dtype, seed=8)
+    host = x.clone().pin_memory()
+    hl = torch.as_tensor(lens).pin_memory()
+    dev = torch.empty_like(x, device="cuda")
+    dl = torch.empty(3, dtype=torch.int32, device="cuda")
+    ttlib.tt_softmax_masked_staged(host, hl, dev, dl, W.SCALE_BERT)
+    torch.cuda.synchronize()
+    assert_close("softmax", dtype, host, oracle.softmax_masked(x, lens, W.SCALE_BERT))
+    assert masked_bits_zero(host, lens)
+
+
+def test_binding_rejects_bad_tensors(ttlib):
+    x = torch.zeros(2, 2, 2, 8, device="cuda")
+    with pytest.raises(ValueError):
+        ttlib.tt_softmax_masked(x, torch.zeros(2, dtype=torch.int64, device="cuda"), 1.0)
+    with pytest.raises(ValueError):
+        ttlib.tt_softmax_masked(x.transpose(2, 3), torch.zeros(2, dtype=torch.int32,
+                                                                device="cuda"), 1.0)
+    with pytest.raises(ttlib.TTError):
+        ttlib.tt_softmax_masked(x, torch.zeros(2, dtype=torch.int32, device="cuda"),
+                                float("inf"))
