@@ -1,0 +1,34 @@
+/*
+ * tt_tune.h -- tuning and test hooks of libtt.so (not part of the serving
+ * contract in tt.h).
+ *
+ * Every kernel configuration ("tier") compiled into the library can be listed
+ * and forced, so that tests can run each tier against the oracle and tools can
+ * time them.  Forcing is process-global and meant for single-threaded tools.
+ * A forced tier that cannot serve a call's shape is ignored (automatic
+ * selection is used for that call).  The automatic choice is what
+ * tt_softmax_masked_plan / tt_add_bias_layernorm_plan report.
+ *
+ * op: 0 = softmax, 1 = add-bias LayerNorm.  dtype: 0 = fp32, 1 = fp16, 2 = bf16.
+ */
+#ifndef TT_TUNE_H_
+#define TT_TUNE_H_
+
+#include "tt.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Number of compiled tiers for `op` (same for every dtype); -1 on a bad op. */
+TT_API int ttx_tier_count(int op);
+/* Static name of tier i, or NULL when out of range. */
+TT_API const char* ttx_tier_name(int op, int dtype, int i);
+/* Force tier i for (op, dtype); i = -1 restores automatic selection.
+ * Returns TT_ERROR_INVALID_VALUE for a bad op, dtype or index. */
+TT_API tt_status ttx_force_tier(int op, int dtype, int i);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TT_TUNE_H_ */

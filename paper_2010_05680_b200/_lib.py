@@ -32,6 +32,7 @@ EXPORTS = (
     "tt_softmax_masked_staged", "tt_add_bias_layernorm_staged",
     "tt_status_string", "tt_last_cuda_error", "tt_version",
     "tt_softmax_masked_plan", "tt_add_bias_layernorm_plan",
+    "ttx_tier_count", "ttx_tier_name", "ttx_force_tier",
 )
 
 
@@ -69,10 +70,14 @@ def lib() -> ctypes.CDLL:
                                                        _vp, _i64, _i64, _f, _vp]
             L.tt_softmax_masked_plan.argtypes = [_i, _i64, _i64, _i64, _i64, ctypes.c_char_p, _i]
             L.tt_add_bias_layernorm_plan.argtypes = [_i, _i64, _i64, ctypes.c_char_p, _i]
+            L.ttx_tier_count.argtypes = [_i]
+            L.ttx_tier_name.argtypes = [_i, _i, _i]
+            L.ttx_tier_name.restype = ctypes.c_char_p
+            L.ttx_force_tier.argtypes = [_i, _i, _i]
             L.tt_status_string.argtypes = [_i]
             L.tt_status_string.restype = ctypes.c_char_p
             for name in EXPORTS:
-                if name != "tt_status_string":
+                if name not in ("tt_status_string", "ttx_tier_name"):
                     getattr(L, name).restype = _i
             _lib = L
     return _lib
@@ -202,3 +207,19 @@ def layernorm_plan(dtype: torch.dtype, rows: int, hidden: int) -> str:
     _check(lib().tt_add_bias_layernorm_plan(DTYPE_CODE[dtype], rows, hidden, buf, 128),
            "tt_add_bias_layernorm_plan")
     return buf.value.decode()
+
+
+# --------------------------------------------------------------------- tuning
+OPS = {"softmax": 0, "layernorm": 1}
+
+
+def tiers(op: str, dtype: torch.dtype) -> list:
+    """Names of every compiled tier of `op` for `dtype` (include/tt_tune.h)."""
+    L = lib()
+    o = OPS[op]
+    return [L.ttx_tier_name(o, DTYPE_CODE[dtype], i).decode() for i in range(L.ttx_tier_count(o))]
+
+
+def force_tier(op: str, dtype: torch.dtype, index: int):
+    """Force tier `index` (-1 = automatic) for subsequent calls in this process."""
+    _check(lib().ttx_force_tier(OPS[op], DTYPE_CODE[dtype], int(index)), "ttx_force_tier")

@@ -22,4 +22,15 @@ cudaError_t layernorm_launch(int dtype, void* out, const void* x, const void* re
                              bool* supported);
 const char* layernorm_tier_name(int dtype, int64_t hidden, int vec_bytes);
 
+// Tuning / test hooks (include/tt_tune.h): enumerate every compiled tier and
+// force one (-1 = automatic selection).  A forced tier that cannot serve the
+// call's shape is ignored.
+int softmax_tier_count();
+const char* softmax_tier_name_at(int dtype, int i);
+int softmax_tier_max_cols_at(int dtype, int i);
+bool softmax_force_tier(int dtype, int i);
+int layernorm_tier_count();
+const char* layernorm_tier_name_at(int dtype, int i);
+bool layernorm_force_tier(int dtype, int i);
+
 }  // namespace tt

@@ -5,21 +5,24 @@
 //
 // One group of G threads owns one row:
 //   LN-1  v_k = (x_k + bias_k) + residual_k in fp32, held in registers
-//   LN-2  mean = sum(v) / N, then var = sum((v - mean)^2) / N: two register
-//         butterflies over the SAME registers (one extra shuffle round, zero
-//         extra HBM bytes).  The paper's one-pass E(x^2) - E(x)^2 (Eq. 1 RHS)
+//   LN-2  mean = K + sum(v - K) / N (K = the row's first element, a shift
+//         that keeps the accumulator small), then var = sum((v - mean)^2) / N:
+//         two register butterflies over the SAME registers (one extra shuffle
+//         round, zero extra HBM bytes).  The paper's one-pass E(x^2) - E(x)^2 (Eq. 1 RHS)
 //         saves that round but loses ~3 digits in fp32 when |mean| >> std
 //         (DESIGN R9, offset test), so it is not used.
 //   LN-3  y_k = (v_k - mean) * rsqrt(var + eps) * gamma_k + beta_k, RNE
 //         narrowing, vector store.  `out` may alias x or residual exactly:
 //         every element of a row is loaded before any element is stored.
+#include <atomic>
+
 #include "common.cuh"
 #include "launch.h"
 
 namespace tt {
 
-template <typename T, int VB, int G, int NV, int R, int NT>
-__global__ void __launch_bounds__(NT)
+template <typename T, int VB, int G, int NV, int R, int NT, int MINB>
+__global__ void __launch_bounds__(NT, MINB)
     ln_rows_kernel(T* out, const T* x, const T* residual, const T* __restrict__ bias,
                    const T* __restrict__ gamma, const T* __restrict__ beta, int64_t rows,
                    int hidden, float eps) {
@@ -71,22 +74,35 @@ __global__ void __launch_bounds__(NT)
         }
     }
 
-    // ---- LN-2: mean, then centred second moment
-    float mean[R];
+    // ---- LN-2: mean, then centred second moment.  The mean is accumulated
+    // on data shifted by the row's first element K (exact in fp32 for nearby
+    // values), so |mean| >> std loses no digits to the accumulator.
+    float shift[R], mean[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) {
+        if constexpr (G <= 32) {
+            shift[r] = __shfl_sync(0xffffffffu, v[r][0][0], (int)(threadIdx.x & 31) & ~(G - 1));
+        } else {
+            shift[r] = live[r] ? (Elem<T>::to_f(x[off[r]]) + Elem<T>::to_f(bias[0])) +
+                                     Elem<T>::to_f(residual[off[r]])
+                               : 0.f;
+        }
         float a = 0.f;
 #pragma unroll
-        for (int k = 0; k < NV; ++k)
+        for (int k = 0; k < NV; ++k) {
+            const int vi = q + k * G;
+            if (vi < nvec) {
 #pragma unroll
-            for (int e = 0; e < VE; ++e) a += v[r][k][e];
+                for (int e = 0; e < VE; ++e) a += v[r][k][e] - shift[r];
+            }
+        }
         mean[r] = a;
     }
     group_sum<G, R>(mean, red_a);
     float var[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-        mean[r] *= invN;
+        mean[r] = fmaf(mean[r], invN, shift[r]);
         float a = 0.f;
 #pragma unroll
         for (int k = 0; k < NV; ++k) {
@@ -130,7 +146,7 @@ __global__ void __launch_bounds__(NT)
 
 namespace {
 
-template <typename T, int VB, int G, int NV, int R, int NT>
+template <typename T, int VB, int G, int NV, int R, int NT, int MINB>
 cudaError_t launch_ln(void* out, const void* x, const void* res, const void* bias,
                       const void* gamma, const void* beta, int64_t rows, int hidden, float eps,
                       cudaStream_t st) {
@@ -138,7 +154,7 @@ cudaError_t launch_ln(void* out, const void* x, const void* res, const void* bia
     const int64_t rows_per_cta = (int64_t)GPB * R;
     const int64_t grid = (rows + rows_per_cta - 1) / rows_per_cta;
     if (grid > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
-    ln_rows_kernel<T, VB, G, NV, R, NT><<<(unsigned)grid, NT, 0, st>>>(
+    ln_rows_kernel<T, VB, G, NV, R, NT, MINB><<<(unsigned)grid, NT, 0, st>>>(
         static_cast<T*>(out), static_cast<const T*>(x), static_cast<const T*>(res),
         static_cast<const T*>(bias), static_cast<const T*>(gamma), static_cast<const T*>(beta),
         rows, hidden, eps);
@@ -149,53 +165,76 @@ using LnFn = cudaError_t (*)(void*, const void*, const void*, const void*, const
                              const void*, int64_t, int, float, cudaStream_t);
 
 struct LnTier {
-    int vb;        // vector bytes
-    int ve;        // elements per vector
-    int capacity;  // G * NV * VE: largest hidden
+    int vb;          // vector bytes
+    int ve;          // elements per vector
+    int capacity;    // G * NV * VE: largest hidden
+    bool automatic;  // eligible for automatic selection (else: tuning candidate only)
     LnFn fn;
     const char* name;
 };
 
-#define TT_LN_TIER(T, TN, VB, G, NV, R, NT)                                                \
+#define TT_LN_TIER(AUTO, T, TN, VB, G, NV, R, NT, MINB)                                    \
     LnTier {                                                                               \
-        VB, (VB) / (int)sizeof(T), (G) * (NV) * ((VB) / (int)sizeof(T)),                   \
-            &launch_ln<T, VB, G, NV, R, NT>,                                               \
-            "ln_rows<" TN ",V" #VB ",G" #G ",NV" #NV ",R" #R ",T" #NT ">"                 \
+        VB, (VB) / (int)sizeof(T), (G) * (NV) * ((VB) / (int)sizeof(T)), AUTO,             \
+            &launch_ln<T, VB, G, NV, R, NT, MINB>,                                         \
+            "ln_rows<" TN ",V" #VB ",G" #G ",NV" #NV ",R" #R ",T" #NT ",M" #MINB ">"      \
     }
 
 // Main tiers use 16- or 32-byte vectors; the scalar tiers (VB = sizeof(T))
 // only serve hidden sizes whose row pitch is not a multiple of 16 bytes.
-// NVC = CTA-tier vectors per thread (NV * VE = 32 registers of row data);
-// NVS = scalar CTA tier (VE = 1).
-#define TT_LN_TABLE(T, TN, SB, NVC32, NVC16)                                               \
-    static const LnTier kLn_##TN[] = {                                                     \
-        TT_LN_TIER(T, #TN, 16, 4, 1, 2, 256),   TT_LN_TIER(T, #TN, 16, 8, 1, 2, 256),       \
-        TT_LN_TIER(T, #TN, 16, 16, 1, 2, 256),  TT_LN_TIER(T, #TN, 16, 32, 1, 2, 256),      \
-        TT_LN_TIER(T, #TN, 16, 32, 2, 2, 256),  TT_LN_TIER(T, #TN, 16, 32, 3, 1, 256),      \
-        TT_LN_TIER(T, #TN, 16, 32, 4, 1, 256),  TT_LN_TIER(T, #TN, 16, 32, 6, 1, 256),      \
-        TT_LN_TIER(T, #TN, 16, 32, 8, 1, 256),  TT_LN_TIER(T, #TN, 32, 4, 1, 2, 256),       \
-        TT_LN_TIER(T, #TN, 32, 8, 1, 2, 256),   TT_LN_TIER(T, #TN, 32, 16, 1, 2, 256),      \
-        TT_LN_TIER(T, #TN, 32, 32, 1, 2, 256),  TT_LN_TIER(T, #TN, 32, 32, 2, 1, 256),      \
-        TT_LN_TIER(T, #TN, 32, 32, 3, 1, 256),  TT_LN_TIER(T, #TN, 32, 32, 4, 1, 256),      \
-        TT_LN_TIER(T, #TN, 16, 128, NVC16, 1, 128), TT_LN_TIER(T, #TN, 16, 256, NVC16, 1, 256), \
-        TT_LN_TIER(T, #TN, 16, 512, NVC16, 1, 512), TT_LN_TIER(T, #TN, 16, 1024, NVC16, 1, 1024), \
-        TT_LN_TIER(T, #TN, 32, 128, NVC32, 1, 128), TT_LN_TIER(T, #TN, 32, 256, NVC32, 1, 256), \
-        TT_LN_TIER(T, #TN, 32, 512, NVC32, 1, 512), TT_LN_TIER(T, #TN, 32, 1024, NVC32, 1, 1024), \
-        TT_LN_TIER(T, #TN, SB, 32, 1, 1, 256),  TT_LN_TIER(T, #TN, SB, 32, 4, 1, 256),      \
-        TT_LN_TIER(T, #TN, SB, 32, 16, 1, 256), TT_LN_TIER(T, #TN, SB, 256, 16, 1, 256),    \
-        TT_LN_TIER(T, #TN, SB, 1024, 32, 1, 1024),                                         \
-    };
+// NVC32 / NVC16 = CTA-tier vectors per thread (NV * VE = 32 registers of row
+// data).  Non-automatic entries are tuning candidates (tt_tune.h).
+#define TT_LN_LIST(T, TN, SB, NVC32, NVC16)                                                  \
+    TT_LN_TIER(true, T, TN, 16, 4, 1, 2, 256, 1), TT_LN_TIER(true, T, TN, 16, 8, 1, 2, 256, 1), \
+    TT_LN_TIER(true, T, TN, 16, 16, 1, 2, 256, 1), TT_LN_TIER(true, T, TN, 16, 32, 1, 2, 256, 1), \
+    TT_LN_TIER(true, T, TN, 16, 32, 2, 2, 256, 1), TT_LN_TIER(true, T, TN, 16, 32, 3, 1, 256, 1), \
+    TT_LN_TIER(true, T, TN, 16, 32, 4, 1, 256, 1), TT_LN_TIER(true, T, TN, 16, 32, 6, 1, 256, 1), \
+    TT_LN_TIER(true, T, TN, 16, 32, 8, 1, 256, 1), TT_LN_TIER(true, T, TN, 32, 4, 1, 2, 256, 1), \
+    TT_LN_TIER(true, T, TN, 32, 8, 1, 2, 256, 1), TT_LN_TIER(true, T, TN, 32, 16, 1, 2, 256, 1), \
+    TT_LN_TIER(true, T, TN, 32, 32, 1, 2, 256, 1), TT_LN_TIER(true, T, TN, 32, 32, 2, 1, 256, 1), \
+    TT_LN_TIER(true, T, TN, 32, 32, 3, 1, 256, 1), TT_LN_TIER(true, T, TN, 32, 32, 4, 1, 256, 1), \
+    TT_LN_TIER(true, T, TN, 16, 128, NVC16, 1, 128, 1), TT_LN_TIER(true, T, TN, 16, 256, NVC16, 1, 256, 1), \
+    TT_LN_TIER(true, T, TN, 16, 512, NVC16, 1, 512, 1), TT_LN_TIER(true, T, TN, 16, 1024, NVC16, 1, 1024, 1), \
+    TT_LN_TIER(true, T, TN, 32, 128, NVC32, 1, 128, 1), TT_LN_TIER(true, T, TN, 32, 256, NVC32, 1, 256, 1), \
+    TT_LN_TIER(true, T, TN, 32, 512, NVC32, 1, 512, 1), TT_LN_TIER(true, T, TN, 32, 1024, NVC32, 1, 1024, 1), \
+    TT_LN_TIER(true, T, TN, SB, 32, 1, 1, 256, 1), TT_LN_TIER(true, T, TN, SB, 32, 4, 1, 256, 1), \
+    TT_LN_TIER(true, T, TN, SB, 32, 16, 1, 256, 1), TT_LN_TIER(true, T, TN, SB, 256, 16, 1, 256, 1), \
+    TT_LN_TIER(true, T, TN, SB, 1024, 32, 1, 1024, 1),                                      \
+    TT_LN_TIER(false, T, TN, 32, 32, 2, 2, 256, 1), TT_LN_TIER(false, T, TN, 32, 32, 2, 1, 128, 1), \
+    TT_LN_TIER(false, T, TN, 32, 32, 2, 1, 256, 4), \
+    TT_LN_TIER(false, T, TN, 16, 32, 4, 2, 256, 1), TT_LN_TIER(false, T, TN, 32, 32, 2, 2, 128, 2), \
+    TT_LN_TIER(false, T, TN, 32, 32, 3, 2, 256, 1), TT_LN_TIER(false, T, TN, 32, 32, 3, 1, 128, 1), \
+    TT_LN_TIER(false, T, TN, 16, 32, 3, 2, 256, 1)
 
-TT_LN_TABLE(float, f32, 4, 4, 8)
-TT_LN_TABLE(__half, f16, 2, 2, 4)
-TT_LN_TABLE(__nv_bfloat16, bf16, 2, 2, 4)
+const LnTier kLn_f32[] = {TT_LN_LIST(float, "f32", 4, 4, 8)};
+const LnTier kLn_f16[] = {TT_LN_LIST(__half, "f16", 2, 2, 4)};
+const LnTier kLn_bf16[] = {TT_LN_LIST(__nv_bfloat16, "bf16", 2, 2, 4)};
+constexpr int kLnN = (int)(sizeof(kLn_f32) / sizeof(kLn_f32[0]));
 
-template <size_t N>
-const LnTier* pick_from(const LnTier (&tab)[N], int64_t hidden, int vec_bytes) {
+std::atomic<int> g_force[3] = {{-1}, {-1}, {-1}};
+
+const LnTier* table(int dtype) {
+    switch (dtype) {
+        case 0: return kLn_f32;
+        case 1: return kLn_f16;
+        case 2: return kLn_bf16;
+        default: return nullptr;
+    }
+}
+
+bool fits(const LnTier& t, int64_t hidden, int vec_bytes) {
+    return t.vb <= vec_bytes && hidden % t.ve == 0 && hidden <= t.capacity;
+}
+
+const LnTier* pick_dtype(int dtype, int64_t hidden, int vec_bytes) {
+    const LnTier* tab = table(dtype);
+    if (!tab) return nullptr;
+    const int f = g_force[dtype].load(std::memory_order_relaxed);
+    if (f >= 0 && f < kLnN && fits(tab[f], hidden, vec_bytes)) return &tab[f];
     const LnTier* best = nullptr;
-    for (size_t i = 0; i < N; ++i) {
+    for (int i = 0; i < kLnN; ++i) {
         const LnTier& t = tab[i];
-        if (t.vb > vec_bytes || hidden % t.ve != 0 || hidden > t.capacity) continue;
+        if (!t.automatic || !fits(t, hidden, vec_bytes)) continue;
         // least padding first (fewest idle lanes), then the widest vector
         if (!best || t.capacity < best->capacity ||
             (t.capacity == best->capacity && t.vb > best->vb))
@@ -204,16 +243,20 @@ const LnTier* pick_from(const LnTier (&tab)[N], int64_t hidden, int vec_bytes) {
     return best;
 }
 
-const LnTier* pick_dtype(int dtype, int64_t hidden, int vec_bytes) {
-    switch (dtype) {
-        case 0: return pick_from(kLn_f32, hidden, vec_bytes);
-        case 1: return pick_from(kLn_f16, hidden, vec_bytes);
-        case 2: return pick_from(kLn_bf16, hidden, vec_bytes);
-        default: return nullptr;
-    }
+}  // namespace
+
+int layernorm_tier_count() { return kLnN; }
+
+const char* layernorm_tier_name_at(int dtype, int i) {
+    const LnTier* t = table(dtype);
+    return (t && i >= 0 && i < kLnN) ? t[i].name : nullptr;
 }
 
-}  // namespace
+bool layernorm_force_tier(int dtype, int i) {
+    if (dtype < 0 || dtype > 2 || i < -1 || i >= kLnN) return false;
+    g_force[dtype].store(i);
+    return true;
+}
 
 const char* layernorm_tier_name(int dtype, int64_t hidden, int vec_bytes) {
     const LnTier* t = pick_dtype(dtype, hidden, vec_bytes);

@@ -16,6 +16,8 @@
 // Rows of any length: a row starts at an arbitrary element offset, so each row
 // is split into an unaligned head (< VE elements, scalar), an aligned body of
 // VB-byte vectors and a tail (< VE elements, scalar).
+#include <atomic>
+
 #include "common.cuh"
 #include "launch.h"
 
@@ -23,8 +25,8 @@ namespace tt {
 
 constexpr float kLog2e = 1.4426950408889634f;
 
-template <typename T, int VB, int G, int NV, int R, int NT>
-__global__ void __launch_bounds__(NT) softmax_rows_kernel(T* __restrict__ scores,
+template <typename T, int VB, int G, int NV, int R, int NT, int MINB>
+__global__ void __launch_bounds__(NT, MINB) softmax_rows_kernel(T* __restrict__ scores,
                                                           const int32_t* __restrict__ lengths,
                                                           int64_t nrows, int64_t rows_per_batch,
                                                           int Sk, float c) {
@@ -159,14 +161,14 @@ __global__ void __launch_bounds__(NT) softmax_rows_kernel(T* __restrict__ scores
 // ----------------------------------------------------------------------------
 namespace {
 
-template <typename T, int VB, int G, int NV, int R, int NT>
+template <typename T, int VB, int G, int NV, int R, int NT, int MINB>
 cudaError_t launch_softmax(void* scores, const int32_t* lengths, int64_t nrows, int64_t rpb,
                            int Sk, float scale, cudaStream_t st) {
     constexpr int GPB = NT / G;
     const int64_t rows_per_cta = (int64_t)GPB * R;
     const int64_t grid = (nrows + rows_per_cta - 1) / rows_per_cta;
     if (grid > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
-    softmax_rows_kernel<T, VB, G, NV, R, NT><<<(unsigned)grid, NT, 0, st>>>(
+    softmax_rows_kernel<T, VB, G, NV, R, NT, MINB><<<(unsigned)grid, NT, 0, st>>>(
         static_cast<T*>(scores), lengths, nrows, rpb, Sk, scale * kLog2e);
     return cudaGetLastError();
 }
@@ -176,65 +178,85 @@ using SoftmaxFn = cudaError_t (*)(void*, const int32_t*, int64_t, int64_t, int, 
 
 struct SoftmaxTier {
     int max_cols;  // largest Sk this tier handles for its dtype
+    bool automatic;  // eligible for automatic selection (else: tuning candidate only)
     SoftmaxFn fn;
     const char* name;
 };
 
-#define TT_SM_TIER(T, TN, VB, G, NV, R, NT)                                                 \
-    SoftmaxTier {                                                                           \
-        (G) * (NV) * ((VB) / (int)sizeof(T)), &launch_softmax<T, VB, G, NV, R, NT>,        \
-            "softmax_rows<" TN ",V" #VB ",G" #G ",NV" #NV ",R" #R ",T" #NT ">"            \
+#define TT_SM_TIER(AUTO, T, TN, VB, G, NV, R, NT, MINB)                                    \
+    SoftmaxTier {                                                                          \
+        (G) * (NV) * ((VB) / (int)sizeof(T)), AUTO,                                        \
+            &launch_softmax<T, VB, G, NV, R, NT, MINB>,                                    \
+            "softmax_rows<" TN ",V" #VB ",G" #G ",NV" #NV ",R" #R ",T" #NT ",M" #MINB ">" \
     }
 
-// Ordered by max_cols; the first tier that fits is used.  Short rows use
-// 16-byte vectors so that more lanes carry bytes; rows of >= 256 B use
-// 32-byte vectors (LDG.256).  Sub-warp groups handle many short rows per
-// warp; R = 2 rows per group in flight doubles the memory-level parallelism.
-template <typename T>
-struct SoftmaxTable;
+// Automatic tiers are ordered by max_cols; the first that fits is used.
+// Short rows use 16-byte vectors so that more lanes carry bytes; rows of
+// >= 256 B use 32-byte vectors (LDG.256).  Sub-warp groups handle many short
+// rows per warp; R = 2 rows per group in flight doubles the memory-level
+// parallelism.  CTA tiers keep NV * VE = 32 fp32 registers of row data per
+// thread so that a 1024-thread CTA fits the 64-register limit: NVC = 4 (fp32)
+// or 2 (16-bit).  Non-automatic entries are tuning candidates (tt_tune.h).
+#define TT_SM_LIST(T, TN, NVC)                                                               \
+    TT_SM_TIER(true, T, TN, 16, 4, 1, 2, 256, 1), TT_SM_TIER(true, T, TN, 16, 8, 1, 2, 256, 1), \
+    TT_SM_TIER(true, T, TN, 16, 16, 1, 2, 256, 1), TT_SM_TIER(true, T, TN, 32, 16, 1, 2, 256, 1), \
+    TT_SM_TIER(true, T, TN, 32, 32, 1, 2, 256, 1), TT_SM_TIER(true, T, TN, 32, 32, 2, 1, 256, 1), \
+    TT_SM_TIER(true, T, TN, 32, 32, 3, 1, 256, 1), TT_SM_TIER(true, T, TN, 32, 32, 4, 1, 256, 1), \
+    TT_SM_TIER(true, T, TN, 32, 64, NVC, 1, 64, 1), TT_SM_TIER(true, T, TN, 32, 128, NVC, 1, 128, 1), \
+    TT_SM_TIER(true, T, TN, 32, 256, NVC, 1, 256, 1), TT_SM_TIER(true, T, TN, 32, 512, NVC, 1, 512, 1), \
+    TT_SM_TIER(true, T, TN, 32, 1024, NVC, 1, 1024, 1),                                     \
+    TT_SM_TIER(false, T, TN, 32, 32, 1, 1, 256, 1), TT_SM_TIER(false, T, TN, 32, 32, 1, 4, 256, 1), \
+    TT_SM_TIER(false, T, TN, 32, 32, 1, 2, 128, 1), TT_SM_TIER(false, T, TN, 32, 32, 1, 1, 128, 1), \
+    TT_SM_TIER(false, T, TN, 32, 32, 1, 2, 256, 4), TT_SM_TIER(false, T, TN, 32, 32, 1, 1, 256, 6), \
+    TT_SM_TIER(false, T, TN, 32, 32, 1, 2, 512, 2), TT_SM_TIER(false, T, TN, 16, 32, 2, 1, 256, 1), \
+    TT_SM_TIER(false, T, TN, 16, 32, 2, 2, 256, 1), TT_SM_TIER(false, T, TN, 32, 32, 1, 4, 128, 2), \
+    TT_SM_TIER(false, T, TN, 32, 32, 2, 2, 256, 1), TT_SM_TIER(false, T, TN, 32, 32, 2, 1, 128, 1)
 
-#define TT_SM_TABLE(T, TN, NVC)                                                             \
-    template <>                                                                             \
-    struct SoftmaxTable<T> {                                                                \
-        static constexpr int N = 13;                                                        \
-        static const SoftmaxTier* tiers() {                                                 \
-            static const SoftmaxTier t[N] = {                                               \
-                TT_SM_TIER(T, TN, 16, 4, 1, 2, 256),     TT_SM_TIER(T, TN, 16, 8, 1, 2, 256),  \
-                TT_SM_TIER(T, TN, 16, 16, 1, 2, 256),    TT_SM_TIER(T, TN, 32, 16, 1, 2, 256), \
-                TT_SM_TIER(T, TN, 32, 32, 1, 2, 256),    TT_SM_TIER(T, TN, 32, 32, 2, 1, 256), \
-                TT_SM_TIER(T, TN, 32, 32, 3, 1, 256),    TT_SM_TIER(T, TN, 32, 32, 4, 1, 256), \
-                TT_SM_TIER(T, TN, 32, 64, NVC, 1, 64),   TT_SM_TIER(T, TN, 32, 128, NVC, 1, 128), \
-                TT_SM_TIER(T, TN, 32, 256, NVC, 1, 256), TT_SM_TIER(T, TN, 32, 512, NVC, 1, 512), \
-                TT_SM_TIER(T, TN, 32, 1024, NVC, 1, 1024),                                 \
-            };                                                                              \
-            return t;                                                                       \
-        }                                                                                   \
-    };
+const SoftmaxTier kSm_f32[] = {TT_SM_LIST(float, "f32", 4)};
+const SoftmaxTier kSm_f16[] = {TT_SM_LIST(__half, "f16", 2)};
+const SoftmaxTier kSm_bf16[] = {TT_SM_LIST(__nv_bfloat16, "bf16", 2)};
+constexpr int kSmN = (int)(sizeof(kSm_f32) / sizeof(kSm_f32[0]));
 
-// CTA tiers keep NV * VE = 32 fp32 registers of row data per thread so that a
-// 1024-thread CTA fits the 64-register limit: NVC = 4 (fp32) or 2 (16-bit).
-TT_SM_TABLE(float, "f32", 4)
-TT_SM_TABLE(__half, "f16", 2)
-TT_SM_TABLE(__nv_bfloat16, "bf16", 2)
+std::atomic<int> g_force[3] = {{-1}, {-1}, {-1}};
 
-template <typename T>
-const SoftmaxTier* pick(int64_t Sk) {
-    const SoftmaxTier* t = SoftmaxTable<T>::tiers();
-    for (int i = 0; i < SoftmaxTable<T>::N; ++i)
-        if (Sk <= t[i].max_cols) return &t[i];
-    return nullptr;
-}
-
-const SoftmaxTier* pick_dtype(int dtype, int64_t Sk) {
+const SoftmaxTier* table(int dtype) {
     switch (dtype) {
-        case 0: return pick<float>(Sk);
-        case 1: return pick<__half>(Sk);
-        case 2: return pick<__nv_bfloat16>(Sk);
+        case 0: return kSm_f32;
+        case 1: return kSm_f16;
+        case 2: return kSm_bf16;
         default: return nullptr;
     }
 }
 
+const SoftmaxTier* pick_dtype(int dtype, int64_t Sk) {
+    const SoftmaxTier* t = table(dtype);
+    if (!t) return nullptr;
+    const int f = g_force[dtype].load(std::memory_order_relaxed);
+    if (f >= 0 && f < kSmN && Sk <= t[f].max_cols) return &t[f];
+    for (int i = 0; i < kSmN; ++i)
+        if (t[i].automatic && Sk <= t[i].max_cols) return &t[i];
+    return nullptr;
+}
+
 }  // namespace
+
+int softmax_tier_count() { return kSmN; }
+
+const char* softmax_tier_name_at(int dtype, int i) {
+    const SoftmaxTier* t = table(dtype);
+    return (t && i >= 0 && i < kSmN) ? t[i].name : nullptr;
+}
+
+int softmax_tier_max_cols_at(int dtype, int i) {
+    const SoftmaxTier* t = table(dtype);
+    return (t && i >= 0 && i < kSmN) ? t[i].max_cols : -1;
+}
+
+bool softmax_force_tier(int dtype, int i) {
+    if (dtype < 0 || dtype > 2 || i < -1 || i >= kSmN) return false;
+    g_force[dtype].store(i);
+    return true;
+}
 
 const char* softmax_tier_name(int dtype, int64_t Sk) {
     const SoftmaxTier* t = pick_dtype(dtype, Sk);

@@ -8,6 +8,7 @@
 #include <string.h>
 
 #include "../../include/tt.h"
+#include "../../include/tt_tune.h"
 #include "launch.h"
 
 namespace {
@@ -263,6 +264,21 @@ tt_status tt_add_bias_layernorm_plan(int dtype, int64_t rows, int64_t hidden, ch
         }
     copy_name(tt::layernorm_tier_name(dtype, hidden, vb), buf, cap);
     return TT_SUCCESS;
+}
+
+int ttx_tier_count(int op) {
+    return op == 0 ? tt::softmax_tier_count() : op == 1 ? tt::layernorm_tier_count() : -1;
+}
+
+const char* ttx_tier_name(int op, int dtype, int i) {
+    return op == 0 ? tt::softmax_tier_name_at(dtype, i)
+                   : op == 1 ? tt::layernorm_tier_name_at(dtype, i) : nullptr;
+}
+
+tt_status ttx_force_tier(int op, int dtype, int i) {
+    bool ok = op == 0 ? tt::softmax_force_tier(dtype, i)
+                      : op == 1 ? tt::layernorm_force_tier(dtype, i) : false;
+    return ok ? TT_SUCCESS : TT_ERROR_INVALID_VALUE;
 }
 
 }  // extern "C"

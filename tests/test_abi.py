@@ -15,8 +15,12 @@ FAKE = 0x10000  # 16-B aligned, never dereferenced: validation fails first
 
 
 def _declared():
-    src = open(os.path.join(ROOT, "include", "tt.h")).read()
-    return set(re.findall(r"TT_API\s+[\w\s\*]+?\b(tt_\w+)\s*\(", src))
+    names = set()
+    for h in os.listdir(os.path.join(ROOT, "include")):
+        if h.endswith(".h"):
+            src = open(os.path.join(ROOT, "include", h)).read()
+            names |= set(re.findall(r"TT_API\s+[\w\s\*]+?\b(ttx?_\w+)\s*\(", src))
+    return names
 
 
 def test_header_declares_expected_api(ttlib):
@@ -114,25 +118,41 @@ def test_launch_without_device_fails_loudly(ttlib):
 
 
 @pytest.mark.parametrize("dtype,Sk,tier", [
-    (torch.float32, 40, "softmax_rows<f32,V16,G16,NV1,R2,T256>"),
-    (torch.float16, 37, "softmax_rows<f16,V16,G8,NV1,R2,T256>"),
-    (torch.bfloat16, 512, "softmax_rows<bf16,V32,G32,NV1,R2,T256>"),
-    (torch.float16, 491, "softmax_rows<f16,V32,G32,NV1,R2,T256>"),
-    (torch.float32, 500, "softmax_rows<f32,V32,G32,NV2,R1,T256>"),
-    (torch.float32, 4096, "softmax_rows<f32,V32,G128,NV4,R1,T128>"),
-    (torch.bfloat16, 32768, "softmax_rows<bf16,V32,G1024,NV2,R1,T1024>"),
+    (torch.float32, 40, "softmax_rows<f32,V16,G16,NV1,R2,T256,M1>"),
+    (torch.float16, 37, "softmax_rows<f16,V16,G8,NV1,R2,T256,M1>"),
+    (torch.bfloat16, 512, "softmax_rows<bf16,V32,G32,NV1,R2,T256,M1>"),
+    (torch.float16, 491, "softmax_rows<f16,V32,G32,NV1,R2,T256,M1>"),
+    (torch.float32, 500, "softmax_rows<f32,V32,G32,NV2,R1,T256,M1>"),
+    (torch.float32, 4096, "softmax_rows<f32,V32,G128,NV4,R1,T128,M1>"),
+    (torch.bfloat16, 32768, "softmax_rows<bf16,V32,G1024,NV2,R1,T1024,M1>"),
 ])
 def test_softmax_tier_plan(ttlib, dtype, Sk, tier):
     assert ttlib.softmax_plan(dtype, 2, 12, 3, Sk) == tier
 
 
 @pytest.mark.parametrize("dtype,hidden,tier", [
-    (torch.float32, 768, "ln_rows<f32,V32,G32,NV3,R1,T256>"),
-    (torch.float16, 768, "ln_rows<f16,V16,G32,NV3,R1,T256>"),
-    (torch.bfloat16, 1024, "ln_rows<bf16,V32,G32,NV2,R1,T256>"),
-    (torch.float32, 37, "ln_rows<f32,V4,G32,NV4,R1,T256>"),
-    (torch.float16, 16, "ln_rows<f16,V16,G4,NV1,R2,T256>"),
-    (torch.float32, 4096, "ln_rows<f32,V32,G128,NV4,R1,T128>"),
+    (torch.float32, 768, "ln_rows<f32,V32,G32,NV3,R1,T256,M1>"),
+    (torch.float16, 768, "ln_rows<f16,V16,G32,NV3,R1,T256,M1>"),
+    (torch.bfloat16, 1024, "ln_rows<bf16,V32,G32,NV2,R1,T256,M1>"),
+    (torch.float32, 37, "ln_rows<f32,V4,G32,NV4,R1,T256,M1>"),
+    (torch.float16, 16, "ln_rows<f16,V16,G4,NV1,R2,T256,M1>"),
+    (torch.float32, 4096, "ln_rows<f32,V32,G128,NV4,R1,T128,M1>"),
 ])
 def test_layernorm_tier_plan(ttlib, dtype, hidden, tier):
     assert ttlib.layernorm_plan(dtype, 10, hidden) == tier
+
+
+def test_tier_enumeration_and_force(ttlib):
+    for op in ("softmax", "layernorm"):
+        for dt in DT:
+            names = ttlib.tiers(op, dt)
+            assert len(names) == len(set(names)) >= 10
+    with pytest.raises(ttlib.TTError):
+        ttlib.force_tier("softmax", torch.float32, 10 ** 6)
+    ttlib.force_tier("softmax", torch.bfloat16, 0)   # G4 tier cannot serve Sk=512
+    try:
+        assert ttlib.softmax_plan(torch.bfloat16, 1, 1, 1, 512) == \
+            "softmax_rows<bf16,V32,G32,NV1,R2,T256,M1>"
+        assert ttlib.softmax_plan(torch.bfloat16, 1, 1, 1, 8) == ttlib.tiers("softmax", torch.bfloat16)[0]
+    finally:
+        ttlib.force_tier("softmax", torch.bfloat16, -1)

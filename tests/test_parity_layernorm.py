@@ -131,3 +131,18 @@ def test_staged_host_buffers(ttlib, dtype):
 def test_rows_not_multiple_of_cta(ttlib):
     for rows in (1, 7, 15, 17, 1023, 1025):
         _check(ttlib, rows, 768, torch.float16, seed=rows)
+
+
+@pytest.mark.parametrize("dtype", DT)
+def test_every_compiled_tier(ttlib, dtype):
+    """Force each tier (include/tt_tune.h) and check it on shapes it can serve."""
+    names = ttlib.tiers("layernorm", dtype)
+    try:
+        for i, name in enumerate(names):
+            ttlib.force_tier("layernorm", dtype, i)
+            for hidden in (16, 37, 96, 512, 768, 1024, 2048, 4096, 12288):
+                if ttlib.layernorm_plan(dtype, 7, hidden) != name:
+                    continue
+                _check(ttlib, 37, hidden, dtype, eps=1e-5, seed=hidden + i, what=name)
+    finally:
+        ttlib.force_tier("layernorm", dtype, -1)

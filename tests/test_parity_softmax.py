@@ -208,3 +208,20 @@ def test_binding_rejects_bad_tensors(ttlib):
     with pytest.raises(ttlib.TTError):
         ttlib.tt_softmax_masked(x, torch.zeros(2, dtype=torch.int32, device="cuda"),
                                 float("inf"))
+
+
+@pytest.mark.parametrize("dtype", DT)
+def test_every_compiled_tier(ttlib, dtype):
+    """Force each tier (include/tt_tune.h) and check it on shapes it can serve."""
+    names = ttlib.tiers("softmax", dtype)
+    try:
+        for i, name in enumerate(names):
+            ttlib.force_tier("softmax", dtype, i)
+            for Sk in (3, 37, 130, 512, 1000, 2100, 9000):
+                if ttlib.softmax_plan(dtype, 1, 1, 1, Sk) != name:
+                    continue
+                lens = [Sk, max(1, Sk - 5), 1, 0, Sk // 2]
+                x = W.scores(len(lens), 2, 3, Sk, dtype, seed=Sk + i)
+                _full_check(ttlib, x, lens, W.SCALE_BERT, f"{name} Sk={Sk}")
+    finally:
+        ttlib.force_tier("softmax", dtype, -1)

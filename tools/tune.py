@@ -1,0 +1,80 @@
+#!/usr/bin/env python
+"""Time every compiled tier (include/tt_tune.h) on one shape; prints JSON lines.
+
+  python tools/tune.py softmax bf16 64 16 512 512      # B H Sq Sk (all keys valid)
+  python tools/tune.py layernorm bf16 32768 1024       # rows hidden
+
+Inputs are larger than L2 for the headline shapes; smaller shapes rotate over
+enough buffers to exceed 4x L2.  CUDA events on the launching stream.
+"""
+import json
+import os
+import sys
+
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import paper_2010_05680_b200 as tt  # noqa: E402
+import workloads as W  # noqa: E402
+
+L2 = 126 * 1024 * 1024
+
+
+def timeit(fn, nbufs, reps=50, warm=5):
+    st = torch.cuda.current_stream()
+    for i in range(warm):
+        fn(i % nbufs)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    a.record(st)
+    for i in range(reps):
+        fn(i % nbufs)
+    b.record(st)
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / reps
+
+
+def main():
+    op, dt = sys.argv[1], W.DTYPES[sys.argv[2]]
+    dims = [int(v) for v in sys.argv[3:]]
+    ragged = os.environ.get("RAGGED") == "1"
+    e = W.ELEM_BYTES[dt]
+    names = tt.tiers(op, dt)
+    only = os.environ.get("ONLY")
+    if op == "softmax":
+        B, H, Sq, Sk = dims
+        lens = W.lengths_ragged(B, Sk) if ragged else W.lengths_full(B, Sk)
+        nbytes = B * H * Sq * Sk * e
+        nbufs = max(1, -(-4 * L2 // nbytes))
+        bufs = [W.scores(B, H, Sq, Sk, dt, device="cuda", seed=i) for i in range(nbufs)]
+        L = torch.as_tensor(lens).cuda()
+        alg = W.softmax_bytes_alg(lens, H, Sq, Sk, e)
+        fn = lambda i: tt.tt_softmax_masked(bufs[i], L, 0.125)  # noqa: E731
+        plan = tt.softmax_plan(dt, B, H, Sq, Sk)
+    else:
+        rows, hidden = dims
+        nbytes = 3 * rows * hidden * e
+        nbufs = max(1, -(-4 * L2 // nbytes))
+        ds = [W.ln_inputs(rows, hidden, dt, device="cuda", seed=i) for i in range(nbufs)]
+        outs = [torch.empty_like(d["x"]) for d in ds]
+        alg = W.ln_bytes_alg(rows, hidden, e)
+        fn = lambda i: tt.tt_add_bias_layernorm(outs[i], ds[i]["x"], ds[i]["residual"],  # noqa
+                                                ds[i]["bias"], ds[i]["gamma"], ds[i]["beta"], 1e-12)
+        plan = tt.layernorm_plan(dt, rows, hidden)
+    for i, name in enumerate([None] + names):
+        if only and name and only not in name:
+            continue
+        tt.force_tier(op, dt, i - 1)
+        chosen = tt.softmax_plan(dt, *dims) if op == "softmax" else tt.layernorm_plan(dt, *dims)
+        if name is not None and chosen != name:
+            continue  # tier cannot serve this shape
+        ms = timeit(fn, nbufs)
+        print(json.dumps({"op": op, "dtype": sys.argv[2], "dims": dims, "ragged": ragged,
+                          "tier": chosen, "auto": name is None or name == plan,
+                          "us": round(ms * 1e3, 2), "GBps": round(alg / ms / 1e6, 1)}), flush=True)
+    tt.force_tier(op, dt, -1)
+
+
+if __name__ == "__main__":
+    main()
