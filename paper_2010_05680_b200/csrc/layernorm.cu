@@ -144,6 +144,171 @@ __global__ void __launch_bounds__(NT, MINB)
     }
 }
 
+
+// ----------------------------------------------------------------------------
+// TMA-staged variant (warp per row, 16-byte chunks): persistent kernel, each
+// warp streams its rows' x and residual through a private ring of D shared-
+// memory slots filled by 1-D bulk copies (cp.async.bulk) issued D rows ahead.
+// Requires hidden * sizeof(T) % 16 == 0 and 16-byte aligned operands.
+// ----------------------------------------------------------------------------
+template <typename T, int NV, int NW>
+__global__ void __launch_bounds__(NW * 32)
+    ln_tma_kernel(T* out, const T* x, const T* residual, const T* __restrict__ bias,
+                  const T* __restrict__ gamma, const T* __restrict__ beta, int64_t rows, int hidden,
+                  float eps, int D, int slot_bytes) {
+    constexpr int VE = 16 / (int)sizeof(T);
+    extern __shared__ __align__(128) unsigned char smem[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem) + warp * D;
+    unsigned char* ring = smem + ((NW * D * 8 + 127) & ~127) + (size_t)warp * D * slot_bytes;
+    const int64_t TW = (int64_t)gridDim.x * NW;
+    const int64_t gw = (int64_t)blockIdx.x * NW + warp;
+    const uint32_t rb = (uint32_t)hidden * (uint32_t)sizeof(T);  // row bytes, multiple of 16
+    const int nchunks = hidden / VE;
+    const float invN = 1.0f / (float)hidden;
+
+    auto issue = [&](int64_t row, int sl) {
+        if (row >= rows) return;
+        unsigned char* dst = ring + (size_t)sl * slot_bytes;
+        mbar_arrive_expect_tx(&bars[sl], 2 * rb);
+        tma_load_1d(dst, x + row * (int64_t)hidden, rb, &bars[sl]);
+        tma_load_1d(dst + rb, residual + row * (int64_t)hidden, rb, &bars[sl]);
+    };
+    if (lane == 0) {
+        for (int s = 0; s < D; ++s) mbar_init(&bars[s], 1);
+        fence_mbar_init();
+        fence_proxy_async_smem();
+        for (int s = 0; s < D; ++s) issue(gw + s * TW, s);
+    }
+    __syncwarp();
+
+    int sl = 0;
+    uint32_t ph = 0;
+    for (int64_t row = gw; row < rows; row += TW) {
+        const unsigned char* slot = ring + (size_t)sl * slot_bytes;
+        mbar_wait(&bars[sl], ph);
+        // ---- LN-1
+        float v[NV][VE];
+#pragma unroll
+        for (int k = 0; k < NV; ++k) {
+            const int ci = lane + 32 * k;
+            if (ci < nchunks) {
+                Raw<16> wx, wr, wb;
+                lds128(slot + 16 * ci, wx.w);
+                lds128(slot + rb + 16 * ci, wr.w);
+                ld_param<16>(bias + ci * VE, wb);
+                float fr[VE], fb[VE];
+                Elem<T>::template unpack<16>(wx, v[k]);
+                Elem<T>::template unpack<16>(wr, fr);
+                Elem<T>::template unpack<16>(wb, fb);
+#pragma unroll
+                for (int e = 0; e < VE; ++e) v[k][e] = (v[k][e] + fb[e]) + fr[e];
+            } else {
+#pragma unroll
+                for (int e = 0; e < VE; ++e) v[k][e] = 0.f;
+            }
+        }
+        // slot consumed (values are in registers once the shift is formed)
+        float shift[1] = {__shfl_sync(0xffffffffu, v[0][0], 0)};
+        __syncwarp();
+        if (lane == 0) {
+            fence_proxy_async_smem();
+            issue(row + (int64_t)D * TW, sl);
+        }
+        if (++sl == D) {
+            sl = 0;
+            ph ^= 1;
+        }
+        // ---- LN-2
+        float mean[1] = {0.f};
+#pragma unroll
+        for (int k = 0; k < NV; ++k)
+            if (lane + 32 * k < nchunks) {
+#pragma unroll
+                for (int e = 0; e < VE; ++e) mean[0] += v[k][e] - shift[0];
+            }
+        group_sum<32, 1>(mean, nullptr);
+        const float mu = fmaf(mean[0], invN, shift[0]);
+        float var[1] = {0.f};
+#pragma unroll
+        for (int k = 0; k < NV; ++k)
+            if (lane + 32 * k < nchunks) {
+#pragma unroll
+                for (int e = 0; e < VE; ++e) {
+                    const float d = v[k][e] - mu;
+                    var[0] = fmaf(d, d, var[0]);
+                }
+            }
+        group_sum<32, 1>(var, nullptr);
+        const float rstd = rsqrtf(var[0] * invN + eps);
+        // ---- LN-3
+        T* o = out + row * (int64_t)hidden;
+#pragma unroll
+        for (int k = 0; k < NV; ++k) {
+            const int ci = lane + 32 * k;
+            if (ci < nchunks) {
+                Raw<16> wg, wb, wy;
+                ld_param<16>(gamma + ci * VE, wg);
+                ld_param<16>(beta + ci * VE, wb);
+                float fg[VE], fb[VE], y[VE];
+                Elem<T>::template unpack<16>(wg, fg);
+                Elem<T>::template unpack<16>(wb, fb);
+#pragma unroll
+                for (int e = 0; e < VE; ++e) y[e] = fmaf((v[k][e] - mu) * rstd, fg[e], fb[e]);
+                Elem<T>::template pack<16>(y, wy);
+                st_stream<16>(o + ci * VE, wy);
+            }
+        }
+    }
+}
+
+namespace {
+
+int sm_count() {
+    static int cached[64] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) dev = 0;
+    if (!cached[dev]) {
+        int n = 0;
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        cached[dev] = n > 0 ? n : 148;
+    }
+    return cached[dev];
+}
+
+template <typename T, int NV, int NW>
+cudaError_t launch_ln_tma(void* out, const void* x, const void* res, const void* bias,
+                          const void* gamma, const void* beta, int64_t rows, int hidden, float eps,
+                          cudaStream_t st) {
+    auto kern = ln_tma_kernel<T, NV, NW>;
+    const int rb = hidden * (int)sizeof(T);
+    const int slot_bytes = (2 * rb + 127) & ~127;
+    const int D = max(2, min(8, 8192 / slot_bytes + 1));
+    const size_t smem = (size_t)((NW * D * 8 + 127) & ~127) + (size_t)NW * D * slot_bytes;
+    static std::atomic<int> attr_done{0};
+    if (smem > 48 * 1024 && attr_done.load() < (int)smem) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+        if (e != cudaSuccess) return e;
+        attr_done.store((int)smem);
+    }
+    int occ = 0;
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NW * 32, smem);
+    if (e != cudaSuccess) return e;
+    occ = max(occ, 1);
+    const int64_t need = (rows + NW - 1) / NW;
+    const int64_t cap = (int64_t)sm_count() * occ;
+    const int64_t grid = need < cap ? need : cap;
+    kern<<<(unsigned)grid, NW * 32, smem, st>>>(
+        static_cast<T*>(out), static_cast<const T*>(x), static_cast<const T*>(res),
+        static_cast<const T*>(bias), static_cast<const T*>(gamma), static_cast<const T*>(beta),
+        rows, hidden, eps, D, slot_bytes);
+    return cudaGetLastError();
+}
+
+}  // namespace
+
 namespace {
 
 template <typename T, int VB, int G, int NV, int R, int NT, int MINB>
@@ -180,6 +345,12 @@ struct LnTier {
             "ln_rows<" TN ",V" #VB ",G" #G ",NV" #NV ",R" #R ",T" #NT ",M" #MINB ">"      \
     }
 
+#define TT_LN_TMA(AUTO, T, TN, NV, NW)                                                     \
+    LnTier {                                                                               \
+        16, 16 / (int)sizeof(T), 32 * (NV) * (16 / (int)sizeof(T)), AUTO,                 \
+            &launch_ln_tma<T, NV, NW>, "ln_tma<" TN ",V16,G32,NV" #NV ",W" #NW ">"        \
+    }
+
 // Main tiers use 16- or 32-byte vectors; the scalar tiers (VB = sizeof(T))
 // only serve hidden sizes whose row pitch is not a multiple of 16 bytes.
 // NVC32 / NVC16 = CTA-tier vectors per thread (NV * VE = 32 registers of row
@@ -204,7 +375,9 @@ struct LnTier {
     TT_LN_TIER(false, T, TN, 32, 32, 2, 1, 256, 4), \
     TT_LN_TIER(false, T, TN, 16, 32, 4, 2, 256, 1), TT_LN_TIER(false, T, TN, 32, 32, 2, 2, 128, 2), \
     TT_LN_TIER(false, T, TN, 32, 32, 3, 2, 256, 1), TT_LN_TIER(false, T, TN, 32, 32, 3, 1, 128, 1), \
-    TT_LN_TIER(false, T, TN, 16, 32, 3, 2, 256, 1)
+    TT_LN_TIER(false, T, TN, 16, 32, 3, 2, 256, 1), \
+    TT_LN_TMA(false, T, TN, 3, 8), TT_LN_TMA(false, T, TN, 4, 8), TT_LN_TMA(false, T, TN, 4, 4),       \
+    TT_LN_TMA(false, T, TN, 6, 4), TT_LN_TMA(false, T, TN, 8, 4), TT_LN_TMA(false, T, TN, 2, 8)
 
 const LnTier kLn_f32[] = {TT_LN_LIST(float, "f32", 4, 4, 8)};
 const LnTier kLn_f16[] = {TT_LN_LIST(__half, "f16", 2, 2, 4)};

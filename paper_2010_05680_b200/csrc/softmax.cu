@@ -70,9 +70,14 @@ __global__ void __launch_bounds__(NT, MINB) softmax_rows_kernel(T* __restrict__ 
                 Raw<VB> w;
                 ld_stream<VB>(p[r] + j0, w);
                 Elem<T>::template unpack<VB>(w, v[r][k]);
+                if (j0 + VE <= Lr[r]) {  // whole vector valid: no per-element mask
 #pragma unroll
-                for (int e = 0; e < VE; ++e)
-                    v[r][k][e] = (j0 + e < Lr[r]) ? v[r][k][e] * c : -INFINITY;
+                    for (int e = 0; e < VE; ++e) v[r][k][e] *= c;
+                } else {
+#pragma unroll
+                    for (int e = 0; e < VE; ++e)
+                        v[r][k][e] = (j0 + e < Lr[r]) ? v[r][k][e] * c : -INFINITY;
+                }
             } else {
 #pragma unroll
                 for (int e = 0; e < VE; ++e) v[r][k][e] = -INFINITY;
@@ -137,8 +142,13 @@ __global__ void __launch_bounds__(NT, MINB) softmax_rows_kernel(T* __restrict__ 
             if (vi < nv[r]) {
                 const int j0 = hd[r] + vi * VE;
                 float y[VE];
+                if (j0 + VE <= Lr[r]) {
 #pragma unroll
-                for (int e = 0; e < VE; ++e) y[e] = (j0 + e < Lr[r]) ? v[r][k][e] * inv : 0.f;
+                    for (int e = 0; e < VE; ++e) y[e] = v[r][k][e] * inv;
+                } else {
+#pragma unroll
+                    for (int e = 0; e < VE; ++e) y[e] = (j0 + e < Lr[r]) ? v[r][k][e] * inv : 0.f;
+                }
                 Raw<VB> w;
                 Elem<T>::template pack<VB>(y, w);
                 st_stream<VB>(p[r] + j0, w);
@@ -154,6 +164,230 @@ __global__ void __launch_bounds__(NT, MINB) softmax_rows_kernel(T* __restrict__ 
         }
     }
 }
+
+
+// ----------------------------------------------------------------------------
+// TMA-staged variant for warp-sized rows (G = 32): a persistent kernel where
+// every warp streams its rows through a private ring of D shared-memory slots.
+// Lane 0 issues one 1-D bulk copy (cp.async.bulk, SASS UBLKCP) per row, of the
+// row's VALID prefix only (16-byte aligned span), D rows ahead of the row being
+// computed, so the bytes in flight per SM are set by the ring depth instead of
+// by the register file.  The math and the stores are those of
+// softmax_rows_kernel; the body is read from shared memory in 16-byte chunks
+// (lane-contiguous, conflict-free LDS.128) and written with 16-byte STG.
+// ----------------------------------------------------------------------------
+template <typename T, int NV, int NW>
+__global__ void __launch_bounds__(NW * 32) softmax_tma_kernel(T* __restrict__ scores,
+                                                              const int32_t* __restrict__ lengths,
+                                                              int64_t nrows, int64_t rows_per_batch,
+                                                              int Sk, float c, int D,
+                                                              int slot_bytes) {
+    constexpr int E = (int)sizeof(T);
+    constexpr int VE = 16 / E;               // elements per 16-byte chunk
+    constexpr int HI = (VE - 1 + 31) / 32;   // = 1
+    extern __shared__ __align__(128) unsigned char smem[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem) + warp * D;
+    unsigned char* ring = smem + ((NW * D * 8 + 127) & ~127) + (size_t)warp * D * slot_bytes;
+    const int64_t TW = (int64_t)gridDim.x * NW;
+    const int64_t gw = (int64_t)blockIdx.x * NW + warp;
+
+    auto row_len = [&](int64_t row) {
+        const int L = __ldg(lengths + row / rows_per_batch);
+        return min(max(L, 0), Sk);
+    };
+    // lane 0: stage row `row` into slot `sl` (valid prefix only)
+    auto issue = [&](int64_t row, int sl) {
+        if (row >= nrows) return;
+        const int L = row_len(row);
+        const uintptr_t a = reinterpret_cast<uintptr_t>(scores + row * (int64_t)Sk);
+        if (L == 0) {
+            mbar_arrive(&bars[sl]);  // nothing to read: complete the phase
+            return;
+        }
+        const uintptr_t a0 = a & ~(uintptr_t)15;
+        const uint32_t bytes = (uint32_t)(((a + (uintptr_t)L * E + 15) & ~(uintptr_t)15) - a0);
+        mbar_arrive_expect_tx(&bars[sl], bytes);
+        tma_load_1d(ring + (size_t)sl * slot_bytes, reinterpret_cast<const void*>(a0), bytes,
+                    &bars[sl]);
+    };
+
+    if (lane == 0) {
+        for (int s = 0; s < D; ++s) mbar_init(&bars[s], 1);
+        fence_mbar_init();
+        fence_proxy_async_smem();
+        for (int s = 0; s < D; ++s) issue(gw + s * TW, s);
+    }
+    __syncwarp();
+
+    int sl = 0;
+    uint32_t ph = 0;
+    for (int64_t row = gw; row < nrows; row += TW) {
+        T* p = scores + row * (int64_t)Sk;
+        const int L = row_len(row);
+        const int off = (int)(reinterpret_cast<uintptr_t>(p) & 15);
+        const int hd = off ? min((16 - off) / E, Sk) : 0;
+        const int nb = (Sk - hd) / VE;
+        const int tl0 = hd + nb * VE;
+        const unsigned char* slot = ring + (size_t)sl * slot_bytes;
+        const unsigned char* body = slot + (off ? 16 : 0);
+
+        mbar_wait(&bars[sl], ph);
+
+        // ---- SM-2: shared -> registers, scaled into the log2 domain
+        float v[NV][VE];
+        float hv[HI], tv[HI];
+#pragma unroll
+        for (int k = 0; k < NV; ++k) {
+            const int ci = lane + 32 * k;
+            const int j0 = hd + ci * VE;
+            if (ci < nb && j0 < L) {
+                Raw<16> w;
+                lds128(body + 16 * ci, w.w);
+                Elem<T>::template unpack<16>(w, v[k]);
+                if (j0 + VE <= L) {
+#pragma unroll
+                    for (int e = 0; e < VE; ++e) v[k][e] *= c;
+                } else {
+#pragma unroll
+                    for (int e = 0; e < VE; ++e) v[k][e] = (j0 + e < L) ? v[k][e] * c : -INFINITY;
+                }
+            } else {
+#pragma unroll
+                for (int e = 0; e < VE; ++e) v[k][e] = -INFINITY;
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < HI; ++i) {
+            const int jh = lane + 32 * i;
+            hv[i] = (jh < hd && jh < L)
+                        ? Elem<T>::to_f(*reinterpret_cast<const T*>(slot + off + jh * E)) * c
+                        : -INFINITY;
+            const int jt = tl0 + lane + 32 * i;
+            tv[i] = (jt < Sk && jt < L)
+                        ? Elem<T>::to_f(*reinterpret_cast<const T*>(body + 16 * nb +
+                                                                    (jt - tl0) * E)) * c
+                        : -INFINITY;
+        }
+
+        // ---- SM-3: row max (consumes every staged value)
+        float m[1];
+        {
+            float a = -INFINITY;
+#pragma unroll
+            for (int k = 0; k < NV; ++k)
+#pragma unroll
+                for (int e = 0; e < VE; ++e) a = fmaxf(a, v[k][e]);
+#pragma unroll
+            for (int i = 0; i < HI; ++i) a = fmaxf(a, fmaxf(hv[i], tv[i]));
+            m[0] = a;
+        }
+        group_max<32, 1>(m, nullptr);
+
+        // slot consumed: refill it with the row D iterations ahead
+        __syncwarp();
+        if (lane == 0) {
+            fence_proxy_async_smem();
+            issue(row + (int64_t)D * TW, sl);
+        }
+        if (++sl == D) {
+            sl = 0;
+            ph ^= 1;
+        }
+
+        // ---- SM-4: exponentiate once, sum
+        const float mm = (m[0] == -INFINITY) ? 0.f : m[0];
+        float s[1] = {0.f};
+#pragma unroll
+        for (int k = 0; k < NV; ++k)
+#pragma unroll
+            for (int e = 0; e < VE; ++e) {
+                v[k][e] = ex2_approx(v[k][e] - mm);
+                s[0] += v[k][e];
+            }
+#pragma unroll
+        for (int i = 0; i < HI; ++i) {
+            hv[i] = ex2_approx(hv[i] - mm);
+            tv[i] = ex2_approx(tv[i] - mm);
+            s[0] += hv[i] + tv[i];
+        }
+        group_sum<32, 1>(s, nullptr);
+
+        // ---- SM-5: normalise, +0.0 for padding keys, store every column
+        const float inv = 1.0f / s[0];
+#pragma unroll
+        for (int k = 0; k < NV; ++k) {
+            const int ci = lane + 32 * k;
+            if (ci < nb) {
+                const int j0 = hd + ci * VE;
+                float y[VE];
+                if (j0 + VE <= L) {
+#pragma unroll
+                    for (int e = 0; e < VE; ++e) y[e] = v[k][e] * inv;
+                } else {
+#pragma unroll
+                    for (int e = 0; e < VE; ++e) y[e] = (j0 + e < L) ? v[k][e] * inv : 0.f;
+                }
+                Raw<16> w;
+                Elem<T>::template pack<16>(y, w);
+                st_stream<16>(p + j0, w);
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < HI; ++i) {
+            const int jh = lane + 32 * i;
+            if (jh < hd) p[jh] = Elem<T>::from_f(jh < L ? hv[i] * inv : 0.f);
+            const int jt = tl0 + lane + 32 * i;
+            if (jt < Sk) p[jt] = Elem<T>::from_f(jt < L ? tv[i] * inv : 0.f);
+        }
+    }
+}
+
+namespace {
+
+int sm_count() {
+    static int cached[64] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) dev = 0;
+    if (!cached[dev]) {
+        int n = 0;
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        cached[dev] = n > 0 ? n : 148;
+    }
+    return cached[dev];
+}
+
+// Ring depth: about 4 KB of rows in flight per warp, 2..8 slots.
+int tma_depth(int slot_bytes) { return max(2, min(8, 4096 / slot_bytes + 1)); }
+
+template <typename T, int NV, int NW>
+cudaError_t launch_softmax_tma(void* scores, const int32_t* lengths, int64_t nrows, int64_t rpb,
+                               int Sk, float scale, cudaStream_t st) {
+    auto kern = softmax_tma_kernel<T, NV, NW>;
+    const int slot_bytes = ((Sk * (int)sizeof(T) + 32) + 127) & ~127;
+    const int D = tma_depth(slot_bytes);
+    const size_t smem = (size_t)((NW * D * 8 + 127) & ~127) + (size_t)NW * D * slot_bytes;
+    static std::atomic<int> attr_done{0};
+    if (smem > 48 * 1024 && attr_done.load() < (int)smem) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+        if (e != cudaSuccess) return e;
+        attr_done.store((int)smem);
+    }
+    int occ = 0;
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NW * 32, smem);
+    if (e != cudaSuccess) return e;
+    occ = max(occ, 1);
+    const int64_t need = (nrows + NW - 1) / NW;
+    const int64_t cap = (int64_t)sm_count() * occ;
+    const int64_t grid = need < cap ? need : cap;
+    kern<<<(unsigned)grid, NW * 32, smem, st>>>(static_cast<T*>(scores), lengths, nrows, rpb, Sk,
+                                                scale * kLog2e, D, slot_bytes);
+    return cudaGetLastError();
+}
+
+}  // namespace
 
 // ----------------------------------------------------------------------------
 // Tier table.  Selection is by (dtype, Sk) only; per-row lengths only shorten
@@ -190,6 +424,12 @@ struct SoftmaxTier {
             "softmax_rows<" TN ",V" #VB ",G" #G ",NV" #NV ",R" #R ",T" #NT ",M" #MINB ">" \
     }
 
+#define TT_SM_TMA(AUTO, T, TN, NV, NW)                                                     \
+    SoftmaxTier {                                                                          \
+        32 * (NV) * (16 / (int)sizeof(T)), AUTO, &launch_softmax_tma<T, NV, NW>,           \
+            "softmax_tma<" TN ",V16,G32,NV" #NV ",W" #NW ">"                              \
+    }
+
 // Automatic tiers are ordered by max_cols; the first that fits is used.
 // Short rows use 16-byte vectors so that more lanes carry bytes; rows of
 // >= 256 B use 32-byte vectors (LDG.256).  Sub-warp groups handle many short
@@ -210,7 +450,9 @@ struct SoftmaxTier {
     TT_SM_TIER(false, T, TN, 32, 32, 1, 2, 256, 4), TT_SM_TIER(false, T, TN, 32, 32, 1, 1, 256, 6), \
     TT_SM_TIER(false, T, TN, 32, 32, 1, 2, 512, 2), TT_SM_TIER(false, T, TN, 16, 32, 2, 1, 256, 1), \
     TT_SM_TIER(false, T, TN, 16, 32, 2, 2, 256, 1), TT_SM_TIER(false, T, TN, 32, 32, 1, 4, 128, 2), \
-    TT_SM_TIER(false, T, TN, 32, 32, 2, 2, 256, 1), TT_SM_TIER(false, T, TN, 32, 32, 2, 1, 128, 1)
+    TT_SM_TIER(false, T, TN, 32, 32, 2, 2, 256, 1), TT_SM_TIER(false, T, TN, 32, 32, 2, 1, 128, 1), \
+    TT_SM_TMA(false, T, TN, 2, 8), TT_SM_TMA(false, T, TN, 2, 4), TT_SM_TMA(false, T, TN, 4, 8),     \
+    TT_SM_TMA(false, T, TN, 4, 4), TT_SM_TMA(false, T, TN, 8, 4), TT_SM_TMA(false, T, TN, 1, 8)
 
 const SoftmaxTier kSm_f32[] = {TT_SM_LIST(float, "f32", 4)};
 const SoftmaxTier kSm_f16[] = {TT_SM_LIST(__half, "f16", 2)};
