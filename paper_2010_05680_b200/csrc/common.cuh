@@ -272,6 +272,31 @@ __device__ __forceinline__ void group_sum(float (&v)[R], float* smem) {
 }
 
 // ----------------------------------------------------------------------------
+// Division of a 32-bit row index by a runtime constant (rows per batch) with a
+// multiply-high and two shifts instead of the ~25-instruction integer divide:
+// the round-up magic-number method (Granlund & Montgomery), exact for every
+// n < 2^32 and 1 <= d < 2^31.
+// ----------------------------------------------------------------------------
+struct FastDivU32 {
+    uint32_t d, m, s;
+    static FastDivU32 make(uint32_t d) {
+        FastDivU32 f{d, 0u, 0u};
+        if (d > 1) {
+            uint32_t l = 0;
+            while ((1ull << l) < d) ++l;                         // l = ceil(log2 d)
+            f.m = (uint32_t)((((1ull << l) - d) << 32) / d + 1);
+            f.s = l;
+        }
+        return f;
+    }
+    __device__ __forceinline__ uint32_t div(uint32_t n) const {
+        if (d == 1) return n;
+        const uint32_t t = __umulhi(n, m);
+        return (t + ((n - t) >> 1)) >> (s - 1);
+    }
+};
+
+// ----------------------------------------------------------------------------
 // 1-D TMA (cp.async.bulk, SASS UBLKCP) + mbarrier helpers.  A bulk copy moves
 // a 16-byte-aligned, 16-byte-multiple span global -> shared and signals the
 // slot's mbarrier with complete_tx; the consumer waits on the barrier phase.

@@ -146,6 +146,116 @@ __global__ void __launch_bounds__(NT, MINB)
 
 
 // ----------------------------------------------------------------------------
+// Warp / sub-warp tier (G <= 32, VB >= 16), the production path for hidden up
+// to 32 * NV * VE.  Persistent CTAs; per CTA, bias / gamma / beta are widened
+// to fp32 ONCE into shared memory in a lane-interleaved layout (quad j of
+// chunk c at float4 index (p * VE/4 + j) * nvec + c, so a warp's LDS.128 are
+// conflict-free), which removes their per-row global loads and conversions.
+// Per row: x and residual vector loads, v = (x + bias) + residual, shifted
+// mean, centred variance (d = v - mean kept in the same registers), then
+// y = d * rstd * gamma + beta.
+// ----------------------------------------------------------------------------
+template <typename T, int VB, int G, int NV, int NT, int MINB>
+__global__ void __launch_bounds__(NT, MINB)
+    ln_warp_kernel(T* out, const T* x, const T* residual, const T* __restrict__ bias,
+                   const T* __restrict__ gamma, const T* __restrict__ beta, uint32_t rows,
+                   int hidden, float eps) {
+    constexpr int VE = VB / (int)sizeof(T);
+    constexpr int QV = VE / 4;  // float4 quads per vector
+    constexpr int GPB = NT / G;
+    static_assert(G <= 32 && VE % 4 == 0, "warp tier with >= 4-element vectors");
+    extern __shared__ __align__(16) float4 prm[];  // [3][QV][nvec] float4
+    const int nvec = hidden / VE;
+    const float invN = 1.0f / (float)hidden;
+
+    // stage the three parameter vectors as fp32 (once per persistent CTA)
+    for (int i = threadIdx.x; i < 3 * hidden; i += NT) {
+        const int pi = i / hidden, col = i - pi * hidden;
+        const T* src = pi == 0 ? bias : pi == 1 ? gamma : beta;
+        const int c = col / VE, e = col - c * VE;
+        reinterpret_cast<float*>(prm)[(((pi * QV + (e >> 2)) * nvec + c) << 2) + (e & 3)] =
+            Elem<T>::to_f(src[col]);
+    }
+    __syncthreads();
+    const float4* pb = prm;
+    const float4* pg = prm + QV * nvec;
+    const float4* pe = prm + 2 * QV * nvec;
+
+    const int q = threadIdx.x % G;
+    const uint32_t stride = gridDim.x * GPB;
+    for (uint32_t row = blockIdx.x * GPB + threadIdx.x / G; row < rows; row += stride) {
+        const size_t off = (size_t)row * (size_t)hidden;
+        // ---- LN-1
+        float v[NV][VE];
+#pragma unroll
+        for (int k = 0; k < NV; ++k) {
+            const int vi = q + k * G;
+            if (vi < nvec) {
+                Raw<VB> wx, wr;
+                ld_stream<VB>(x + off + vi * VE, wx);
+                ld_stream<VB>(residual + off + vi * VE, wr);
+                float fr[VE];
+                Elem<T>::template unpack<VB>(wx, v[k]);
+                Elem<T>::template unpack<VB>(wr, fr);
+#pragma unroll
+                for (int j = 0; j < QV; ++j) {
+                    const float4 b = pb[j * nvec + vi];
+                    v[k][4 * j + 0] = (v[k][4 * j + 0] + b.x) + fr[4 * j + 0];
+                    v[k][4 * j + 1] = (v[k][4 * j + 1] + b.y) + fr[4 * j + 1];
+                    v[k][4 * j + 2] = (v[k][4 * j + 2] + b.z) + fr[4 * j + 2];
+                    v[k][4 * j + 3] = (v[k][4 * j + 3] + b.w) + fr[4 * j + 3];
+                }
+            } else {
+#pragma unroll
+                for (int e = 0; e < VE; ++e) v[k][e] = 0.f;
+            }
+        }
+        // ---- LN-2: shifted mean, centred variance
+        float sh[1] = {__shfl_sync(0xffffffffu, v[0][0], (int)(threadIdx.x & 31) & ~(G - 1))};
+        float mean[1] = {0.f};
+#pragma unroll
+        for (int k = 0; k < NV; ++k)
+            if (q + k * G < nvec) {
+#pragma unroll
+                for (int e = 0; e < VE; ++e) mean[0] += v[k][e] - sh[0];
+            }
+        group_sum<G, 1>(mean, nullptr);
+        const float mu = fmaf(mean[0], invN, sh[0]);
+        float var[1] = {0.f};
+#pragma unroll
+        for (int k = 0; k < NV; ++k)
+            if (q + k * G < nvec) {
+#pragma unroll
+                for (int e = 0; e < VE; ++e) {
+                    v[k][e] -= mu;
+                    var[0] = fmaf(v[k][e], v[k][e], var[0]);
+                }
+            }
+        group_sum<G, 1>(var, nullptr);
+        const float rstd = rsqrtf(var[0] * invN + eps);
+        // ---- LN-3
+#pragma unroll
+        for (int k = 0; k < NV; ++k) {
+            const int vi = q + k * G;
+            if (vi < nvec) {
+                float y[VE];
+#pragma unroll
+                for (int j = 0; j < QV; ++j) {
+                    const float4 g = pg[j * nvec + vi], b = pe[j * nvec + vi];
+                    y[4 * j + 0] = fmaf(v[k][4 * j + 0] * rstd, g.x, b.x);
+                    y[4 * j + 1] = fmaf(v[k][4 * j + 1] * rstd, g.y, b.y);
+                    y[4 * j + 2] = fmaf(v[k][4 * j + 2] * rstd, g.z, b.z);
+                    y[4 * j + 3] = fmaf(v[k][4 * j + 3] * rstd, g.w, b.w);
+                }
+                Raw<VB> wy;
+                Elem<T>::template pack<VB>(y, wy);
+                st_stream<VB>(out + off + vi * VE, wy);
+            }
+        }
+    }
+}
+
+// ----------------------------------------------------------------------------
 // TMA-staged variant (warp per row, 16-byte chunks): persistent kernel, each
 // warp streams its rows' x and residual through a private ring of D shared-
 // memory slots filled by 1-D bulk copies (cp.async.bulk) issued D rows ahead.
@@ -326,6 +436,38 @@ cudaError_t launch_ln(void* out, const void* x, const void* res, const void* bia
     return cudaGetLastError();
 }
 
+
+template <typename T, int VB, int G, int NV, int NT, int MINB>
+cudaError_t launch_ln_warp(void* out, const void* x, const void* res, const void* bias,
+                           const void* gamma, const void* beta, int64_t rows, int hidden,
+                           float eps, cudaStream_t st) {
+    constexpr int GPB = NT / G;
+    if (rows >= (int64_t)0xffffffffLL)
+        return launch_ln<T, VB, G, NV, 1, NT, MINB>(out, x, res, bias, gamma, beta, rows, hidden,
+                                                    eps, st);
+    auto kern = ln_warp_kernel<T, VB, G, NV, NT, MINB>;
+    const size_t smem = (size_t)3 * hidden * sizeof(float);
+    static std::atomic<int> attr_done{0};
+    if (smem > 48 * 1024 && attr_done.load() < (int)smem) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+        if (e != cudaSuccess) return e;
+        attr_done.store((int)smem);
+    }
+    int occ = 0;
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT, smem);
+    if (e != cudaSuccess) return e;
+    occ = occ > 0 ? occ : 1;
+    const int64_t need = (rows + GPB - 1) / GPB;
+    const int64_t cap = (int64_t)sm_count() * occ;
+    const int64_t grid = need < cap ? need : cap;
+    kern<<<(unsigned)grid, NT, smem, st>>>(
+        static_cast<T*>(out), static_cast<const T*>(x), static_cast<const T*>(res),
+        static_cast<const T*>(bias), static_cast<const T*>(gamma), static_cast<const T*>(beta),
+        (uint32_t)rows, hidden, eps);
+    return cudaGetLastError();
+}
+
 using LnFn = cudaError_t (*)(void*, const void*, const void*, const void*, const void*,
                              const void*, int64_t, int, float, cudaStream_t);
 
@@ -345,6 +487,13 @@ struct LnTier {
             "ln_rows<" TN ",V" #VB ",G" #G ",NV" #NV ",R" #R ",T" #NT ",M" #MINB ">"      \
     }
 
+#define TT_LN_WARP(AUTO, T, TN, VB, G, NV, NT, MINB)                                      \
+    LnTier {                                                                               \
+        VB, (VB) / (int)sizeof(T), (G) * (NV) * ((VB) / (int)sizeof(T)), AUTO,             \
+            &launch_ln_warp<T, VB, G, NV, NT, MINB>,                                       \
+            "ln_warp<" TN ",V" #VB ",G" #G ",NV" #NV ",T" #NT ",M" #MINB ">"              \
+    }
+
 #define TT_LN_TMA(AUTO, T, TN, NV, NW)                                                     \
     LnTier {                                                                               \
         16, 16 / (int)sizeof(T), 32 * (NV) * (16 / (int)sizeof(T)), AUTO,                 \
@@ -355,15 +504,15 @@ struct LnTier {
 // only serve hidden sizes whose row pitch is not a multiple of 16 bytes.
 // NVC32 / NVC16 = CTA-tier vectors per thread (NV * VE = 32 registers of row
 // data).  Non-automatic entries are tuning candidates (tt_tune.h).
-#define TT_LN_LIST(T, TN, SB, NVC32, NVC16)                                                  \
-    TT_LN_TIER(true, T, TN, 16, 4, 1, 2, 256, 1), TT_LN_TIER(true, T, TN, 16, 8, 1, 2, 256, 1), \
-    TT_LN_TIER(true, T, TN, 16, 16, 1, 2, 256, 1), TT_LN_TIER(true, T, TN, 16, 32, 1, 2, 256, 1), \
-    TT_LN_TIER(true, T, TN, 16, 32, 2, 2, 256, 1), TT_LN_TIER(true, T, TN, 16, 32, 3, 1, 256, 1), \
-    TT_LN_TIER(true, T, TN, 16, 32, 4, 1, 256, 1), TT_LN_TIER(true, T, TN, 16, 32, 6, 1, 256, 1), \
-    TT_LN_TIER(true, T, TN, 16, 32, 8, 1, 256, 1), TT_LN_TIER(true, T, TN, 32, 4, 1, 2, 256, 1), \
-    TT_LN_TIER(true, T, TN, 32, 8, 1, 2, 256, 1), TT_LN_TIER(true, T, TN, 32, 16, 1, 2, 256, 1), \
-    TT_LN_TIER(true, T, TN, 32, 32, 1, 2, 256, 1), TT_LN_TIER(true, T, TN, 32, 32, 2, 1, 256, 1), \
-    TT_LN_TIER(true, T, TN, 32, 32, 3, 1, 256, 1), TT_LN_TIER(true, T, TN, 32, 32, 4, 1, 256, 1), \
+#define TT_LN_LIST(T, TN, SB, NVC32, NVC16, MA, MB, MC)                                       \
+    TT_LN_WARP(true, T, TN, 16, 4, 1, 256, 4), TT_LN_WARP(true, T, TN, 16, 8, 1, 256, 4),       \
+    TT_LN_WARP(true, T, TN, 16, 16, 1, 256, 4), TT_LN_WARP(true, T, TN, 16, 32, 1, 256, 4),     \
+    TT_LN_WARP(true, T, TN, 16, 32, 2, 256, MA), TT_LN_WARP(true, T, TN, 16, 32, 3, 256, MB),   \
+    TT_LN_WARP(true, T, TN, 16, 32, 4, 256, MB), TT_LN_WARP(true, T, TN, 16, 32, 6, 256, MC),   \
+    TT_LN_WARP(true, T, TN, 16, 32, 8, 256, MC), TT_LN_WARP(true, T, TN, 32, 4, 1, 256, 4),     \
+    TT_LN_WARP(true, T, TN, 32, 8, 1, 256, 4), TT_LN_WARP(true, T, TN, 32, 16, 1, 256, 4),      \
+    TT_LN_WARP(true, T, TN, 32, 32, 1, 256, MA), TT_LN_WARP(true, T, TN, 32, 32, 2, 256, MB),   \
+    TT_LN_WARP(true, T, TN, 32, 32, 3, 256, MC), TT_LN_WARP(true, T, TN, 32, 32, 4, 256, MC),   \
     TT_LN_TIER(true, T, TN, 16, 128, NVC16, 1, 128, 1), TT_LN_TIER(true, T, TN, 16, 256, NVC16, 1, 256, 1), \
     TT_LN_TIER(true, T, TN, 16, 512, NVC16, 1, 512, 1), TT_LN_TIER(true, T, TN, 16, 1024, NVC16, 1, 1024, 1), \
     TT_LN_TIER(true, T, TN, 32, 128, NVC32, 1, 128, 1), TT_LN_TIER(true, T, TN, 32, 256, NVC32, 1, 256, 1), \
@@ -371,17 +520,23 @@ struct LnTier {
     TT_LN_TIER(true, T, TN, SB, 32, 1, 1, 256, 1), TT_LN_TIER(true, T, TN, SB, 32, 4, 1, 256, 1), \
     TT_LN_TIER(true, T, TN, SB, 32, 16, 1, 256, 1), TT_LN_TIER(true, T, TN, SB, 256, 16, 1, 256, 1), \
     TT_LN_TIER(true, T, TN, SB, 1024, 32, 1, 1024, 1),                                      \
-    TT_LN_TIER(false, T, TN, 32, 32, 2, 2, 256, 1), TT_LN_TIER(false, T, TN, 32, 32, 2, 1, 128, 1), \
-    TT_LN_TIER(false, T, TN, 32, 32, 2, 1, 256, 4), \
-    TT_LN_TIER(false, T, TN, 16, 32, 4, 2, 256, 1), TT_LN_TIER(false, T, TN, 32, 32, 2, 2, 128, 2), \
-    TT_LN_TIER(false, T, TN, 32, 32, 3, 2, 256, 1), TT_LN_TIER(false, T, TN, 32, 32, 3, 1, 128, 1), \
-    TT_LN_TIER(false, T, TN, 16, 32, 3, 2, 256, 1), \
+    TT_LN_TIER(false, T, TN, 32, 32, 2, 1, 256, 1), TT_LN_TIER(false, T, TN, 32, 32, 2, 1, 128, 6), \
+    TT_LN_TIER(false, T, TN, 16, 32, 3, 1, 256, 1), TT_LN_TIER(false, T, TN, 32, 32, 3, 1, 256, 1), \
     TT_LN_TMA(false, T, TN, 3, 8), TT_LN_TMA(false, T, TN, 4, 8), TT_LN_TMA(false, T, TN, 4, 4),       \
-    TT_LN_TMA(false, T, TN, 6, 4), TT_LN_TMA(false, T, TN, 8, 4), TT_LN_TMA(false, T, TN, 2, 8)
+    TT_LN_TMA(false, T, TN, 6, 4), TT_LN_TMA(false, T, TN, 8, 4), TT_LN_TMA(false, T, TN, 2, 8),       \
+    TT_LN_WARP(false, T, TN, 32, 32, 2, 256, 3), TT_LN_WARP(false, T, TN, 32, 32, 2, 256, 5),   \
+    TT_LN_WARP(false, T, TN, 32, 32, 2, 256, 6), TT_LN_WARP(false, T, TN, 32, 32, 2, 128, 8),   \
+    TT_LN_WARP(false, T, TN, 32, 32, 2, 128, 12), TT_LN_WARP(false, T, TN, 32, 32, 3, 128, 6),  \
+    TT_LN_WARP(false, T, TN, 32, 32, 3, 256, 5), TT_LN_WARP(false, T, TN, 16, 32, 3, 256, 3),   \
+    TT_LN_WARP(false, T, TN, 16, 32, 3, 256, 5), TT_LN_WARP(false, T, TN, 16, 32, 3, 128, 8),   \
+    TT_LN_WARP(false, T, TN, 16, 32, 4, 256, 3), TT_LN_WARP(false, T, TN, 16, 32, 4, 256, 5),   \
+    TT_LN_WARP(false, T, TN, 32, 32, 4, 128, 6)
 
-const LnTier kLn_f32[] = {TT_LN_LIST(float, "f32", 4, 4, 8)};
-const LnTier kLn_f16[] = {TT_LN_LIST(__half, "f16", 2, 2, 4)};
-const LnTier kLn_bf16[] = {TT_LN_LIST(__nv_bfloat16, "bf16", 2, 2, 4)};
+// MA / MB / MC: min CTAs/SM (register cap) for warp tiers holding about
+// 16 / 24-32 / 48-64 fp32 row values per lane.
+const LnTier kLn_f32[] = {TT_LN_LIST(float, "f32", 4, 4, 8, 6, 4, 3)};
+const LnTier kLn_f16[] = {TT_LN_LIST(__half, "f16", 2, 2, 4, 4, 4, 2)};
+const LnTier kLn_bf16[] = {TT_LN_LIST(__nv_bfloat16, "bf16", 2, 2, 4, 4, 4, 2)};
 constexpr int kLnN = (int)(sizeof(kLn_f32) / sizeof(kLn_f32[0]));
 
 std::atomic<int> g_force[3] = {{-1}, {-1}, {-1}};

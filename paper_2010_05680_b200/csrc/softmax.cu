@@ -167,6 +167,173 @@ __global__ void __launch_bounds__(NT, MINB) softmax_rows_kernel(T* __restrict__ 
 
 
 // ----------------------------------------------------------------------------
+// Warp / sub-warp tier (G <= 32), the production path for rows up to
+// 32 * NV * VE keys.  Persistent grid-stride loop over rows; per row:
+//   * the next row's length is fetched one iteration ahead (its latency is off
+//     the load -> compute chain),
+//   * the row index is divided by H*Sq with a multiply-high (FastDivU32),
+//   * the max is taken over the RAW values (max if scale >= 0, min otherwise),
+//     so the exponent is one FFMA: e = 2^(x*c - m*c),
+//   * full vectors (all keys valid, the common case) carry no per-element
+//     masking; only the vector that straddles L selects,
+//   * ALIGNED (row pitch and base are multiples of VB) drops the scalar head /
+//     tail code entirely.
+// ----------------------------------------------------------------------------
+template <typename T, int VB, int G, int NV, int NT, int MINB, bool ALIGNED>
+__global__ void __launch_bounds__(NT, MINB) softmax_warp_kernel(T* __restrict__ scores,
+                                                                const int32_t* __restrict__ lengths,
+                                                                uint32_t nrows, FastDivU32 rpb,
+                                                                int Sk, float c) {
+    constexpr int VE = VB / (int)sizeof(T);
+    constexpr int HI = ALIGNED ? 0 : (VE - 1 + G - 1) / G;
+    constexpr int HIA = HI > 0 ? HI : 1;
+    constexpr int GPB = NT / G;
+    static_assert(G <= 32, "warp tier");
+
+    const int q = threadIdx.x % G;
+    const uint32_t stride = gridDim.x * GPB;
+    uint32_t row = blockIdx.x * GPB + threadIdx.x / G;
+    const bool up = c >= 0.f;                 // max of raw x (else min)
+    const float sent = up ? -INFINITY : INFINITY;
+
+    auto len_of = [&](uint32_t r) {
+        return min(max(__ldg(lengths + rpb.div(r)), 0), Sk);
+    };
+    int Lnext = row < nrows ? len_of(row) : 0;
+
+    for (; row < nrows; row += stride) {
+        const int L = Lnext;
+        if (row + stride < nrows) Lnext = len_of(row + stride);
+        T* p = scores + (size_t)row * (size_t)Sk;
+        int hd = 0, nv = Sk / VE;
+        if constexpr (!ALIGNED) {
+            const int mis = (int)((reinterpret_cast<uintptr_t>(p) & (VB - 1)) / sizeof(T));
+            hd = mis ? min(VE - mis, Sk) : 0;
+            nv = (Sk - hd) / VE;
+        }
+
+        // ---- SM-2: load the valid prefix (raw values)
+        float v[NV][VE];
+        bool full[NV];
+#pragma unroll
+        for (int k = 0; k < NV; ++k) {
+            const int vi = q + k * G;
+            const int j0 = hd + vi * VE;
+            full[k] = (vi < nv) && (j0 + VE <= L);
+            if (vi < nv && j0 < L) {
+                Raw<VB> w;
+                ld_stream<VB>(p + j0, w);
+                Elem<T>::template unpack<VB>(w, v[k]);
+                if (!full[k]) {
+#pragma unroll
+                    for (int e = 0; e < VE; ++e)
+                        if (j0 + e >= L) v[k][e] = sent;
+                }
+            } else {
+#pragma unroll
+                for (int e = 0; e < VE; ++e) v[k][e] = sent;
+            }
+        }
+        float hv[HIA], tv[HIA];
+        const int tl0 = hd + nv * VE;
+        if constexpr (!ALIGNED) {
+#pragma unroll
+            for (int i = 0; i < HI; ++i) {
+                const int jh = q + i * G;
+                hv[i] = (jh < hd && jh < L) ? Elem<T>::to_f(p[jh]) : sent;
+                const int jt = tl0 + q + i * G;
+                tv[i] = (jt < Sk && jt < L) ? Elem<T>::to_f(p[jt]) : sent;
+            }
+        }
+
+        // ---- SM-3: row max of the scaled logits, c * (max or min of raw x)
+        float m[1];
+        {
+            float a = sent;
+            if (up) {
+#pragma unroll
+                for (int k = 0; k < NV; ++k)
+#pragma unroll
+                    for (int e = 0; e < VE; ++e) a = fmaxf(a, v[k][e]);
+                if constexpr (!ALIGNED) {
+#pragma unroll
+                    for (int i = 0; i < HI; ++i) a = fmaxf(a, fmaxf(hv[i], tv[i]));
+                }
+            } else {
+#pragma unroll
+                for (int k = 0; k < NV; ++k)
+#pragma unroll
+                    for (int e = 0; e < VE; ++e) a = fminf(a, v[k][e]);
+                if constexpr (!ALIGNED) {
+#pragma unroll
+                    for (int i = 0; i < HI; ++i) a = fminf(a, fminf(hv[i], tv[i]));
+                }
+            }
+            m[0] = up ? a : -a;
+        }
+        group_max<G, 1>(m, nullptr);
+        const float mr = up ? m[0] : -m[0];
+        float nm = -(mr * c);                       // -max_j (c * x_j)
+        if (!(fabsf(nm) <= 3.0e38f)) nm = 0.f;      // empty row (L = 0): no valid key
+
+        // ---- SM-4: e_j = 2^(c x_j - m), once; s = sum e_j
+        float s[1] = {0.f};
+#pragma unroll
+        for (int k = 0; k < NV; ++k) {
+            const int j0 = hd + (q + k * G) * VE;
+            if (full[k]) {
+#pragma unroll
+                for (int e = 0; e < VE; ++e) {
+                    v[k][e] = ex2_approx(fmaf(v[k][e], c, nm));
+                    s[0] += v[k][e];
+                }
+            } else {
+#pragma unroll
+                for (int e = 0; e < VE; ++e) {
+                    v[k][e] = (j0 + e < L) ? ex2_approx(fmaf(v[k][e], c, nm)) : 0.f;
+                    s[0] += v[k][e];
+                }
+            }
+        }
+        if constexpr (!ALIGNED) {
+#pragma unroll
+            for (int i = 0; i < HI; ++i) {
+                const int jh = q + i * G, jt = tl0 + q + i * G;
+                hv[i] = (jh < hd && jh < L) ? ex2_approx(fmaf(hv[i], c, nm)) : 0.f;
+                tv[i] = (jt < Sk && jt < L) ? ex2_approx(fmaf(tv[i], c, nm)) : 0.f;
+                s[0] += hv[i] + tv[i];
+            }
+        }
+        group_sum<G, 1>(s, nullptr);
+        // masked keys hold e = +0.0, so y = e * inv is +0.0 there; L = 0 -> inv = 0
+        const float inv = s[0] > 0.f ? __fdividef(1.0f, s[0]) : 0.f;
+
+        // ---- SM-5: normalise and store every column
+#pragma unroll
+        for (int k = 0; k < NV; ++k) {
+            const int vi = q + k * G;
+            if (vi < nv) {
+                float y[VE];
+#pragma unroll
+                for (int e = 0; e < VE; ++e) y[e] = v[k][e] * inv;
+                Raw<VB> w;
+                Elem<T>::template pack<VB>(y, w);
+                st_stream<VB>(p + hd + vi * VE, w);
+            }
+        }
+        if constexpr (!ALIGNED) {
+#pragma unroll
+            for (int i = 0; i < HI; ++i) {
+                const int jh = q + i * G;
+                if (jh < hd) p[jh] = Elem<T>::from_f(hv[i] * inv);
+                const int jt = tl0 + q + i * G;
+                if (jt < Sk) p[jt] = Elem<T>::from_f(tv[i] * inv);
+            }
+        }
+    }
+}
+
+// ----------------------------------------------------------------------------
 // TMA-staged variant for warp-sized rows (G = 32): a persistent kernel where
 // every warp streams its rows through a private ring of D shared-memory slots.
 // Lane 0 issues one 1-D bulk copy (cp.async.bulk, SASS UBLKCP) per row, of the
@@ -407,6 +574,33 @@ cudaError_t launch_softmax(void* scores, const int32_t* lengths, int64_t nrows, 
     return cudaGetLastError();
 }
 
+
+template <typename T, int VB, int G, int NV, int NT, int MINB>
+cudaError_t launch_softmax_warp(void* scores, const int32_t* lengths, int64_t nrows, int64_t rpb,
+                                int Sk, float scale, cudaStream_t st) {
+    constexpr int GPB = NT / G;
+    if (nrows >= (int64_t)0xffffffffLL || rpb >= (int64_t)0x7fffffffLL)
+        return launch_softmax<T, VB, G, NV, 1, NT, MINB>(scores, lengths, nrows, rpb, Sk, scale, st);
+    const bool aligned = (reinterpret_cast<uintptr_t>(scores) % VB) == 0 &&
+                         ((int64_t)Sk * (int64_t)sizeof(T)) % VB == 0;
+    auto kern = aligned ? softmax_warp_kernel<T, VB, G, NV, NT, MINB, true>
+                        : softmax_warp_kernel<T, VB, G, NV, NT, MINB, false>;
+    static std::atomic<int> occ_cache[2] = {{0}, {0}};
+    int occ = occ_cache[aligned].load(std::memory_order_relaxed);
+    if (!occ) {
+        cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT, 0);
+        if (e != cudaSuccess) return e;
+        occ = occ > 0 ? occ : 1;
+        occ_cache[aligned].store(occ);
+    }
+    const int64_t need = (nrows + GPB - 1) / GPB;
+    const int64_t cap = (int64_t)sm_count() * occ;
+    const int64_t grid = need < cap ? need : cap;
+    kern<<<(unsigned)grid, NT, 0, st>>>(static_cast<T*>(scores), lengths, (uint32_t)nrows,
+                                       FastDivU32::make((uint32_t)rpb), Sk, scale * kLog2e);
+    return cudaGetLastError();
+}
+
 using SoftmaxFn = cudaError_t (*)(void*, const int32_t*, int64_t, int64_t, int, float,
                                   cudaStream_t);
 
@@ -424,6 +618,12 @@ struct SoftmaxTier {
             "softmax_rows<" TN ",V" #VB ",G" #G ",NV" #NV ",R" #R ",T" #NT ",M" #MINB ">" \
     }
 
+#define TT_SM_WARP(AUTO, T, TN, VB, G, NV, NT, MINB)                                      \
+    SoftmaxTier {                                                                          \
+        (G) * (NV) * ((VB) / (int)sizeof(T)), AUTO, &launch_softmax_warp<T, VB, G, NV, NT, MINB>, \
+            "softmax_warp<" TN ",V" #VB ",G" #G ",NV" #NV ",T" #NT ",M" #MINB ">"         \
+    }
+
 #define TT_SM_TMA(AUTO, T, TN, NV, NW)                                                     \
     SoftmaxTier {                                                                          \
         32 * (NV) * (16 / (int)sizeof(T)), AUTO, &launch_softmax_tma<T, NV, NW>,           \
@@ -437,26 +637,31 @@ struct SoftmaxTier {
 // parallelism.  CTA tiers keep NV * VE = 32 fp32 registers of row data per
 // thread so that a 1024-thread CTA fits the 64-register limit: NVC = 4 (fp32)
 // or 2 (16-bit).  Non-automatic entries are tuning candidates (tt_tune.h).
-#define TT_SM_LIST(T, TN, NVC)                                                               \
-    TT_SM_TIER(true, T, TN, 16, 4, 1, 2, 256, 1), TT_SM_TIER(true, T, TN, 16, 8, 1, 2, 256, 1), \
-    TT_SM_TIER(true, T, TN, 16, 16, 1, 2, 256, 1), TT_SM_TIER(true, T, TN, 32, 16, 1, 2, 256, 1), \
-    TT_SM_TIER(true, T, TN, 32, 32, 1, 2, 256, 1), TT_SM_TIER(true, T, TN, 32, 32, 2, 1, 256, 1), \
-    TT_SM_TIER(true, T, TN, 32, 32, 3, 1, 256, 1), TT_SM_TIER(true, T, TN, 32, 32, 4, 1, 256, 1), \
+#define TT_SM_LIST(T, TN, NVC, M2, M3, M4)                                                   \
+    TT_SM_WARP(true, T, TN, 16, 4, 1, 256, 6), TT_SM_WARP(true, T, TN, 16, 8, 1, 256, 6),       \
+    TT_SM_WARP(true, T, TN, 16, 16, 1, 256, 6), TT_SM_WARP(true, T, TN, 32, 16, 1, 256, 6),     \
+    TT_SM_WARP(true, T, TN, 32, 32, 1, 256, 6), TT_SM_WARP(true, T, TN, 32, 32, 2, 256, M2),    \
+    TT_SM_WARP(true, T, TN, 32, 32, 3, 256, M3), TT_SM_WARP(true, T, TN, 32, 32, 4, 256, M4),   \
     TT_SM_TIER(true, T, TN, 32, 64, NVC, 1, 64, 1), TT_SM_TIER(true, T, TN, 32, 128, NVC, 1, 128, 1), \
     TT_SM_TIER(true, T, TN, 32, 256, NVC, 1, 256, 1), TT_SM_TIER(true, T, TN, 32, 512, NVC, 1, 512, 1), \
     TT_SM_TIER(true, T, TN, 32, 1024, NVC, 1, 1024, 1),                                     \
-    TT_SM_TIER(false, T, TN, 32, 32, 1, 1, 256, 1), TT_SM_TIER(false, T, TN, 32, 32, 1, 4, 256, 1), \
-    TT_SM_TIER(false, T, TN, 32, 32, 1, 2, 128, 1), TT_SM_TIER(false, T, TN, 32, 32, 1, 1, 128, 1), \
-    TT_SM_TIER(false, T, TN, 32, 32, 1, 2, 256, 4), TT_SM_TIER(false, T, TN, 32, 32, 1, 1, 256, 6), \
-    TT_SM_TIER(false, T, TN, 32, 32, 1, 2, 512, 2), TT_SM_TIER(false, T, TN, 16, 32, 2, 1, 256, 1), \
-    TT_SM_TIER(false, T, TN, 16, 32, 2, 2, 256, 1), TT_SM_TIER(false, T, TN, 32, 32, 1, 4, 128, 2), \
-    TT_SM_TIER(false, T, TN, 32, 32, 2, 2, 256, 1), TT_SM_TIER(false, T, TN, 32, 32, 2, 1, 128, 1), \
+    TT_SM_TIER(false, T, TN, 32, 32, 1, 1, 256, 6), TT_SM_TIER(false, T, TN, 32, 32, 1, 2, 256, 1), \
+    TT_SM_TIER(false, T, TN, 32, 32, 2, 1, 256, 1), TT_SM_TIER(false, T, TN, 16, 32, 1, 2, 256, 1), \
     TT_SM_TMA(false, T, TN, 2, 8), TT_SM_TMA(false, T, TN, 2, 4), TT_SM_TMA(false, T, TN, 4, 8),     \
-    TT_SM_TMA(false, T, TN, 4, 4), TT_SM_TMA(false, T, TN, 8, 4), TT_SM_TMA(false, T, TN, 1, 8)
+    TT_SM_TMA(false, T, TN, 4, 4), TT_SM_TMA(false, T, TN, 8, 4), TT_SM_TMA(false, T, TN, 1, 8),     \
+    TT_SM_WARP(false, T, TN, 32, 32, 1, 256, 4), TT_SM_WARP(false, T, TN, 32, 32, 1, 256, 5),   \
+    TT_SM_WARP(false, T, TN, 32, 32, 1, 256, 7), TT_SM_WARP(false, T, TN, 32, 32, 1, 256, 8),   \
+    TT_SM_WARP(false, T, TN, 32, 32, 1, 128, 12), TT_SM_WARP(false, T, TN, 32, 32, 1, 128, 16), \
+    TT_SM_WARP(false, T, TN, 32, 32, 1, 512, 4), TT_SM_WARP(false, T, TN, 32, 32, 2, 256, 3),   \
+    TT_SM_WARP(false, T, TN, 32, 32, 2, 256, 5), TT_SM_WARP(false, T, TN, 32, 32, 2, 128, 10),  \
+    TT_SM_WARP(false, T, TN, 16, 32, 2, 256, 6), TT_SM_WARP(false, T, TN, 16, 32, 2, 256, 8),   \
+    TT_SM_WARP(false, T, TN, 16, 32, 1, 256, 8), TT_SM_WARP(false, T, TN, 32, 32, 3, 256, 2)
 
-const SoftmaxTier kSm_f32[] = {TT_SM_LIST(float, "f32", 4)};
-const SoftmaxTier kSm_f16[] = {TT_SM_LIST(__half, "f16", 2)};
-const SoftmaxTier kSm_bf16[] = {TT_SM_LIST(__nv_bfloat16, "bf16", 2)};
+// M2..M4: min CTAs/SM (register cap) of the NV = 2..4 warp tiers, chosen so
+// the row (NV * VE fp32 values per lane) fits without spilling.
+const SoftmaxTier kSm_f32[] = {TT_SM_LIST(float, "f32", 4, 6, 5, 4)};
+const SoftmaxTier kSm_f16[] = {TT_SM_LIST(__half, "f16", 2, 4, 3, 2)};
+const SoftmaxTier kSm_bf16[] = {TT_SM_LIST(__nv_bfloat16, "bf16", 2, 4, 3, 2)};
 constexpr int kSmN = (int)(sizeof(kSm_f32) / sizeof(kSm_f32[0]));
 
 std::atomic<int> g_force[3] = {{-1}, {-1}, {-1}};

@@ -1,0 +1,52 @@
+#!/usr/bin/env python
+"""Run one op N times with an optional forced tier -- a small target for ncu.
+
+  python tools/prof_one.py softmax bf16 64 16 512 512 [--tier NAME] [--reps 5]
+  python tools/prof_one.py layernorm bf16 32768 1024 [--tier NAME]
+"""
+import argparse
+import os
+import sys
+
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import paper_2010_05680_b200 as tt  # noqa: E402
+import workloads as W  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("op")
+    ap.add_argument("dtype")
+    ap.add_argument("dims", nargs="+", type=int)
+    ap.add_argument("--tier", default=None)
+    ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--ragged", action="store_true")
+    a = ap.parse_args()
+    dt = W.DTYPES[a.dtype]
+    if a.tier:
+        names = tt.tiers(a.op, dt)
+        tt.force_tier(a.op, dt, names.index(a.tier))
+    if a.op == "softmax":
+        B, H, Sq, Sk = a.dims
+        lens = W.lengths_ragged(B, Sk) if a.ragged else W.lengths_full(B, Sk)
+        x = W.scores(B, H, Sq, Sk, dt, device="cuda")
+        L = torch.as_tensor(lens).cuda()
+        print("tier:", tt.softmax_plan(dt, B, H, Sq, Sk))
+        for _ in range(a.reps):
+            tt.tt_softmax_masked(x, L, 0.125)
+    else:
+        rows, hidden = a.dims
+        d = W.ln_inputs(rows, hidden, dt, device="cuda")
+        out = torch.empty_like(d["x"])
+        print("tier:", tt.layernorm_plan(dt, rows, hidden))
+        for _ in range(a.reps):
+            tt.tt_add_bias_layernorm(out, d["x"], d["residual"], d["bias"], d["gamma"], d["beta"],
+                                     1e-12)
+    torch.cuda.synchronize()
+
+
+if __name__ == "__main__":
+    main()
