@@ -256,10 +256,14 @@ __global__ void __launch_bounds__(NT, MINB)
 }
 
 // ----------------------------------------------------------------------------
-// TMA-staged variant (warp per row, 16-byte chunks): persistent kernel, each
+// TMA-staged variant (warp per row, 16-byte chunks): persistent CTAs; each
 // warp streams its rows' x and residual through a private ring of D shared-
-// memory slots filled by 1-D bulk copies (cp.async.bulk) issued D rows ahead.
+// memory slots filled by 1-D bulk copies (cp.async.bulk, SASS UBLKCP) issued
+// D rows ahead, so the bytes in flight per SM are set by the ring, not by
+// the register file.  bias / gamma / beta are staged once per CTA as fp32 in
+// shared memory (lane-interleaved float4 layout, conflict-free LDS.128).
 // Requires hidden * sizeof(T) % 16 == 0 and 16-byte aligned operands.
+// Dynamic smem: [params 3*hidden fp32][NW*D mbarriers][NW*D slots].
 // ----------------------------------------------------------------------------
 template <typename T, int NV, int NW>
 __global__ void __launch_bounds__(NW * 32)
@@ -267,14 +271,18 @@ __global__ void __launch_bounds__(NW * 32)
                   const T* __restrict__ gamma, const T* __restrict__ beta, int64_t rows, int hidden,
                   float eps, int D, int slot_bytes) {
     constexpr int VE = 16 / (int)sizeof(T);
+    constexpr int QV = VE / 4;
     extern __shared__ __align__(128) unsigned char smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem) + warp * D;
-    unsigned char* ring = smem + ((NW * D * 8 + 127) & ~127) + (size_t)warp * D * slot_bytes;
+    const int nchunks = hidden / VE;
+    const size_t prm_bytes = ((size_t)3 * hidden * 4 + 127) & ~(size_t)127;
+    float4* prm = reinterpret_cast<float4*>(smem);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + prm_bytes) + warp * D;
+    unsigned char* ring = smem + prm_bytes + ((NW * D * 8 + 127) & ~127) +
+                          (size_t)warp * D * slot_bytes;
     const int64_t TW = (int64_t)gridDim.x * NW;
     const int64_t gw = (int64_t)blockIdx.x * NW + warp;
     const uint32_t rb = (uint32_t)hidden * (uint32_t)sizeof(T);  // row bytes, multiple of 16
-    const int nchunks = hidden / VE;
     const float invN = 1.0f / (float)hidden;
 
     auto issue = [&](int64_t row, int sl) {
@@ -290,7 +298,17 @@ __global__ void __launch_bounds__(NW * 32)
         fence_proxy_async_smem();
         for (int s = 0; s < D; ++s) issue(gw + s * TW, s);
     }
-    __syncwarp();
+    for (int i = threadIdx.x; i < 3 * hidden; i += NW * 32) {
+        const int pi = i / hidden, col = i - pi * hidden;
+        const T* src = pi == 0 ? bias : pi == 1 ? gamma : beta;
+        const int c = col / VE, e = col - c * VE;
+        reinterpret_cast<float*>(prm)[(((pi * QV + (e >> 2)) * nchunks + c) << 2) + (e & 3)] =
+            Elem<T>::to_f(src[col]);
+    }
+    __syncthreads();
+    const float4* pb = prm;
+    const float4* pg = prm + QV * nchunks;
+    const float4* pe = prm + 2 * QV * nchunks;
 
     int sl = 0;
     uint32_t ph = 0;
@@ -303,23 +321,27 @@ __global__ void __launch_bounds__(NW * 32)
         for (int k = 0; k < NV; ++k) {
             const int ci = lane + 32 * k;
             if (ci < nchunks) {
-                Raw<16> wx, wr, wb;
+                Raw<16> wx, wr;
                 lds128(slot + 16 * ci, wx.w);
                 lds128(slot + rb + 16 * ci, wr.w);
-                ld_param<16>(bias + ci * VE, wb);
-                float fr[VE], fb[VE];
+                float fr[VE];
                 Elem<T>::template unpack<16>(wx, v[k]);
                 Elem<T>::template unpack<16>(wr, fr);
-                Elem<T>::template unpack<16>(wb, fb);
 #pragma unroll
-                for (int e = 0; e < VE; ++e) v[k][e] = (v[k][e] + fb[e]) + fr[e];
+                for (int j = 0; j < QV; ++j) {
+                    const float4 b = pb[j * nchunks + ci];
+                    v[k][4 * j + 0] = (v[k][4 * j + 0] + b.x) + fr[4 * j + 0];
+                    v[k][4 * j + 1] = (v[k][4 * j + 1] + b.y) + fr[4 * j + 1];
+                    v[k][4 * j + 2] = (v[k][4 * j + 2] + b.z) + fr[4 * j + 2];
+                    v[k][4 * j + 3] = (v[k][4 * j + 3] + b.w) + fr[4 * j + 3];
+                }
             } else {
 #pragma unroll
                 for (int e = 0; e < VE; ++e) v[k][e] = 0.f;
             }
         }
-        // slot consumed (values are in registers once the shift is formed)
-        float shift[1] = {__shfl_sync(0xffffffffu, v[0][0], 0)};
+        float sh[1] = {__shfl_sync(0xffffffffu, v[0][0], 0)};
+        // slot consumed (values are in registers): refill it D rows ahead
         __syncwarp();
         if (lane == 0) {
             fence_proxy_async_smem();
@@ -335,18 +357,18 @@ __global__ void __launch_bounds__(NW * 32)
         for (int k = 0; k < NV; ++k)
             if (lane + 32 * k < nchunks) {
 #pragma unroll
-                for (int e = 0; e < VE; ++e) mean[0] += v[k][e] - shift[0];
+                for (int e = 0; e < VE; ++e) mean[0] += v[k][e] - sh[0];
             }
         group_sum<32, 1>(mean, nullptr);
-        const float mu = fmaf(mean[0], invN, shift[0]);
+        const float mu = fmaf(mean[0], invN, sh[0]);
         float var[1] = {0.f};
 #pragma unroll
         for (int k = 0; k < NV; ++k)
             if (lane + 32 * k < nchunks) {
 #pragma unroll
                 for (int e = 0; e < VE; ++e) {
-                    const float d = v[k][e] - mu;
-                    var[0] = fmaf(d, d, var[0]);
+                    v[k][e] -= mu;
+                    var[0] = fmaf(v[k][e], v[k][e], var[0]);
                 }
             }
         group_sum<32, 1>(var, nullptr);
@@ -357,14 +379,16 @@ __global__ void __launch_bounds__(NW * 32)
         for (int k = 0; k < NV; ++k) {
             const int ci = lane + 32 * k;
             if (ci < nchunks) {
-                Raw<16> wg, wb, wy;
-                ld_param<16>(gamma + ci * VE, wg);
-                ld_param<16>(beta + ci * VE, wb);
-                float fg[VE], fb[VE], y[VE];
-                Elem<T>::template unpack<16>(wg, fg);
-                Elem<T>::template unpack<16>(wb, fb);
+                float y[VE];
 #pragma unroll
-                for (int e = 0; e < VE; ++e) y[e] = fmaf((v[k][e] - mu) * rstd, fg[e], fb[e]);
+                for (int j = 0; j < QV; ++j) {
+                    const float4 g = pg[j * nchunks + ci], b = pe[j * nchunks + ci];
+                    y[4 * j + 0] = fmaf(v[k][4 * j + 0] * rstd, g.x, b.x);
+                    y[4 * j + 1] = fmaf(v[k][4 * j + 1] * rstd, g.y, b.y);
+                    y[4 * j + 2] = fmaf(v[k][4 * j + 2] * rstd, g.z, b.z);
+                    y[4 * j + 3] = fmaf(v[k][4 * j + 3] * rstd, g.w, b.w);
+                }
+                Raw<16> wy;
                 Elem<T>::template pack<16>(y, wy);
                 st_stream<16>(o + ci * VE, wy);
             }
@@ -387,15 +411,19 @@ int sm_count() {
     return cached[dev];
 }
 
-template <typename T, int NV, int NW>
+template <typename T, int NV, int NW, int KB>
 cudaError_t launch_ln_tma(void* out, const void* x, const void* res, const void* bias,
                           const void* gamma, const void* beta, int64_t rows, int hidden, float eps,
                           cudaStream_t st) {
     auto kern = ln_tma_kernel<T, NV, NW>;
     const int rb = hidden * (int)sizeof(T);
     const int slot_bytes = (2 * rb + 127) & ~127;
-    const int D = max(2, min(8, 8192 / slot_bytes + 1));
-    const size_t smem = (size_t)((NW * D * 8 + 127) & ~127) + (size_t)NW * D * slot_bytes;
+    // ring depth: about KB kilobytes of rows in flight per warp, 2..8 slots
+    const int D = max(2, min(8, (KB * 1024) / slot_bytes));
+    const size_t prm_bytes = ((size_t)3 * hidden * 4 + 127) & ~(size_t)127;
+    const size_t smem =
+        prm_bytes + (size_t)((NW * D * 8 + 127) & ~127) + (size_t)NW * D * slot_bytes;
+    if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
     static std::atomic<int> attr_done{0};
     if (smem > 48 * 1024 && attr_done.load() < (int)smem) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -494,11 +522,13 @@ struct LnTier {
             "ln_warp<" TN ",V" #VB ",G" #G ",NV" #NV ",T" #NT ",M" #MINB ">"              \
     }
 
-#define TT_LN_TMA(AUTO, T, TN, NV, NW)                                                     \
+#define TT_LN_TMA_K(AUTO, T, TN, NV, NW, KB)                                               \
     LnTier {                                                                               \
         16, 16 / (int)sizeof(T), 32 * (NV) * (16 / (int)sizeof(T)), AUTO,                 \
-            &launch_ln_tma<T, NV, NW>, "ln_tma<" TN ",V16,G32,NV" #NV ",W" #NW ">"        \
+            &launch_ln_tma<T, NV, NW, KB>,                                                 \
+            "ln_tma<" TN ",V16,G32,NV" #NV ",W" #NW ",K" #KB ">"                          \
     }
+#define TT_LN_TMA(AUTO, T, TN, NV, NW) TT_LN_TMA_K(AUTO, T, TN, NV, NW, 8)
 
 // Main tiers use 16- or 32-byte vectors; the scalar tiers (VB = sizeof(T))
 // only serve hidden sizes whose row pitch is not a multiple of 16 bytes.
@@ -530,7 +560,11 @@ struct LnTier {
     TT_LN_WARP(false, T, TN, 32, 32, 3, 256, 5), TT_LN_WARP(false, T, TN, 16, 32, 3, 256, 3),   \
     TT_LN_WARP(false, T, TN, 16, 32, 3, 256, 5), TT_LN_WARP(false, T, TN, 16, 32, 3, 128, 8),   \
     TT_LN_WARP(false, T, TN, 16, 32, 4, 256, 3), TT_LN_WARP(false, T, TN, 16, 32, 4, 256, 5),   \
-    TT_LN_WARP(false, T, TN, 32, 32, 4, 128, 6)
+    TT_LN_WARP(false, T, TN, 32, 32, 4, 128, 6),                                              \
+    TT_LN_TMA_K(false, T, TN, 4, 4, 12), TT_LN_TMA_K(false, T, TN, 4, 4, 16),                   \
+    TT_LN_TMA_K(false, T, TN, 4, 8, 12), TT_LN_TMA_K(false, T, TN, 3, 4, 12),                   \
+    TT_LN_TMA_K(false, T, TN, 3, 8, 12), TT_LN_TMA_K(false, T, TN, 8, 4, 12),                   \
+    TT_LN_TMA_K(false, T, TN, 4, 2, 16), TT_LN_TMA_K(false, T, TN, 3, 2, 16)
 
 // MA / MB / MC: min CTAs/SM (register cap) for warp tiers holding about
 // 16 / 24-32 / 48-64 fp32 row values per lane.

@@ -183,27 +183,32 @@ template <typename T, int VB, int G, int NV, int NT, int MINB, bool ALIGNED>
 __global__ void __launch_bounds__(NT, MINB) softmax_warp_kernel(T* __restrict__ scores,
                                                                 const int32_t* __restrict__ lengths,
                                                                 uint32_t nrows, FastDivU32 rpb,
-                                                                int Sk, float c) {
+                                                                int Sk, float c, int rpg) {
     constexpr int VE = VB / (int)sizeof(T);
     constexpr int HI = ALIGNED ? 0 : (VE - 1 + G - 1) / G;
     constexpr int HIA = HI > 0 ? HI : 1;
     constexpr int GPB = NT / G;
     static_assert(G <= 32, "warp tier");
 
+    // CTA b owns rows [b * GPB * rpg, (b + 1) * GPB * rpg); its groups walk them
+    // GPB rows at a time (adjacent groups on adjacent rows).  rpg trades the
+    // per-CTA setup and the length prefetch against load balance across CTAs
+    // when row costs vary (ragged lengths).
     const int q = threadIdx.x % G;
-    const uint32_t stride = gridDim.x * GPB;
-    uint32_t row = blockIdx.x * GPB + threadIdx.x / G;
+    const uint32_t stride = GPB;
+    uint32_t row = blockIdx.x * (uint32_t)(GPB * rpg) + threadIdx.x / G;
+    const uint32_t row_end = min(nrows, (blockIdx.x + 1) * (uint32_t)(GPB * rpg));
     const bool up = c >= 0.f;                 // max of raw x (else min)
     const float sent = up ? -INFINITY : INFINITY;
 
     auto len_of = [&](uint32_t r) {
         return min(max(__ldg(lengths + rpb.div(r)), 0), Sk);
     };
-    int Lnext = row < nrows ? len_of(row) : 0;
+    int Lnext = row < row_end ? len_of(row) : 0;
 
-    for (; row < nrows; row += stride) {
+    for (; row < row_end; row += stride) {
         const int L = Lnext;
-        if (row + stride < nrows) Lnext = len_of(row + stride);
+        if (row + stride < row_end) Lnext = len_of(row + stride);
         T* p = scores + (size_t)row * (size_t)Sk;
         int hd = 0, nv = Sk / VE;
         if constexpr (!ALIGNED) {
@@ -281,6 +286,7 @@ __global__ void __launch_bounds__(NT, MINB) softmax_warp_kernel(T* __restrict__ 
 #pragma unroll
         for (int k = 0; k < NV; ++k) {
             const int j0 = hd + (q + k * G) * VE;
+            const int lim = (q + k * G < nv) ? L : 0;  // keys of this vector that are valid
             if (full[k]) {
 #pragma unroll
                 for (int e = 0; e < VE; ++e) {
@@ -290,7 +296,7 @@ __global__ void __launch_bounds__(NT, MINB) softmax_warp_kernel(T* __restrict__ 
             } else {
 #pragma unroll
                 for (int e = 0; e < VE; ++e) {
-                    v[k][e] = (j0 + e < L) ? ex2_approx(fmaf(v[k][e], c, nm)) : 0.f;
+                    v[k][e] = (j0 + e < lim) ? ex2_approx(fmaf(v[k][e], c, nm)) : 0.f;
                     s[0] += v[k][e];
                 }
             }
@@ -575,7 +581,7 @@ cudaError_t launch_softmax(void* scores, const int32_t* lengths, int64_t nrows, 
 }
 
 
-template <typename T, int VB, int G, int NV, int NT, int MINB>
+template <typename T, int VB, int G, int NV, int NT, int MINB, int RPG>
 cudaError_t launch_softmax_warp(void* scores, const int32_t* lengths, int64_t nrows, int64_t rpb,
                                 int Sk, float scale, cudaStream_t st) {
     constexpr int GPB = NT / G;
@@ -585,19 +591,25 @@ cudaError_t launch_softmax_warp(void* scores, const int32_t* lengths, int64_t nr
                          ((int64_t)Sk * (int64_t)sizeof(T)) % VB == 0;
     auto kern = aligned ? softmax_warp_kernel<T, VB, G, NV, NT, MINB, true>
                         : softmax_warp_kernel<T, VB, G, NV, NT, MINB, false>;
-    static std::atomic<int> occ_cache[2] = {{0}, {0}};
-    int occ = occ_cache[aligned].load(std::memory_order_relaxed);
-    if (!occ) {
-        cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT, 0);
-        if (e != cudaSuccess) return e;
-        occ = occ > 0 ? occ : 1;
-        occ_cache[aligned].store(occ);
+    // RPG > 0: fixed rows per group; RPG = 0: one persistent wave (rows spread
+    // evenly over SMs x resident CTAs).
+    int rpg = RPG;
+    if (RPG == 0) {
+        static std::atomic<int> occ_cache[2] = {{0}, {0}};
+        int occ = occ_cache[aligned].load(std::memory_order_relaxed);
+        if (!occ) {
+            cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT, 0);
+            if (e != cudaSuccess) return e;
+            occ = occ > 0 ? occ : 1;
+            occ_cache[aligned].store(occ);
+        }
+        const int64_t slots = (int64_t)sm_count() * occ * GPB;
+        rpg = (int)((nrows + slots - 1) / slots);
     }
-    const int64_t need = (nrows + GPB - 1) / GPB;
-    const int64_t cap = (int64_t)sm_count() * occ;
-    const int64_t grid = need < cap ? need : cap;
+    const int64_t per_cta = (int64_t)GPB * rpg;
+    const int64_t grid = (nrows + per_cta - 1) / per_cta;
     kern<<<(unsigned)grid, NT, 0, st>>>(static_cast<T*>(scores), lengths, (uint32_t)nrows,
-                                       FastDivU32::make((uint32_t)rpb), Sk, scale * kLog2e);
+                                       FastDivU32::make((uint32_t)rpb), Sk, scale * kLog2e, rpg);
     return cudaGetLastError();
 }
 
@@ -618,11 +630,14 @@ struct SoftmaxTier {
             "softmax_rows<" TN ",V" #VB ",G" #G ",NV" #NV ",R" #R ",T" #NT ",M" #MINB ">" \
     }
 
-#define TT_SM_WARP(AUTO, T, TN, VB, G, NV, NT, MINB)                                      \
+#define TT_SM_WARP_R(AUTO, T, TN, VB, G, NV, NT, MINB, RPG)                               \
     SoftmaxTier {                                                                          \
-        (G) * (NV) * ((VB) / (int)sizeof(T)), AUTO, &launch_softmax_warp<T, VB, G, NV, NT, MINB>, \
-            "softmax_warp<" TN ",V" #VB ",G" #G ",NV" #NV ",T" #NT ",M" #MINB ">"         \
+        (G) * (NV) * ((VB) / (int)sizeof(T)), AUTO,                                        \
+            &launch_softmax_warp<T, VB, G, NV, NT, MINB, RPG>,                             \
+            "softmax_warp<" TN ",V" #VB ",G" #G ",NV" #NV ",T" #NT ",M" #MINB ",P" #RPG ">" \
     }
+// default: 4 rows per group per CTA
+#define TT_SM_WARP(AUTO, T, TN, VB, G, NV, NT, MINB) TT_SM_WARP_R(AUTO, T, TN, VB, G, NV, NT, MINB, 4)
 
 #define TT_SM_TMA(AUTO, T, TN, NV, NW)                                                     \
     SoftmaxTier {                                                                          \
@@ -655,7 +670,13 @@ struct SoftmaxTier {
     TT_SM_WARP(false, T, TN, 32, 32, 1, 512, 4), TT_SM_WARP(false, T, TN, 32, 32, 2, 256, 3),   \
     TT_SM_WARP(false, T, TN, 32, 32, 2, 256, 5), TT_SM_WARP(false, T, TN, 32, 32, 2, 128, 10),  \
     TT_SM_WARP(false, T, TN, 16, 32, 2, 256, 6), TT_SM_WARP(false, T, TN, 16, 32, 2, 256, 8),   \
-    TT_SM_WARP(false, T, TN, 16, 32, 1, 256, 8), TT_SM_WARP(false, T, TN, 32, 32, 3, 256, 2)
+    TT_SM_WARP(false, T, TN, 16, 32, 1, 256, 8), TT_SM_WARP(false, T, TN, 32, 32, 3, 256, 2),   \
+    TT_SM_WARP_R(false, T, TN, 32, 32, 1, 256, 5, 0), TT_SM_WARP_R(false, T, TN, 32, 32, 1, 256, 5, 1), \
+    TT_SM_WARP_R(false, T, TN, 32, 32, 1, 256, 5, 2), TT_SM_WARP_R(false, T, TN, 32, 32, 1, 256, 5, 8), \
+    TT_SM_WARP_R(false, T, TN, 32, 32, 1, 256, 5, 16), TT_SM_WARP_R(false, T, TN, 32, 32, 1, 256, 6, 0), \
+    TT_SM_WARP_R(false, T, TN, 32, 32, 1, 256, 6, 1), TT_SM_WARP_R(false, T, TN, 32, 32, 1, 256, 6, 2), \
+    TT_SM_WARP_R(false, T, TN, 32, 32, 1, 256, 6, 8), TT_SM_WARP_R(false, T, TN, 32, 32, 2, 256, 3, 0), \
+    TT_SM_WARP_R(false, T, TN, 32, 32, 2, 256, 3, 2), TT_SM_WARP_R(false, T, TN, 32, 32, 2, 256, 3, 8)
 
 // M2..M4: min CTAs/SM (register cap) of the NV = 2..4 warp tiers, chosen so
 // the row (NV * VE fp32 values per lane) fits without spilling.
