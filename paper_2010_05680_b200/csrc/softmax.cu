@@ -168,188 +168,174 @@ __global__ void __launch_bounds__(NT, MINB) softmax_rows_kernel(T* __restrict__ 
 
 // ----------------------------------------------------------------------------
 // Warp / sub-warp tier (G <= 32), the production path for rows up to
-// 32 * NV * VE keys.  CTA b owns GPB * rpg consecutive rows; per row:
+// 32 * NV * VE keys.  Persistent grid-stride loop over rows; per row:
 //   * the next row's length is fetched one iteration ahead (its latency is off
 //     the load -> compute chain),
 //   * the row index is divided by H*Sq with a multiply-high (FastDivU32),
 //   * the max is taken over the RAW values (max if scale >= 0, min otherwise),
-//     so each exponent is one FFMA + one MUFU.EX2: e = 2^(x*c - m*c),
-//   * rows with every key valid (L == Sk, the common case) take a path with no
-//     masking at all; other rows mask per vector / element,
+//     so the exponent is one FFMA: e = 2^(x*c - m*c),
+//   * full vectors (all keys valid, the common case) carry no per-element
+//     masking; only the vector that straddles L selects,
 //   * ALIGNED (row pitch and base are multiples of VB) drops the scalar head /
 //     tail code entirely.
 // ----------------------------------------------------------------------------
-template <typename T, int VB, int G, int NV, bool ALIGNED, bool FULL>
-__device__ __forceinline__ void softmax_row(T* __restrict__ p, int L, int Sk, float c, int q) {
-    constexpr int VE = VB / (int)sizeof(T);
-    constexpr int HI = ALIGNED ? 0 : (VE - 1 + G - 1) / G;
-    constexpr int HIA = HI > 0 ? HI : 1;
-    const bool up = c >= 0.f;  // max of raw x (else min)
-    const float sent = up ? -INFINITY : INFINITY;
-    int hd = 0, nv = Sk / VE;
-    if constexpr (!ALIGNED) {
-        const int mis = (int)((reinterpret_cast<uintptr_t>(p) & (VB - 1)) / sizeof(T));
-        hd = mis ? min(VE - mis, Sk) : 0;
-        nv = (Sk - hd) / VE;
-    }
-    const int tl0 = hd + nv * VE;
-
-    // kact[k]: some lane's vector k holds a valid key.  Uniform across the
-    // group (lane 0's vector k starts first), so padding-only vectors skip
-    // the load / max / exp work entirely and only store zeros.
-    bool kact[NV];
-#pragma unroll
-    for (int k = 0; k < NV; ++k) kact[k] = FULL || (hd + k * G * VE < L);
-
-    // ---- SM-2: load the valid prefix (raw values)
-    float v[NV][VE];
-#pragma unroll
-    for (int k = 0; k < NV; ++k) {
-        const int vi = q + k * G;
-        const int j0 = hd + vi * VE;
-        if (!kact[k]) continue;
-        if (vi < nv && (FULL || j0 < L)) {
-            Raw<VB> w;
-            ld_stream<VB>(p + j0, w);
-            Elem<T>::template unpack<VB>(w, v[k]);
-            if (!FULL && j0 + VE > L) {
-#pragma unroll
-                for (int e = 0; e < VE; ++e)
-                    if (j0 + e >= L) v[k][e] = sent;
-            }
-        } else {
-#pragma unroll
-            for (int e = 0; e < VE; ++e) v[k][e] = sent;
-        }
-    }
-    float hv[HIA], tv[HIA];
-    if constexpr (!ALIGNED) {
-#pragma unroll
-        for (int i = 0; i < HI; ++i) {
-            const int jh = q + i * G, jt = tl0 + q + i * G;
-            hv[i] = (jh < hd && (FULL || jh < L)) ? Elem<T>::to_f(p[jh]) : sent;
-            tv[i] = (jt < Sk && (FULL || jt < L)) ? Elem<T>::to_f(p[jt]) : sent;
-        }
-    }
-
-    // ---- SM-3: row max of the scaled logits, c * (max or min of raw x)
-    float m[1];
-    {
-        float a = sent;
-        if (up) {
-#pragma unroll
-            for (int k = 0; k < NV; ++k)
-                if (kact[k]) {
-#pragma unroll
-                    for (int e = 0; e < VE; ++e) a = fmaxf(a, v[k][e]);
-                }
-            if constexpr (!ALIGNED) {
-#pragma unroll
-                for (int i = 0; i < HI; ++i) a = fmaxf(a, fmaxf(hv[i], tv[i]));
-            }
-        } else {
-#pragma unroll
-            for (int k = 0; k < NV; ++k)
-                if (kact[k]) {
-#pragma unroll
-                    for (int e = 0; e < VE; ++e) a = fminf(a, v[k][e]);
-                }
-            if constexpr (!ALIGNED) {
-#pragma unroll
-                for (int i = 0; i < HI; ++i) a = fminf(a, fminf(hv[i], tv[i]));
-            }
-        }
-        m[0] = up ? a : -a;
-    }
-    group_max<G, 1>(m, nullptr);
-    float nm = -((up ? m[0] : -m[0]) * c);  // -max_j (c * x_j)
-    if (!FULL && !(fabsf(nm) <= 3.0e38f)) nm = 0.f;  // empty row (L = 0)
-
-    // ---- SM-4: e_j = 2^(c x_j - m), once; s = sum e_j.  Masked keys get
-    // e = +0.0 (the select also covers c = 0, where the sentinel gives NaN).
-    float s[1] = {0.f};
-#pragma unroll
-    for (int k = 0; k < NV; ++k) {
-        const int vi = q + k * G;
-        const int j0 = hd + vi * VE;
-        const int lim = (vi < nv) ? (FULL ? Sk : L) : 0;
-        if (!kact[k]) {
-#pragma unroll
-            for (int e = 0; e < VE; ++e) v[k][e] = 0.f;
-            continue;
-        }
-#pragma unroll
-        for (int e = 0; e < VE; ++e) v[k][e] = ex2_approx(fmaf(v[k][e], c, nm));
-        if (!FULL || NV * G * VE > Sk) {
-            if (j0 + VE > lim) {
-#pragma unroll
-                for (int e = 0; e < VE; ++e) v[k][e] = (j0 + e < lim) ? v[k][e] : 0.f;
-            }
-        }
-#pragma unroll
-        for (int e = 0; e < VE; ++e) s[0] += v[k][e];
-    }
-    if constexpr (!ALIGNED) {
-#pragma unroll
-        for (int i = 0; i < HI; ++i) {
-            const int jh = q + i * G, jt = tl0 + q + i * G;
-            hv[i] = (jh < hd && (FULL || jh < L)) ? ex2_approx(fmaf(hv[i], c, nm)) : 0.f;
-            tv[i] = (jt < Sk && (FULL || jt < L)) ? ex2_approx(fmaf(tv[i], c, nm)) : 0.f;
-            s[0] += hv[i] + tv[i];
-        }
-    }
-    group_sum<G, 1>(s, nullptr);
-    // masked keys hold e = +0.0, so y = e * inv is +0.0 there; L = 0 -> inv = 0
-    const float inv = (FULL || s[0] > 0.f) ? __fdividef(1.0f, s[0]) : 0.f;
-
-    // ---- SM-5: normalise and store every column
-#pragma unroll
-    for (int k = 0; k < NV; ++k) {
-        const int vi = q + k * G;
-        if (vi < nv) {
-            float y[VE];
-#pragma unroll
-            for (int e = 0; e < VE; ++e) y[e] = v[k][e] * inv;
-            Raw<VB> w;
-            Elem<T>::template pack<VB>(y, w);
-            st_stream<VB>(p + hd + vi * VE, w);
-        }
-    }
-    if constexpr (!ALIGNED) {
-#pragma unroll
-        for (int i = 0; i < HI; ++i) {
-            const int jh = q + i * G, jt = tl0 + q + i * G;
-            if (jh < hd) p[jh] = Elem<T>::from_f(hv[i] * inv);
-            if (jt < Sk) p[jt] = Elem<T>::from_f(tv[i] * inv);
-        }
-    }
-}
-
 template <typename T, int VB, int G, int NV, int NT, int MINB, bool ALIGNED>
 __global__ void __launch_bounds__(NT, MINB) softmax_warp_kernel(T* __restrict__ scores,
                                                                 const int32_t* __restrict__ lengths,
                                                                 uint32_t nrows, FastDivU32 rpb,
                                                                 int Sk, float c, int rpg) {
+    constexpr int VE = VB / (int)sizeof(T);
+    constexpr int HI = ALIGNED ? 0 : (VE - 1 + G - 1) / G;
+    constexpr int HIA = HI > 0 ? HI : 1;
     constexpr int GPB = NT / G;
     static_assert(G <= 32, "warp tier");
+
     // CTA b owns rows [b * GPB * rpg, (b + 1) * GPB * rpg); its groups walk them
     // GPB rows at a time (adjacent groups on adjacent rows).  rpg trades the
     // per-CTA setup and the length prefetch against load balance across CTAs
     // when row costs vary (ragged lengths).
     const int q = threadIdx.x % G;
+    const uint32_t stride = GPB;
     uint32_t row = blockIdx.x * (uint32_t)(GPB * rpg) + threadIdx.x / G;
     const uint32_t row_end = min(nrows, (blockIdx.x + 1) * (uint32_t)(GPB * rpg));
-    auto len_of = [&](uint32_t r) { return min(max(__ldg(lengths + rpb.div(r)), 0), Sk); };
+    const bool up = c >= 0.f;                 // max of raw x (else min)
+    const float sent = up ? -INFINITY : INFINITY;
+
+    auto len_of = [&](uint32_t r) {
+        return min(max(__ldg(lengths + rpb.div(r)), 0), Sk);
+    };
     int Lnext = row < row_end ? len_of(row) : 0;
-    for (; row < row_end; row += GPB) {
+
+    for (; row < row_end; row += stride) {
         const int L = Lnext;
-        if (row + GPB < row_end) Lnext = len_of(row + GPB);
+        if (row + stride < row_end) Lnext = len_of(row + stride);
         T* p = scores + (size_t)row * (size_t)Sk;
-        // the group shares one row, so this branch is uniform within a group
-        if (L == Sk)
-            softmax_row<T, VB, G, NV, ALIGNED, true>(p, L, Sk, c, q);
-        else
-            softmax_row<T, VB, G, NV, ALIGNED, false>(p, L, Sk, c, q);
+        int hd = 0, nv = Sk / VE;
+        if constexpr (!ALIGNED) {
+            const int mis = (int)((reinterpret_cast<uintptr_t>(p) & (VB - 1)) / sizeof(T));
+            hd = mis ? min(VE - mis, Sk) : 0;
+            nv = (Sk - hd) / VE;
+        }
+
+        // ---- SM-2: load the valid prefix (raw values)
+        float v[NV][VE];
+        bool full[NV];
+#pragma unroll
+        for (int k = 0; k < NV; ++k) {
+            const int vi = q + k * G;
+            const int j0 = hd + vi * VE;
+            full[k] = (vi < nv) && (j0 + VE <= L);
+            if (vi < nv && j0 < L) {
+                Raw<VB> w;
+                ld_stream<VB>(p + j0, w);
+                Elem<T>::template unpack<VB>(w, v[k]);
+                if (!full[k]) {
+#pragma unroll
+                    for (int e = 0; e < VE; ++e)
+                        if (j0 + e >= L) v[k][e] = sent;
+                }
+            } else {
+#pragma unroll
+                for (int e = 0; e < VE; ++e) v[k][e] = sent;
+            }
+        }
+        float hv[HIA], tv[HIA];
+        const int tl0 = hd + nv * VE;
+        if constexpr (!ALIGNED) {
+#pragma unroll
+            for (int i = 0; i < HI; ++i) {
+                const int jh = q + i * G;
+                hv[i] = (jh < hd && jh < L) ? Elem<T>::to_f(p[jh]) : sent;
+                const int jt = tl0 + q + i * G;
+                tv[i] = (jt < Sk && jt < L) ? Elem<T>::to_f(p[jt]) : sent;
+            }
+        }
+
+        // ---- SM-3: row max of the scaled logits, c * (max or min of raw x)
+        float m[1];
+        {
+            float a = sent;
+            if (up) {
+#pragma unroll
+                for (int k = 0; k < NV; ++k)
+#pragma unroll
+                    for (int e = 0; e < VE; ++e) a = fmaxf(a, v[k][e]);
+                if constexpr (!ALIGNED) {
+#pragma unroll
+                    for (int i = 0; i < HI; ++i) a = fmaxf(a, fmaxf(hv[i], tv[i]));
+                }
+            } else {
+#pragma unroll
+                for (int k = 0; k < NV; ++k)
+#pragma unroll
+                    for (int e = 0; e < VE; ++e) a = fminf(a, v[k][e]);
+                if constexpr (!ALIGNED) {
+#pragma unroll
+                    for (int i = 0; i < HI; ++i) a = fminf(a, fminf(hv[i], tv[i]));
+                }
+            }
+            m[0] = up ? a : -a;
+        }
+        group_max<G, 1>(m, nullptr);
+        const float mr = up ? m[0] : -m[0];
+        float nm = -(mr * c);                       // -max_j (c * x_j)
+        if (!(fabsf(nm) <= 3.0e38f)) nm = 0.f;      // empty row (L = 0): no valid key
+
+        // ---- SM-4: e_j = 2^(c x_j - m), once; s = sum e_j
+        float s[1] = {0.f};
+#pragma unroll
+        for (int k = 0; k < NV; ++k) {
+            const int j0 = hd + (q + k * G) * VE;
+            const int lim = (q + k * G < nv) ? L : 0;  // keys of this vector that are valid
+            if (full[k]) {
+#pragma unroll
+                for (int e = 0; e < VE; ++e) {
+                    v[k][e] = ex2_approx(fmaf(v[k][e], c, nm));
+                    s[0] += v[k][e];
+                }
+            } else {
+#pragma unroll
+                for (int e = 0; e < VE; ++e) {
+                    v[k][e] = (j0 + e < lim) ? ex2_approx(fmaf(v[k][e], c, nm)) : 0.f;
+                    s[0] += v[k][e];
+                }
+            }
+        }
+        if constexpr (!ALIGNED) {
+#pragma unroll
+            for (int i = 0; i < HI; ++i) {
+                const int jh = q + i * G, jt = tl0 + q + i * G;
+                hv[i] = (jh < hd && jh < L) ? ex2_approx(fmaf(hv[i], c, nm)) : 0.f;
+                tv[i] = (jt < Sk && jt < L) ? ex2_approx(fmaf(tv[i], c, nm)) : 0.f;
+                s[0] += hv[i] + tv[i];
+            }
+        }
+        group_sum<G, 1>(s, nullptr);
+        // masked keys hold e = +0.0, so y = e * inv is +0.0 there; L = 0 -> inv = 0
+        const float inv = s[0] > 0.f ? __fdividef(1.0f, s[0]) : 0.f;
+
+        // ---- SM-5: normalise and store every column
+#pragma unroll
+        for (int k = 0; k < NV; ++k) {
+            const int vi = q + k * G;
+            if (vi < nv) {
+                float y[VE];
+#pragma unroll
+                for (int e = 0; e < VE; ++e) y[e] = v[k][e] * inv;
+                Raw<VB> w;
+                Elem<T>::template pack<VB>(y, w);
+                st_stream<VB>(p + hd + vi * VE, w);
+            }
+        }
+        if constexpr (!ALIGNED) {
+#pragma unroll
+            for (int i = 0; i < HI; ++i) {
+                const int jh = q + i * G;
+                if (jh < hd) p[jh] = Elem<T>::from_f(hv[i] * inv);
+                const int jt = tl0 + q + i * G;
+                if (jt < Sk) p[jt] = Elem<T>::from_f(tv[i] * inv);
+            }
+        }
     }
 }
 
@@ -666,12 +652,11 @@ struct SoftmaxTier {
 // parallelism.  CTA tiers keep NV * VE = 32 fp32 registers of row data per
 // thread so that a 1024-thread CTA fits the 64-register limit: NVC = 4 (fp32)
 // or 2 (16-bit).  Non-automatic entries are tuning candidates (tt_tune.h).
-#define TT_SM_LIST(T, TN, NVC, M2, M3, M4, VW)                                               \
+#define TT_SM_LIST(T, TN, NVC, M2, M3, M4)                                                   \
     TT_SM_WARP(true, T, TN, 16, 4, 1, 256, 6), TT_SM_WARP(true, T, TN, 16, 8, 1, 256, 6),       \
-    TT_SM_WARP(true, T, TN, 16, 16, 1, 256, 6), TT_SM_WARP(true, T, TN, VW, 32, 1, 256, 6),     \
-    TT_SM_WARP(true, T, TN, VW, 32, 2, 256, M2), TT_SM_WARP(true, T, TN, VW, 32, 3, 256, M3),   \
-    TT_SM_WARP(true, T, TN, VW, 32, 4, 256, M4), TT_SM_WARP(true, T, TN, 32, 32, 3, 256, M3),   \
-    TT_SM_WARP(true, T, TN, 32, 32, 4, 256, M4),                                               \
+    TT_SM_WARP(true, T, TN, 16, 16, 1, 256, 6), TT_SM_WARP(true, T, TN, 32, 16, 1, 256, 6),     \
+    TT_SM_WARP(true, T, TN, 32, 32, 1, 256, 6), TT_SM_WARP(true, T, TN, 32, 32, 2, 256, M2),    \
+    TT_SM_WARP(true, T, TN, 32, 32, 3, 256, M3), TT_SM_WARP(true, T, TN, 32, 32, 4, 256, M4),   \
     TT_SM_TIER(true, T, TN, 32, 64, NVC, 1, 64, 1), TT_SM_TIER(true, T, TN, 32, 128, NVC, 1, 128, 1), \
     TT_SM_TIER(true, T, TN, 32, 256, NVC, 1, 256, 1), TT_SM_TIER(true, T, TN, 32, 512, NVC, 1, 512, 1), \
     TT_SM_TIER(true, T, TN, 32, 1024, NVC, 1, 1024, 1),                                     \
@@ -695,12 +680,9 @@ struct SoftmaxTier {
 
 // M2..M4: min CTAs/SM (register cap) of the NV = 2..4 warp tiers, chosen so
 // the row (NV * VE fp32 values per lane) fits without spilling.
-// VW: vector bytes of the warp tiers, chosen so every dtype has 8 keys per
-// vector (fp32 32 B, 16-bit 16 B): vector k of the warp then spans 256 keys,
-// the granularity at which padding-only vectors are skipped.
-const SoftmaxTier kSm_f32[] = {TT_SM_LIST(float, "f32", 4, 3, 5, 4, 32)};
-const SoftmaxTier kSm_f16[] = {TT_SM_LIST(__half, "f16", 2, 6, 4, 3, 16)};
-const SoftmaxTier kSm_bf16[] = {TT_SM_LIST(__nv_bfloat16, "bf16", 2, 6, 4, 3, 16)};
+const SoftmaxTier kSm_f32[] = {TT_SM_LIST(float, "f32", 4, 6, 5, 4)};
+const SoftmaxTier kSm_f16[] = {TT_SM_LIST(__half, "f16", 2, 4, 3, 2)};
+const SoftmaxTier kSm_bf16[] = {TT_SM_LIST(__nv_bfloat16, "bf16", 2, 4, 3, 2)};
 constexpr int kSmN = (int)(sizeof(kSm_f32) / sizeof(kSm_f32[0]));
 
 std::atomic<int> g_force[3] = {{-1}, {-1}, {-1}};
