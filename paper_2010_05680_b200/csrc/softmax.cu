@@ -168,17 +168,31 @@ __global__ void __launch_bounds__(NT, MINB) softmax_rows_kernel(T* __restrict__ 
 
 // ----------------------------------------------------------------------------
 // Warp / sub-warp tier (G <= 32), the production path for rows up to
-// 32 * NV * VE keys.  Persistent grid-stride loop over rows; per row:
-//   * the next row's length is fetched one iteration ahead (its latency is off
-//     the load -> compute chain),
-//   * the row index is divided by H*Sq with a multiply-high (FastDivU32),
-//   * the max is taken over the RAW values (max if scale >= 0, min otherwise),
-//     so the exponent is one FFMA: e = 2^(x*c - m*c),
-//   * full vectors (all keys valid, the common case) carry no per-element
-//     masking; only the vector that straddles L selects,
+// 32 * NV * VE keys.  CTA b owns GPB * rpg consecutive rows (rpg = rows per
+// group); its groups walk them GPB rows at a time.  Instruction budget per
+// row is what limits this kernel on B200 once the loads are deep enough, so:
+//   * the request length is looked up once per CTA when the CTA's rows all
+//     belong to one request (the common case), else per row, with the next
+//     row's length prefetched and the row -> request division done by a
+//     multiply-high (FastDivU32);
+//   * loads are never predicated off: a lane whose vector lies past the valid
+//     prefix re-reads the row's first vector (a valid, cached address), so
+//     no sentinel initialisation is needed, and those duplicates of valid
+//     keys cannot raise the max;
+//   * the max is taken over RAW values (max if scale > 0, min if < 0), so
+//     each exponent is one FFMA + one MUFU.EX2: e = 2^(x*c - c*m);
+//   * a row with every key valid (L == Sk) skips all masking; otherwise each
+//     element is masked once, to the +-inf sentinel, which the FFMA/EX2 turns
+//     into e = +0.0 (scale == 0 is mapped to a tiny positive c on the host);
 //   * ALIGNED (row pitch and base are multiples of VB) drops the scalar head /
 //     tail code entirely.
 // ----------------------------------------------------------------------------
+__device__ __forceinline__ float rcp_approx(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
 template <typename T, int VB, int G, int NV, int NT, int MINB, bool ALIGNED>
 __global__ void __launch_bounds__(NT, MINB) softmax_warp_kernel(T* __restrict__ scores,
                                                                 const int32_t* __restrict__ lengths,
@@ -190,25 +204,21 @@ __global__ void __launch_bounds__(NT, MINB) softmax_warp_kernel(T* __restrict__ 
     constexpr int GPB = NT / G;
     static_assert(G <= 32, "warp tier");
 
-    // CTA b owns rows [b * GPB * rpg, (b + 1) * GPB * rpg); its groups walk them
-    // GPB rows at a time (adjacent groups on adjacent rows).  rpg trades the
-    // per-CTA setup and the length prefetch against load balance across CTAs
-    // when row costs vary (ragged lengths).
     const int q = threadIdx.x % G;
-    const uint32_t stride = GPB;
-    uint32_t row = blockIdx.x * (uint32_t)(GPB * rpg) + threadIdx.x / G;
-    const uint32_t row_end = min(nrows, (blockIdx.x + 1) * (uint32_t)(GPB * rpg));
-    const bool up = c >= 0.f;                 // max of raw x (else min)
+    const uint32_t first = blockIdx.x * (uint32_t)(GPB * rpg);
+    const uint32_t row_end = min(nrows, first + (uint32_t)(GPB * rpg));
+    uint32_t row = first + threadIdx.x / G;
+    const bool up = c > 0.f;  // max of raw x (else min); c != 0 (host)
     const float sent = up ? -INFINITY : INFINITY;
 
-    auto len_of = [&](uint32_t r) {
-        return min(max(__ldg(lengths + rpb.div(r)), 0), Sk);
-    };
-    int Lnext = row < row_end ? len_of(row) : 0;
+    auto len_of = [&](uint32_t r) { return min(max(__ldg(lengths + rpb.div(r)), 0), Sk); };
+    // one request for the whole CTA?  (uniform; rpb = H * Sq rows per request)
+    const bool one_req = rpb.div(first) == rpb.div(row_end - 1);
+    int Lnext = one_req ? len_of(first) : (row < row_end ? len_of(row) : 0);
 
-    for (; row < row_end; row += stride) {
+    for (; row < row_end; row += GPB) {
         const int L = Lnext;
-        if (row + stride < row_end) Lnext = len_of(row + stride);
+        if (!one_req && row + GPB < row_end) Lnext = len_of(row + GPB);
         T* p = scores + (size_t)row * (size_t)Sk;
         int hd = 0, nv = Sk / VE;
         if constexpr (!ALIGNED) {
@@ -216,38 +226,48 @@ __global__ void __launch_bounds__(NT, MINB) softmax_warp_kernel(T* __restrict__ 
             hd = mis ? min(VE - mis, Sk) : 0;
             nv = (Sk - hd) / VE;
         }
+        const int tl0 = hd + nv * VE;
+        // masking is needed unless every key is valid and every vector slot of
+        // the group maps onto the row (uniform within the group)
+        const bool masked = (L < Sk) || (nv < G * NV);
 
-        // ---- SM-2: load the valid prefix (raw values)
+        // ---- SM-2: load (never predicated off; see above)
         float v[NV][VE];
-        bool full[NV];
+        if (L > 0) {
 #pragma unroll
-        for (int k = 0; k < NV; ++k) {
-            const int vi = q + k * G;
-            const int j0 = hd + vi * VE;
-            full[k] = (vi < nv) && (j0 + VE <= L);
-            if (vi < nv && j0 < L) {
+            for (int k = 0; k < NV; ++k) {
+                const int vi = q + k * G;
+                const int j0 = hd + vi * VE;
+                const bool in = vi < nv && j0 < L;
                 Raw<VB> w;
-                ld_stream<VB>(p + j0, w);
+                ld_stream<VB>(p + (in ? j0 : hd), w);
                 Elem<T>::template unpack<VB>(w, v[k]);
-                if (!full[k]) {
+            }
+        } else {
 #pragma unroll
-                    for (int e = 0; e < VE; ++e)
-                        if (j0 + e >= L) v[k][e] = sent;
-                }
-            } else {
+            for (int k = 0; k < NV; ++k)
 #pragma unroll
                 for (int e = 0; e < VE; ++e) v[k][e] = sent;
+        }
+        if (masked) {
+#pragma unroll
+            for (int k = 0; k < NV; ++k) {
+                const int vi = q + k * G;
+                const int nvalid = vi < nv ? min(max(L - (hd + vi * VE), 0), VE) : 0;
+#pragma unroll
+                for (int e = 0; e < VE; ++e) v[k][e] = e < nvalid ? v[k][e] : sent;
             }
         }
         float hv[HIA], tv[HIA];
-        const int tl0 = hd + nv * VE;
         if constexpr (!ALIGNED) {
 #pragma unroll
             for (int i = 0; i < HI; ++i) {
-                const int jh = q + i * G;
-                hv[i] = (jh < hd && jh < L) ? Elem<T>::to_f(p[jh]) : sent;
-                const int jt = tl0 + q + i * G;
-                tv[i] = (jt < Sk && jt < L) ? Elem<T>::to_f(p[jt]) : sent;
+                const int jh = q + i * G, jt = tl0 + q + i * G;
+                const bool ih = jh < hd && jh < L, it = jt < Sk && jt < L;
+                const float a = Elem<T>::to_f(p[ih ? jh : 0]);
+                const float b = Elem<T>::to_f(p[it ? jt : 0]);
+                hv[i] = ih ? a : sent;
+                tv[i] = it ? b : sent;
             }
         }
 
@@ -277,42 +297,30 @@ __global__ void __launch_bounds__(NT, MINB) softmax_warp_kernel(T* __restrict__ 
             m[0] = up ? a : -a;
         }
         group_max<G, 1>(m, nullptr);
-        const float mr = up ? m[0] : -m[0];
-        float nm = -(mr * c);                       // -max_j (c * x_j)
-        if (!(fabsf(nm) <= 3.0e38f)) nm = 0.f;      // empty row (L = 0): no valid key
+        float nm = -((up ? m[0] : -m[0]) * c);   // -max_j (c * x_j)
+        if (!(fabsf(nm) <= 3.0e38f)) nm = 0.f;   // empty row (L = 0)
 
-        // ---- SM-4: e_j = 2^(c x_j - m), once; s = sum e_j
+        // ---- SM-4: e_j = 2^(c x_j - m), once (sentinel -> +0.0); s = sum e_j
         float s[1] = {0.f};
 #pragma unroll
-        for (int k = 0; k < NV; ++k) {
-            const int j0 = hd + (q + k * G) * VE;
-            const int lim = (q + k * G < nv) ? L : 0;  // keys of this vector that are valid
-            if (full[k]) {
+        for (int k = 0; k < NV; ++k)
 #pragma unroll
-                for (int e = 0; e < VE; ++e) {
-                    v[k][e] = ex2_approx(fmaf(v[k][e], c, nm));
-                    s[0] += v[k][e];
-                }
-            } else {
-#pragma unroll
-                for (int e = 0; e < VE; ++e) {
-                    v[k][e] = (j0 + e < lim) ? ex2_approx(fmaf(v[k][e], c, nm)) : 0.f;
-                    s[0] += v[k][e];
-                }
+            for (int e = 0; e < VE; ++e) {
+                v[k][e] = ex2_approx(fmaf(v[k][e], c, nm));
+                s[0] += v[k][e];
             }
-        }
         if constexpr (!ALIGNED) {
 #pragma unroll
             for (int i = 0; i < HI; ++i) {
-                const int jh = q + i * G, jt = tl0 + q + i * G;
-                hv[i] = (jh < hd && jh < L) ? ex2_approx(fmaf(hv[i], c, nm)) : 0.f;
-                tv[i] = (jt < Sk && jt < L) ? ex2_approx(fmaf(tv[i], c, nm)) : 0.f;
+                hv[i] = ex2_approx(fmaf(hv[i], c, nm));
+                tv[i] = ex2_approx(fmaf(tv[i], c, nm));
                 s[0] += hv[i] + tv[i];
             }
         }
         group_sum<G, 1>(s, nullptr);
-        // masked keys hold e = +0.0, so y = e * inv is +0.0 there; L = 0 -> inv = 0
-        const float inv = s[0] > 0.f ? __fdividef(1.0f, s[0]) : 0.f;
+        // masked keys hold e = +0.0, so y = e * inv is +0.0 there; L = 0 -> inv = 0.
+        // For L > 0, s >= 1 (the max key contributes 1) or NaN (NaN keys propagate).
+        const float inv = L > 0 ? rcp_approx(s[0]) : 0.f;
 
         // ---- SM-5: normalise and store every column
 #pragma unroll
@@ -330,9 +338,8 @@ __global__ void __launch_bounds__(NT, MINB) softmax_warp_kernel(T* __restrict__ 
         if constexpr (!ALIGNED) {
 #pragma unroll
             for (int i = 0; i < HI; ++i) {
-                const int jh = q + i * G;
+                const int jh = q + i * G, jt = tl0 + q + i * G;
                 if (jh < hd) p[jh] = Elem<T>::from_f(hv[i] * inv);
-                const int jt = tl0 + q + i * G;
                 if (jt < Sk) p[jt] = Elem<T>::from_f(tv[i] * inv);
             }
         }
@@ -608,8 +615,13 @@ cudaError_t launch_softmax_warp(void* scores, const int32_t* lengths, int64_t nr
     }
     const int64_t per_cta = (int64_t)GPB * rpg;
     const int64_t grid = (nrows + per_cta - 1) / per_cta;
+    // c = 0 (scale 0: uniform softmax) is mapped to a tiny positive c so the
+    // masked-key sentinel still exponentiates to exactly +0.0; for finite x,
+    // 2^(x * 1e-30 - m * 1e-30) rounds to exactly 1.0f.
+    float c = scale * kLog2e;
+    if (c == 0.f) c = 1e-30f;
     kern<<<(unsigned)grid, NT, 0, st>>>(static_cast<T*>(scores), lengths, (uint32_t)nrows,
-                                       FastDivU32::make((uint32_t)rpb), Sk, scale * kLog2e, rpg);
+                                       FastDivU32::make((uint32_t)rpb), Sk, c, rpg);
     return cudaGetLastError();
 }
 

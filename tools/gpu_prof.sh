@@ -3,9 +3,9 @@ set -x
 P="ncu --set full --import-source on --clock-control none -k regex:softmax_|ln_ -s 2 -c 1"
 IFS=';' read -ra JOBS <<< "$PROF"
 for j in "${JOBS[@]}"; do
-  IFS='|' read -r name spec tier <<< "$j"
+  IFS='|' read -r name spec tier extra <<< "$j"
   if [ -n "$tier" ]; then
-    $P -o gpurun_out/prof_$name python tools/prof_one.py $spec --tier "$tier" > gpurun_out/prof_$name.log 2>&1
+    $P -o gpurun_out/prof_$name python tools/prof_one.py $spec --tier "$tier" $extra > gpurun_out/prof_$name.log 2>&1
   else
     $P -o gpurun_out/prof_$name python tools/prof_one.py $spec > gpurun_out/prof_$name.log 2>&1
   fi
