@@ -234,13 +234,18 @@ __global__ void __launch_bounds__(NT, MINB) softmax_warp_kernel(T* __restrict__ 
         // ---- SM-2: load (never predicated off; see above)
         float v[NV][VE];
         if (L > 0) {
+            // fallback address for lanes past the prefix: the first body vector,
+            // or (row shorter than its head) the VB-aligned vector containing p
+            const T* fb = nv > 0 ? p + hd
+                                 : reinterpret_cast<const T*>(reinterpret_cast<uintptr_t>(p) &
+                                                              ~(uintptr_t)(VB - 1));
 #pragma unroll
             for (int k = 0; k < NV; ++k) {
                 const int vi = q + k * G;
                 const int j0 = hd + vi * VE;
                 const bool in = vi < nv && j0 < L;
                 Raw<VB> w;
-                ld_stream<VB>(p + (in ? j0 : hd), w);
+                ld_stream<VB>(in ? p + j0 : fb, w);
                 Elem<T>::template unpack<VB>(w, v[k]);
             }
         } else {
