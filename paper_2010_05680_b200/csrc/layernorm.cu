@@ -151,52 +151,41 @@ __global__ void __launch_bounds__(NT, MINB)
 // to fp32 ONCE into shared memory in a lane-interleaved layout (quad j of
 // chunk c at float4 index (p * VE/4 + j) * nvec + c, so a warp's LDS.128 are
 // conflict-free), which removes their per-row global loads and conversions.
-// Per row: x and residual vector loads, v = (x + bias) + residual, shifted
-// mean, centred variance (d = v - mean kept in the same registers), then
-// y = d * rstd * gamma + beta.
+// The first row's x / residual loads are issued before that staging so the
+// staging hides under their latency; with PF = true every row's loads are
+// issued one row ahead (raw registers, loop unrolled by two).  Per row:
+// v = (x + bias) + residual, shifted mean, centred variance (d = v - mean kept
+// in the same registers), y = d * rstd * gamma + beta.
 // ----------------------------------------------------------------------------
-template <typename T, int VB, int G, int NV, int NT, int MINB>
-__global__ void __launch_bounds__(NT, MINB)
-    ln_warp_kernel(T* out, const T* x, const T* residual, const T* __restrict__ bias,
-                   const T* __restrict__ gamma, const T* __restrict__ beta, uint32_t rows,
-                   int hidden, float eps) {
-    constexpr int VE = VB / (int)sizeof(T);
-    constexpr int QV = VE / 4;  // float4 quads per vector
-    constexpr int GPB = NT / G;
-    static_assert(G <= 32 && VE % 4 == 0, "warp tier with >= 4-element vectors");
-    extern __shared__ __align__(16) float4 prm[];  // [3][QV][nvec] float4
-    const int nvec = hidden / VE;
-    const float invN = 1.0f / (float)hidden;
+template <typename T, int VB, int G, int NV>
+struct LnRow {
+    static constexpr int VE = VB / (int)sizeof(T);
+    static constexpr int QV = VE / 4;
+    Raw<VB> x[NV], r[NV];
 
-    // stage the three parameter vectors as fp32 (once per persistent CTA)
-    for (int i = threadIdx.x; i < 3 * hidden; i += NT) {
-        const int pi = i / hidden, col = i - pi * hidden;
-        const T* src = pi == 0 ? bias : pi == 1 ? gamma : beta;
-        const int c = col / VE, e = col - c * VE;
-        reinterpret_cast<float*>(prm)[(((pi * QV + (e >> 2)) * nvec + c) << 2) + (e & 3)] =
-            Elem<T>::to_f(src[col]);
+    __device__ __forceinline__ void load(const T* xp, const T* rp, size_t off, int q, int nvec) {
+#pragma unroll
+        for (int k = 0; k < NV; ++k) {
+            const int vi = q + k * G;
+            if (vi < nvec) {
+                ld_stream<VB>(xp + off + vi * VE, x[k]);
+                ld_stream<VB>(rp + off + vi * VE, r[k]);
+            }
+        }
     }
-    __syncthreads();
-    const float4* pb = prm;
-    const float4* pg = prm + QV * nvec;
-    const float4* pe = prm + 2 * QV * nvec;
 
-    const int q = threadIdx.x % G;
-    const uint32_t stride = gridDim.x * GPB;
-    for (uint32_t row = blockIdx.x * GPB + threadIdx.x / G; row < rows; row += stride) {
-        const size_t off = (size_t)row * (size_t)hidden;
+    __device__ __forceinline__ void finish(T* out, size_t off, int q, int nvec, float invN,
+                                           float eps, const float4* pb, const float4* pg,
+                                           const float4* pe) const {
         // ---- LN-1
         float v[NV][VE];
 #pragma unroll
         for (int k = 0; k < NV; ++k) {
             const int vi = q + k * G;
             if (vi < nvec) {
-                Raw<VB> wx, wr;
-                ld_stream<VB>(x + off + vi * VE, wx);
-                ld_stream<VB>(residual + off + vi * VE, wr);
                 float fr[VE];
-                Elem<T>::template unpack<VB>(wx, v[k]);
-                Elem<T>::template unpack<VB>(wr, fr);
+                Elem<T>::template unpack<VB>(x[k], v[k]);
+                Elem<T>::template unpack<VB>(r[k], fr);
 #pragma unroll
                 for (int j = 0; j < QV; ++j) {
                     const float4 b = pb[j * nvec + vi];
@@ -251,6 +240,58 @@ __global__ void __launch_bounds__(NT, MINB)
                 Elem<T>::template pack<VB>(y, wy);
                 st_stream<VB>(out + off + vi * VE, wy);
             }
+        }
+    }
+};
+
+template <typename T, int VB, int G, int NV, int NT, int MINB, bool PF>
+__global__ void __launch_bounds__(NT, MINB)
+    ln_warp_kernel(T* out, const T* x, const T* residual, const T* __restrict__ bias,
+                   const T* __restrict__ gamma, const T* __restrict__ beta, uint32_t rows,
+                   int hidden, float eps) {
+    using Row = LnRow<T, VB, G, NV>;
+    constexpr int VE = Row::VE;
+    constexpr int QV = Row::QV;
+    constexpr int GPB = NT / G;
+    static_assert(G <= 32 && VE % 4 == 0, "warp tier with >= 4-element vectors");
+    extern __shared__ __align__(16) float4 prm[];  // [3][QV][nvec] float4
+    const int nvec = hidden / VE;
+    const float invN = 1.0f / (float)hidden;
+    const int q = threadIdx.x % G;
+    const uint32_t stride = gridDim.x * GPB;
+    uint32_t row = blockIdx.x * GPB + threadIdx.x / G;
+
+    Row a, b;
+    if (row < rows) a.load(x, residual, (size_t)row * hidden, q, nvec);  // in flight during staging
+
+    // stage the three parameter vectors as fp32 (once per persistent CTA)
+    for (int i = threadIdx.x; i < 3 * hidden; i += NT) {
+        const int pi = i / hidden, col = i - pi * hidden;
+        const T* src = pi == 0 ? bias : pi == 1 ? gamma : beta;
+        const int c = col / VE, e = col - c * VE;
+        reinterpret_cast<float*>(prm)[(((pi * QV + (e >> 2)) * nvec + c) << 2) + (e & 3)] =
+            Elem<T>::to_f(src[col]);
+    }
+    __syncthreads();
+    const float4* pb = prm;
+    const float4* pg = prm + QV * nvec;
+    const float4* pe = prm + 2 * QV * nvec;
+
+    if constexpr (PF) {
+        while (row < rows) {
+            const uint32_t r1 = row + stride;
+            if (r1 < rows) b.load(x, residual, (size_t)r1 * hidden, q, nvec);
+            a.finish(out, (size_t)row * hidden, q, nvec, invN, eps, pb, pg, pe);
+            if (r1 >= rows) break;
+            const uint32_t r2 = r1 + stride;
+            if (r2 < rows) a.load(x, residual, (size_t)r2 * hidden, q, nvec);
+            b.finish(out, (size_t)r1 * hidden, q, nvec, invN, eps, pb, pg, pe);
+            row = r2;
+        }
+    } else {
+        for (bool first = true; row < rows; row += stride, first = false) {
+            if (!first) a.load(x, residual, (size_t)row * hidden, q, nvec);
+            a.finish(out, (size_t)row * hidden, q, nvec, invN, eps, pb, pg, pe);
         }
     }
 }
@@ -465,7 +506,7 @@ cudaError_t launch_ln(void* out, const void* x, const void* res, const void* bia
 }
 
 
-template <typename T, int VB, int G, int NV, int NT, int MINB>
+template <typename T, int VB, int G, int NV, int NT, int MINB, bool PF>
 cudaError_t launch_ln_warp(void* out, const void* x, const void* res, const void* bias,
                            const void* gamma, const void* beta, int64_t rows, int hidden,
                            float eps, cudaStream_t st) {
@@ -473,7 +514,7 @@ cudaError_t launch_ln_warp(void* out, const void* x, const void* res, const void
     if (rows >= (int64_t)0xffffffffLL)
         return launch_ln<T, VB, G, NV, 1, NT, MINB>(out, x, res, bias, gamma, beta, rows, hidden,
                                                     eps, st);
-    auto kern = ln_warp_kernel<T, VB, G, NV, NT, MINB>;
+    auto kern = ln_warp_kernel<T, VB, G, NV, NT, MINB, PF>;
     const size_t smem = (size_t)3 * hidden * sizeof(float);
     static std::atomic<int> attr_done{0};
     if (smem > 48 * 1024 && attr_done.load() < (int)smem) {
@@ -515,12 +556,13 @@ struct LnTier {
             "ln_rows<" TN ",V" #VB ",G" #G ",NV" #NV ",R" #R ",T" #NT ",M" #MINB ">"      \
     }
 
-#define TT_LN_WARP(AUTO, T, TN, VB, G, NV, NT, MINB)                                      \
+#define TT_LN_WARP_P(AUTO, T, TN, VB, G, NV, NT, MINB, PF)                                 \
     LnTier {                                                                               \
         VB, (VB) / (int)sizeof(T), (G) * (NV) * ((VB) / (int)sizeof(T)), AUTO,             \
-            &launch_ln_warp<T, VB, G, NV, NT, MINB>,                                       \
-            "ln_warp<" TN ",V" #VB ",G" #G ",NV" #NV ",T" #NT ",M" #MINB ">"              \
+            &launch_ln_warp<T, VB, G, NV, NT, MINB, PF>,                                   \
+            "ln_warp<" TN ",V" #VB ",G" #G ",NV" #NV ",T" #NT ",M" #MINB ",PF" #PF ">"    \
     }
+#define TT_LN_WARP(AUTO, T, TN, VB, G, NV, NT, MINB) TT_LN_WARP_P(AUTO, T, TN, VB, G, NV, NT, MINB, 0)
 
 #define TT_LN_TMA_K(AUTO, T, TN, NV, NW, KB)                                               \
     LnTier {                                                                               \
@@ -564,7 +606,12 @@ struct LnTier {
     TT_LN_TMA_K(false, T, TN, 4, 4, 12), TT_LN_TMA_K(false, T, TN, 4, 4, 16),                   \
     TT_LN_TMA_K(false, T, TN, 4, 8, 12), TT_LN_TMA_K(false, T, TN, 3, 4, 12),                   \
     TT_LN_TMA_K(false, T, TN, 3, 8, 12), TT_LN_TMA_K(false, T, TN, 8, 4, 12),                   \
-    TT_LN_TMA_K(false, T, TN, 4, 2, 16), TT_LN_TMA_K(false, T, TN, 3, 2, 16)
+    TT_LN_TMA_K(false, T, TN, 4, 2, 16), TT_LN_TMA_K(false, T, TN, 3, 2, 16),                   \
+    TT_LN_WARP_P(false, T, TN, 32, 32, 2, 256, 2, 1), TT_LN_WARP_P(false, T, TN, 32, 32, 2, 256, 3, 1), \
+    TT_LN_WARP_P(false, T, TN, 32, 32, 2, 128, 6, 1), TT_LN_WARP_P(false, T, TN, 16, 32, 3, 256, 3, 1), \
+    TT_LN_WARP_P(false, T, TN, 16, 32, 3, 256, 2, 1), TT_LN_WARP_P(false, T, TN, 32, 32, 3, 256, 2, 1), \
+    TT_LN_WARP_P(false, T, TN, 32, 32, 3, 128, 4, 1), TT_LN_WARP_P(false, T, TN, 16, 32, 4, 256, 2, 1), \
+    TT_LN_WARP_P(false, T, TN, 32, 32, 1, 256, 4, 1), TT_LN_WARP_P(false, T, TN, 32, 32, 4, 256, 2, 1)
 
 // MA / MB / MC: min CTAs/SM (register cap) for warp tiers holding about
 // 16 / 24-32 / 48-64 fp32 row values per lane.
