@@ -15,6 +15,7 @@
 //         narrowing, vector store.  `out` may alias x or residual exactly:
 //         every element of a row is loaded before any element is stored.
 #include <atomic>
+#include <cstring>
 
 #include "common.cuh"
 #include "launch.h"
@@ -246,7 +247,7 @@ struct LnRow {
 
 template <typename T, int VB, int G, int NV, int NT, int MINB, bool PF>
 __global__ void __launch_bounds__(NT, MINB)
-    ln_warp_kernel(T* out, const T* x, const T* residual, const T* __restrict__ bias,
+    ln_pf_kernel(T* out, const T* x, const T* residual, const T* __restrict__ bias,
                    const T* __restrict__ gamma, const T* __restrict__ beta, uint32_t rows,
                    int hidden, float eps) {
     using Row = LnRow<T, VB, G, NV>;
@@ -262,7 +263,20 @@ __global__ void __launch_bounds__(NT, MINB)
     uint32_t row = blockIdx.x * GPB + threadIdx.x / G;
 
     Row a, b;
-    if (row < rows) a.load(x, residual, (size_t)row * hidden, q, nvec);  // in flight during staging
+    if constexpr (PF) {
+        if (row < rows) a.load(x, residual, (size_t)row * hidden, q, nvec);  // in flight
+    } else if (row < rows) {
+        // warm L2 with the first row while the parameters are staged (no registers held)
+        const size_t off = (size_t)row * hidden;
+#pragma unroll
+        for (int k = 0; k < NV; ++k) {
+            const int vi = q + k * G;
+            if (vi < nvec) {
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(x + off + vi * VE));
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(residual + off + vi * VE));
+            }
+        }
+    }
 
     // stage the three parameter vectors as fp32 (once per persistent CTA)
     for (int i = threadIdx.x; i < 3 * hidden; i += NT) {
@@ -289,9 +303,111 @@ __global__ void __launch_bounds__(NT, MINB)
             row = r2;
         }
     } else {
-        for (bool first = true; row < rows; row += stride, first = false) {
-            if (!first) a.load(x, residual, (size_t)row * hidden, q, nvec);
+        for (; row < rows; row += stride) {
+            a.load(x, residual, (size_t)row * hidden, q, nvec);
             a.finish(out, (size_t)row * hidden, q, nvec, invN, eps, pb, pg, pe);
+        }
+    }
+}
+
+
+// Non-prefetching warp tier (PF = 0): loads and unpacks interleaved per vector.
+template <typename T, int VB, int G, int NV, int NT, int MINB>
+__global__ void __launch_bounds__(NT, MINB)
+    ln_warp_kernel(T* out, const T* x, const T* residual, const T* __restrict__ bias,
+                   const T* __restrict__ gamma, const T* __restrict__ beta, uint32_t rows,
+                   int hidden, float eps) {
+    constexpr int VE = VB / (int)sizeof(T);
+    constexpr int QV = VE / 4;  // float4 quads per vector
+    constexpr int GPB = NT / G;
+    static_assert(G <= 32 && VE % 4 == 0, "warp tier with >= 4-element vectors");
+    extern __shared__ __align__(16) float4 prm[];  // [3][QV][nvec] float4
+    const int nvec = hidden / VE;
+    const float invN = 1.0f / (float)hidden;
+
+    // stage the three parameter vectors as fp32 (once per persistent CTA)
+    for (int i = threadIdx.x; i < 3 * hidden; i += NT) {
+        const int pi = i / hidden, col = i - pi * hidden;
+        const T* src = pi == 0 ? bias : pi == 1 ? gamma : beta;
+        const int c = col / VE, e = col - c * VE;
+        reinterpret_cast<float*>(prm)[(((pi * QV + (e >> 2)) * nvec + c) << 2) + (e & 3)] =
+            Elem<T>::to_f(src[col]);
+    }
+    __syncthreads();
+    const float4* pb = prm;
+    const float4* pg = prm + QV * nvec;
+    const float4* pe = prm + 2 * QV * nvec;
+
+    const int q = threadIdx.x % G;
+    const uint32_t stride = gridDim.x * GPB;
+    for (uint32_t row = blockIdx.x * GPB + threadIdx.x / G; row < rows; row += stride) {
+        const size_t off = (size_t)row * (size_t)hidden;
+        // ---- LN-1
+        float v[NV][VE];
+#pragma unroll
+        for (int k = 0; k < NV; ++k) {
+            const int vi = q + k * G;
+            if (vi < nvec) {
+                Raw<VB> wx, wr;
+                ld_stream<VB>(x + off + vi * VE, wx);
+                ld_stream<VB>(residual + off + vi * VE, wr);
+                float fr[VE];
+                Elem<T>::template unpack<VB>(wx, v[k]);
+                Elem<T>::template unpack<VB>(wr, fr);
+#pragma unroll
+                for (int j = 0; j < QV; ++j) {
+                    const float4 b = pb[j * nvec + vi];
+                    v[k][4 * j + 0] = (v[k][4 * j + 0] + b.x) + fr[4 * j + 0];
+                    v[k][4 * j + 1] = (v[k][4 * j + 1] + b.y) + fr[4 * j + 1];
+                    v[k][4 * j + 2] = (v[k][4 * j + 2] + b.z) + fr[4 * j + 2];
+                    v[k][4 * j + 3] = (v[k][4 * j + 3] + b.w) + fr[4 * j + 3];
+                }
+            } else {
+#pragma unroll
+                for (int e = 0; e < VE; ++e) v[k][e] = 0.f;
+            }
+        }
+        // ---- LN-2: shifted mean, centred variance
+        float sh[1] = {__shfl_sync(0xffffffffu, v[0][0], (int)(threadIdx.x & 31) & ~(G - 1))};
+        float mean[1] = {0.f};
+#pragma unroll
+        for (int k = 0; k < NV; ++k)
+            if (q + k * G < nvec) {
+#pragma unroll
+                for (int e = 0; e < VE; ++e) mean[0] += v[k][e] - sh[0];
+            }
+        group_sum<G, 1>(mean, nullptr);
+        const float mu = fmaf(mean[0], invN, sh[0]);
+        float var[1] = {0.f};
+#pragma unroll
+        for (int k = 0; k < NV; ++k)
+            if (q + k * G < nvec) {
+#pragma unroll
+                for (int e = 0; e < VE; ++e) {
+                    v[k][e] -= mu;
+                    var[0] = fmaf(v[k][e], v[k][e], var[0]);
+                }
+            }
+        group_sum<G, 1>(var, nullptr);
+        const float rstd = rsqrtf(var[0] * invN + eps);
+        // ---- LN-3
+#pragma unroll
+        for (int k = 0; k < NV; ++k) {
+            const int vi = q + k * G;
+            if (vi < nvec) {
+                float y[VE];
+#pragma unroll
+                for (int j = 0; j < QV; ++j) {
+                    const float4 g = pg[j * nvec + vi], b = pe[j * nvec + vi];
+                    y[4 * j + 0] = fmaf(v[k][4 * j + 0] * rstd, g.x, b.x);
+                    y[4 * j + 1] = fmaf(v[k][4 * j + 1] * rstd, g.y, b.y);
+                    y[4 * j + 2] = fmaf(v[k][4 * j + 2] * rstd, g.z, b.z);
+                    y[4 * j + 3] = fmaf(v[k][4 * j + 3] * rstd, g.w, b.w);
+                }
+                Raw<VB> wy;
+                Elem<T>::template pack<VB>(y, wy);
+                st_stream<VB>(out + off + vi * VE, wy);
+            }
         }
     }
 }
@@ -514,7 +630,8 @@ cudaError_t launch_ln_warp(void* out, const void* x, const void* res, const void
     if (rows >= (int64_t)0xffffffffLL)
         return launch_ln<T, VB, G, NV, 1, NT, MINB>(out, x, res, bias, gamma, beta, rows, hidden,
                                                     eps, st);
-    auto kern = ln_warp_kernel<T, VB, G, NV, NT, MINB, PF>;
+    auto kern = PF ? ln_pf_kernel<T, VB, G, NV, NT, MINB, true>
+                   : ln_warp_kernel<T, VB, G, NV, NT, MINB>;
     const size_t smem = (size_t)3 * hidden * sizeof(float);
     static std::atomic<int> attr_done{0};
     if (smem > 48 * 1024 && attr_done.load() < (int)smem) {
@@ -594,6 +711,7 @@ struct LnTier {
     TT_LN_TIER(true, T, TN, SB, 1024, 32, 1, 1024, 1),                                      \
     TT_LN_TIER(false, T, TN, 32, 32, 2, 1, 256, 1), TT_LN_TIER(false, T, TN, 32, 32, 2, 1, 128, 6), \
     TT_LN_TIER(false, T, TN, 16, 32, 3, 1, 256, 1), TT_LN_TIER(false, T, TN, 32, 32, 3, 1, 256, 1), \
+    TT_LN_TIER(false, T, TN, 32, 32, 4, 1, 256, 1), TT_LN_TIER(false, T, TN, 32, 32, 4, 1, 128, 1), \
     TT_LN_TMA(false, T, TN, 3, 8), TT_LN_TMA(false, T, TN, 4, 8), TT_LN_TMA(false, T, TN, 4, 4),       \
     TT_LN_TMA(false, T, TN, 6, 4), TT_LN_TMA(false, T, TN, 8, 4), TT_LN_TMA(false, T, TN, 2, 8),       \
     TT_LN_WARP(false, T, TN, 32, 32, 2, 256, 3), TT_LN_WARP(false, T, TN, 32, 32, 2, 256, 5),   \
@@ -635,11 +753,54 @@ bool fits(const LnTier& t, int64_t hidden, int vec_bytes) {
     return t.vb <= vec_bytes && hidden % t.ve == 0 && hidden <= t.capacity;
 }
 
+// Tuned preferences (tools/tune.py on B200, profiles/*_tune.txt): for rows up
+// to max_hidden, use the named tier when it can serve the call.  Anything not
+// covered falls through to the generic rule below.
+struct Pref {
+    int dtype;
+    int min_hidden, max_hidden;  // applies to min_hidden < hidden <= max_hidden
+    const char* name;
+};
+const Pref kLnPref[] = {
+    {0, 512, 768, "ln_rows<f32,V32,G32,NV3,R1,T256,M1>"},
+    {0, 768, 1024, "ln_rows<f32,V32,G32,NV4,R1,T256,M1>"},
+    {1, 512, 768, "ln_warp<f16,V16,G32,NV3,T256,M2,PF1>"},
+    {1, 768, 1024, "ln_warp<f16,V16,G32,NV4,T256,M2,PF1>"},
+    {2, 512, 768, "ln_warp<bf16,V16,G32,NV3,T256,M2,PF1>"},
+    {2, 768, 1024, "ln_warp<bf16,V16,G32,NV4,T256,M2,PF1>"},
+};
+
+const LnTier* by_name(const LnTier* tab, const char* name) {
+    for (int i = 0; i < kLnN; ++i)
+        if (!strcmp(tab[i].name, name)) return &tab[i];
+    return nullptr;
+}
+
 const LnTier* pick_dtype(int dtype, int64_t hidden, int vec_bytes) {
     const LnTier* tab = table(dtype);
     if (!tab) return nullptr;
     const int f = g_force[dtype].load(std::memory_order_relaxed);
     if (f >= 0 && f < kLnN && fits(tab[f], hidden, vec_bytes)) return &tab[f];
+    // preferred tiers: the one whose (min_hidden, max_hidden] holds this row
+    static const LnTier* pref_tier[sizeof(kLnPref) / sizeof(kLnPref[0])] = {};
+    static std::atomic<bool> pref_init{false};
+    if (!pref_init.load(std::memory_order_acquire)) {
+        for (size_t i = 0; i < sizeof(kLnPref) / sizeof(kLnPref[0]); ++i)
+            pref_tier[i] = by_name(table(kLnPref[i].dtype), kLnPref[i].name);
+        pref_init.store(true, std::memory_order_release);
+    }
+    const LnTier* pbest = nullptr;
+    int pmax = 1 << 30;
+    for (size_t i = 0; i < sizeof(kLnPref) / sizeof(kLnPref[0]); ++i) {
+        const LnTier* t = pref_tier[i];
+        if (kLnPref[i].dtype == dtype && t && hidden <= kLnPref[i].max_hidden &&
+            hidden > kLnPref[i].min_hidden &&
+            kLnPref[i].max_hidden < pmax && fits(*t, hidden, vec_bytes)) {
+            pbest = t;
+            pmax = kLnPref[i].max_hidden;
+        }
+    }
+    if (pbest) return pbest;
     const LnTier* best = nullptr;
     for (int i = 0; i < kLnN; ++i) {
         const LnTier& t = tab[i];

@@ -17,6 +17,7 @@
 // is split into an unaligned head (< VE elements, scalar), an aligned body of
 // VB-byte vectors and a tail (< VE elements, scalar).
 #include <atomic>
+#include <cstring>
 
 #include "common.cuh"
 #include "launch.h"
@@ -713,11 +714,27 @@ const SoftmaxTier* table(int dtype) {
     }
 }
 
+// Tuned preferences (tools/tune.py on B200, profiles/*_tune.txt): for rows of
+// more than min_cols and at most max_cols keys, use the named tier.
+struct Pref {
+    int dtype;
+    int min_cols, max_cols;
+    const char* name;
+};
+const Pref kSmPref[] = {
+    {0, 256, 512, "softmax_warp<f32,V32,G32,NV2,T256,M3,P2>"},
+};
+
 const SoftmaxTier* pick_dtype(int dtype, int64_t Sk) {
     const SoftmaxTier* t = table(dtype);
     if (!t) return nullptr;
     const int f = g_force[dtype].load(std::memory_order_relaxed);
     if (f >= 0 && f < kSmN && Sk <= t[f].max_cols) return &t[f];
+    for (const Pref& pr : kSmPref) {
+        if (pr.dtype != dtype || Sk <= pr.min_cols || Sk > pr.max_cols) continue;
+        for (int i = 0; i < kSmN; ++i)
+            if (!strcmp(t[i].name, pr.name) && Sk <= t[i].max_cols) return &t[i];
+    }
     for (int i = 0; i < kSmN; ++i)
         if (t[i].automatic && Sk <= t[i].max_cols) return &t[i];
     return nullptr;

@@ -122,7 +122,7 @@ def test_launch_without_device_fails_loudly(ttlib):
     (torch.float16, 37, "softmax_warp<f16,V16,G8,NV1,T256,M6,P4>"),
     (torch.bfloat16, 512, "softmax_warp<bf16,V32,G32,NV1,T256,M6,P4>"),
     (torch.float16, 491, "softmax_warp<f16,V32,G32,NV1,T256,M6,P4>"),
-    (torch.float32, 500, "softmax_warp<f32,V32,G32,NV2,T256,M6,P4>"),
+    (torch.float32, 500, "softmax_warp<f32,V32,G32,NV2,T256,M3,P2>"),
     (torch.float32, 4096, "softmax_rows<f32,V32,G128,NV4,R1,T128,M1>"),
     (torch.bfloat16, 32768, "softmax_rows<bf16,V32,G1024,NV2,R1,T1024,M1>"),
 ])
@@ -131,9 +131,9 @@ def test_softmax_tier_plan(ttlib, dtype, Sk, tier):
 
 
 @pytest.mark.parametrize("dtype,hidden,tier", [
-    (torch.float32, 768, "ln_warp<f32,V32,G32,NV3,T256,M3,PF0>"),
-    (torch.float16, 768, "ln_warp<f16,V16,G32,NV3,T256,M4,PF0>"),
-    (torch.bfloat16, 1024, "ln_warp<bf16,V32,G32,NV2,T256,M4,PF0>"),
+    (torch.float32, 768, "ln_rows<f32,V32,G32,NV3,R1,T256,M1>"),
+    (torch.float16, 768, "ln_warp<f16,V16,G32,NV3,T256,M2,PF1>"),
+    (torch.bfloat16, 1024, "ln_warp<bf16,V16,G32,NV4,T256,M2,PF1>"),
     (torch.float32, 37, "ln_rows<f32,V4,G32,NV4,R1,T256,M1>"),
     (torch.float16, 16, "ln_warp<f16,V16,G4,NV1,T256,M4,PF0>"),
     (torch.float32, 4096, "ln_rows<f32,V32,G128,NV4,R1,T128,M1>"),
