@@ -764,9 +764,9 @@ struct Pref {
 const Pref kLnPref[] = {
     {0, 512, 768, "ln_rows<f32,V32,G32,NV3,R1,T256,M1>"},
     {0, 768, 1024, "ln_rows<f32,V32,G32,NV4,R1,T256,M1>"},
-    {1, 512, 768, "ln_warp<f16,V16,G32,NV3,T256,M2,PF1>"},
+    {1, 512, 768, "ln_warp<f16,V16,G32,NV4,T256,M2,PF1>"},
     {1, 768, 1024, "ln_warp<f16,V16,G32,NV4,T256,M2,PF1>"},
-    {2, 512, 768, "ln_warp<bf16,V16,G32,NV3,T256,M2,PF1>"},
+    {2, 512, 768, "ln_warp<bf16,V16,G32,NV4,T256,M2,PF1>"},
     {2, 768, 1024, "ln_warp<bf16,V16,G32,NV4,T256,M2,PF1>"},
 };
 

@@ -132,7 +132,7 @@ def test_softmax_tier_plan(ttlib, dtype, Sk, tier):
 
 @pytest.mark.parametrize("dtype,hidden,tier", [
     (torch.float32, 768, "ln_rows<f32,V32,G32,NV3,R1,T256,M1>"),
-    (torch.float16, 768, "ln_warp<f16,V16,G32,NV3,T256,M2,PF1>"),
+    (torch.float16, 768, "ln_warp<f16,V16,G32,NV4,T256,M2,PF1>"),
     (torch.bfloat16, 1024, "ln_warp<bf16,V16,G32,NV4,T256,M2,PF1>"),
     (torch.float32, 37, "ln_rows<f32,V4,G32,NV4,R1,T256,M1>"),
     (torch.float16, 16, "ln_warp<f16,V16,G4,NV1,T256,M4,PF0>"),
