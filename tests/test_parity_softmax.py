@@ -124,6 +124,19 @@ def test_long_rows_and_tier_boundaries(ttlib, dtype, Sk):
 
 
 @pytest.mark.parametrize("dtype", DT)
+@pytest.mark.parametrize("Sk", [491, 500, 512, 257])
+def test_short_requests_narrow_groups(ttlib, dtype, Sk):
+    """Requests whose rows fill whole CTAs take the narrow-group path (4/8/16
+    lanes per row + zero-filled padding vectors); every boundary of those
+    widths, aligned and odd pitches."""
+    lens = [1, 5, 31, 32, 33, 63, 64, 65, 127, 128, 129, 200, 255, 256, Sk - 1, Sk, 0]
+    x = W.scores(len(lens), 4, 16, Sk, dtype, seed=Sk)
+    _full_check(ttlib, x, lens, W.SCALE_BERT, f"narrow Sk={Sk}")
+    xp = W.poison_masked(x, lens)
+    _full_check(ttlib, xp, lens, -0.25, f"narrow poison Sk={Sk}")
+
+
+@pytest.mark.parametrize("dtype", DT)
 def test_length_edge_values(ttlib, dtype):
     Sk = 70
     lens = [0, -5, 1, 69, 70, 71, 1 << 30, -(1 << 30)]
