@@ -92,6 +92,38 @@ TT_API tt_status tt_softmax_masked_bf16(void* scores, const int32_t* lengths, in
                                  int64_t Sq, int64_t Sk, float scale, cudaStream_t stream);
 
 /* ------------------------------------------------------------------------
+ * Packed (padding-free) attention softmax, in place -- SURVEY §8(f) NEXT-1:
+ * the variable-length batch of PAPER.md §5 (l.576, "all requests in the batch
+ * will be zero-padded with regards to the maximum length") stored WITHOUT the
+ * padding.  Request r (0 <= r < num_req) has L_r = cu_seqlens[r+1] -
+ * cu_seqlens[r] tokens and its scores are a dense row-major [H, L_r, L_r]
+ * block starting at element cu_blocks[r]; every row is softmax(scale * x)
+ * over its L_r keys (no masked keys, no padding bytes read or written).
+ *
+ * scores      DEVICE, storage dtype of the entry point, 16-byte aligned base.
+ * cu_seqlens  DEVICE int32[num_req + 1], cu_seqlens[0] = 0, nondecreasing.
+ * cu_blocks   DEVICE int64[num_req], element offset of each request's block
+ *             (dense packing: cu_blocks[r] = H * sum_{i<r} L_i^2).
+ * total_tokens  HOST copy of cu_seqlens[num_req] (sizes the grid).
+ * max_seqlen  HOST upper bound of every L_r (selects the tier); a request
+ *             longer than max_seqlen is undefined (memory-safe, values wrong).
+ * Errors as above; max_seqlen > 1024 (fp32) / 2048 (fp16, bf16) or
+ * H * total_tokens >= 2^32 gives TT_ERROR_NOT_SUPPORTED.
+ * ---------------------------------------------------------------------- */
+TT_API tt_status tt_softmax_packed_f32(float* scores, const int32_t* cu_seqlens,
+                                       const int64_t* cu_blocks, int64_t num_req, int64_t H,
+                                       int64_t total_tokens, int64_t max_seqlen, float scale,
+                                       cudaStream_t stream);
+TT_API tt_status tt_softmax_packed_f16(void* scores, const int32_t* cu_seqlens,
+                                       const int64_t* cu_blocks, int64_t num_req, int64_t H,
+                                       int64_t total_tokens, int64_t max_seqlen, float scale,
+                                       cudaStream_t stream);
+TT_API tt_status tt_softmax_packed_bf16(void* scores, const int32_t* cu_seqlens,
+                                        const int64_t* cu_blocks, int64_t num_req, int64_t H,
+                                        int64_t total_tokens, int64_t max_seqlen, float scale,
+                                        cudaStream_t stream);
+
+/* ------------------------------------------------------------------------
  * Fused add-bias + residual + LayerNorm:  AddBiasLayerNorm (
  * "fusing all the kernels between two GEMM kernels into a single one",
  * l.302; variance per Eq. 1, l.406-409, population form)
@@ -157,6 +189,7 @@ TT_API int tt_version(void);
 TT_API tt_status tt_softmax_masked_plan(int dtype, int64_t B, int64_t H, int64_t Sq, int64_t Sk,
                                  char* buf, int cap);
 TT_API tt_status tt_add_bias_layernorm_plan(int dtype, int64_t rows, int64_t hidden, char* buf, int cap);
+TT_API tt_status tt_softmax_packed_plan(int dtype, int64_t max_seqlen, char* buf, int cap);
 
 #ifdef __cplusplus
 }

@@ -137,3 +137,24 @@ def layernorm_onepass_eq1(x, gamma, beta, eps: float) -> torch.Tensor:
                                            rows, hidden, ctypes.c_float(eps), _ptr(out))
     assert rc == 0
     return out
+
+
+def softmax_packed(flat: torch.Tensor, lengths, H: int, scale: float) -> torch.Tensor:
+    """Packed (padding-free) softmax: request r is a dense [H, L_r, L_r] block,
+    blocks concatenated in request order; each block is the masked softmax with
+    every key valid.  Returns float64 of flat's shape."""
+    src = _host(flat).reshape(-1)
+    lens = [int(v) for v in np.asarray(lengths).reshape(-1)]
+    if sum(H * L * L for L in lens) != src.numel():
+        raise ValueError("flat size does not match the lengths")
+    out = torch.empty(src.shape, dtype=torch.float64)
+    off = 0
+    for L in lens:
+        n = H * L * L
+        if n:
+            out[off:off + n] = softmax_masked(src[off:off + n].reshape(1, H, L, L), [L],
+                                              scale).reshape(-1)
+        off += n
+    if off != src.numel():
+        raise ValueError("flat size does not match the lengths")
+    return out

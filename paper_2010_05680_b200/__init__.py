@@ -8,9 +8,10 @@ from ._lib import (  # noqa: F401
     EXPORTS, TT_ERROR_CUDA, TT_ERROR_INVALID_VALUE, TT_ERROR_NOT_SUPPORTED, TT_MAX_LN_HIDDEN,
     TT_MAX_SOFTMAX_COLS, TT_SUCCESS, TTError, force_tier, layernorm_plan, lib, softmax_plan, status_string,
     tt_add_bias_layernorm, tt_add_bias_layernorm_raw, tt_add_bias_layernorm_staged,
-    tt_softmax_masked, tt_softmax_masked_raw, tt_softmax_masked_staged, tiers, version)
+    tt_softmax_masked, tt_softmax_masked_raw, tt_softmax_masked_staged, tiers, version,
+    packed_offsets, tt_softmax_packed, softmax_packed_plan)
 
 __all__ = [
-    "tt_softmax_masked", "tt_add_bias_layernorm", "tt_softmax_masked_staged",
+    "tt_softmax_masked", "tt_softmax_packed", "packed_offsets", "tt_add_bias_layernorm", "tt_softmax_masked_staged",
     "tt_add_bias_layernorm_staged", "softmax_plan", "layernorm_plan", "TTError", "lib",
 ]

@@ -29,9 +29,10 @@ _SUFFIX = {torch.float32: "f32", torch.float16: "f16", torch.bfloat16: "bf16"}
 EXPORTS = (
     "tt_softmax_masked_f32", "tt_softmax_masked_f16", "tt_softmax_masked_bf16",
     "tt_add_bias_layernorm_f32", "tt_add_bias_layernorm_f16", "tt_add_bias_layernorm_bf16",
+    "tt_softmax_packed_f32", "tt_softmax_packed_f16", "tt_softmax_packed_bf16",
     "tt_softmax_masked_staged", "tt_add_bias_layernorm_staged",
     "tt_status_string", "tt_last_cuda_error", "tt_version",
-    "tt_softmax_masked_plan", "tt_add_bias_layernorm_plan",
+    "tt_softmax_masked_plan", "tt_add_bias_layernorm_plan", "tt_softmax_packed_plan",
     "ttx_tier_count", "ttx_tier_name", "ttx_force_tier",
 )
 
@@ -64,6 +65,10 @@ def lib() -> ctypes.CDLL:
             for s in ("f32", "f16", "bf16"):
                 getattr(L, f"tt_softmax_masked_{s}").argtypes = sm
                 getattr(L, f"tt_add_bias_layernorm_{s}").argtypes = ln
+            pk = [_vp, _vp, _vp, _i64, _i64, _i64, _i64, _f, _vp]
+            for s in ("f32", "f16", "bf16"):
+                getattr(L, f"tt_softmax_packed_{s}").argtypes = pk
+            L.tt_softmax_packed_plan.argtypes = [_i, _i64, ctypes.c_char_p, _i]
             L.tt_softmax_masked_staged.argtypes = [_i, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _i64,
                                                    _f, _vp]
             L.tt_add_bias_layernorm_staged.argtypes = [_i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
@@ -154,6 +159,45 @@ def softmax_plan(dtype: torch.dtype, B: int, H: int, Sq: int, Sk: int) -> str:
     buf = ctypes.create_string_buffer(128)
     _check(lib().tt_softmax_masked_plan(DTYPE_CODE[dtype], B, H, Sq, Sk, buf, 128),
            "tt_softmax_masked_plan")
+    return buf.value.decode()
+
+
+# ---------------------------------------------------------------------- packed
+def packed_offsets(lengths, H: int, device="cuda"):
+    """cu_seqlens (int32[n+1]) and dense block offsets cu_blocks (int64[n],
+    H * sum_{i<r} L_i^2) for requests of the given lengths (host plumbing)."""
+    lens = torch.as_tensor(lengths, dtype=torch.int64).cpu()
+    cu = torch.zeros(lens.numel() + 1, dtype=torch.int64)
+    cu[1:] = torch.cumsum(lens, 0)
+    blocks = torch.zeros(lens.numel(), dtype=torch.int64)
+    if lens.numel() > 1:
+        blocks[1:] = torch.cumsum(H * lens * lens, 0)[:-1]
+    return cu.to(torch.int32).to(device), blocks.to(device), int(cu[-1]), int(
+        (H * lens * lens).sum())
+
+
+def tt_softmax_packed(scores: torch.Tensor, cu_seqlens: torch.Tensor, cu_blocks: torch.Tensor,
+                      H: int, total_tokens: int, max_seqlen: int, scale: float, stream=None):
+    """In place: every [H, L_r, L_r] block of the packed `scores` buffer
+    (tt_softmax_packed_{f32,f16,bf16})."""
+    _dev(scores, "scores")
+    _dev(cu_seqlens, "cu_seqlens")
+    _dev(cu_blocks, "cu_blocks")
+    if cu_seqlens.dtype != torch.int32 or cu_blocks.dtype != torch.int64:
+        raise ValueError("cu_seqlens must be int32, cu_blocks int64")
+    n = cu_blocks.numel()
+    if cu_seqlens.numel() != n + 1:
+        raise ValueError("cu_seqlens must have num_req + 1 entries")
+    fn = getattr(lib(), f"tt_softmax_packed_{_SUFFIX[scores.dtype]}")
+    _check(fn(scores.data_ptr(), cu_seqlens.data_ptr(), cu_blocks.data_ptr(), n, H, total_tokens,
+              max_seqlen, float(scale), _stream_ptr(stream)), fn.__name__)
+    return scores
+
+
+def softmax_packed_plan(dtype: torch.dtype, max_seqlen: int) -> str:
+    buf = ctypes.create_string_buffer(128)
+    _check(lib().tt_softmax_packed_plan(DTYPE_CODE[dtype], max_seqlen, buf, 128),
+           "tt_softmax_packed_plan")
     return buf.value.decode()
 
 

@@ -20,8 +20,8 @@ CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(PKG, "libtt.so")
 BUILD_DIR = os.path.join(PKG, "_build")
-SOURCES = ["tt_api.cu", "softmax.cu", "layernorm.cu"]
-HEADERS = ["common.cuh", "launch.h"]
+SOURCES = ["tt_api.cu", "softmax.cu", "softmax_packed.cu", "layernorm.cu"]
+HEADERS = ["common.cuh", "launch.h", "softmax_row.cuh"]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 GENCODE = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -14,6 +14,15 @@ cudaError_t softmax_launch(int dtype, void* scores, const int32_t* lengths, int6
                            bool* supported);
 const char* softmax_tier_name(int dtype, int64_t Sk);
 
+// Packed (padding-free) softmax: request r is a dense [H, L_r, L_r] block at
+// element offset cu_blocks[r]; L_r = cu_seqlens[r+1] - cu_seqlens[r] <= max_len.
+cudaError_t softmax_packed_launch(int dtype, void* scores, const int32_t* cu_seqlens,
+                                  const int64_t* cu_blocks, int64_t num_req, int64_t H,
+                                  int64_t total_tokens, int64_t max_len, float scale,
+                                  cudaStream_t stream, bool* supported);
+const char* softmax_packed_tier_name(int dtype, int64_t max_len);
+int softmax_packed_max_len(int dtype);
+
 // vec_bytes: widest vector width (bytes) that every operand's alignment and
 // the row pitch allow (host-computed in tt_api.cu).
 cudaError_t layernorm_launch(int dtype, void* out, const void* x, const void* residual,

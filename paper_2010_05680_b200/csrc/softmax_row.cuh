@@ -1,0 +1,167 @@
+// softmax_row.cuh -- the per-row body of the warp / sub-warp softmax tiers,
+// shared by the padded kernel (softmax.cu) and the packed, padding-free
+// kernel (softmax_packed.cu).  See softmax.cu for the design notes.
+#pragma once
+
+#include "common.cuh"
+
+namespace tt {
+
+__device__ __forceinline__ float rcp_approx(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+// One row on a group of GC lanes (GC <= 32), NVC vectors per lane.  `live`
+// false: the group has no row this step (it still joins the shuffles, which use
+// the full warp mask).  NARROW: the request is short enough that every valid key
+// lies in the head and the first GC body vectors; the remaining body vectors
+// are written as zeros without any arithmetic.
+template <typename T, int VB, int GC, int NVC, bool ALIGNED, bool NARROW>
+__device__ __forceinline__ void softmax_row_pass(T* __restrict__ p, bool live, int L, int Sk,
+                                                 float c, int q) {
+    constexpr int VE = VB / (int)sizeof(T);
+    constexpr int HI = ALIGNED ? 0 : (VE - 1 + GC - 1) / GC;
+    constexpr int HIA = HI > 0 ? HI : 1;
+    const bool up = c > 0.f;  // max of raw x (else min); c != 0 (host)
+    const float sent = up ? -INFINITY : INFINITY;
+    if (!live) L = 0;
+    int hd = 0, nv = Sk / VE;
+    if constexpr (!ALIGNED) {
+        const int mis = (int)((reinterpret_cast<uintptr_t>(p) & (VB - 1)) / sizeof(T));
+        hd = mis ? min(VE - mis, Sk) : 0;
+        nv = (Sk - hd) / VE;
+    }
+    const int tl0 = hd + nv * VE;
+    // masking is needed unless every key is valid and every vector slot of
+    // the group maps onto the row (uniform within the group)
+    const bool masked = (L < Sk) || (nv != GC * NVC);
+
+    // ---- SM-2: load (never predicated off; see above)
+    float v[NVC][VE];
+    if (L > 0) {
+        // fallback address for lanes past the prefix: the first body vector,
+        // or (row shorter than its head) the VB-aligned vector containing p
+        const T* fb = nv > 0 ? p + hd
+                             : reinterpret_cast<const T*>(reinterpret_cast<uintptr_t>(p) &
+                                                          ~(uintptr_t)(VB - 1));
+#pragma unroll
+        for (int k = 0; k < NVC; ++k) {
+            const int vi = q + k * GC;
+            const int j0 = hd + vi * VE;
+            const bool in = vi < nv && j0 < L;
+            Raw<VB> w;
+            ld_stream<VB>(in ? p + j0 : fb, w);
+            Elem<T>::template unpack<VB>(w, v[k]);
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < NVC; ++k)
+#pragma unroll
+            for (int e = 0; e < VE; ++e) v[k][e] = sent;
+    }
+    if (masked) {
+#pragma unroll
+        for (int k = 0; k < NVC; ++k) {
+            const int vi = q + k * GC;
+            const int nvalid = vi < nv ? min(max(L - (hd + vi * VE), 0), VE) : 0;
+#pragma unroll
+            for (int e = 0; e < VE; ++e) v[k][e] = e < nvalid ? v[k][e] : sent;
+        }
+    }
+    float hv[HIA], tv[HIA];
+    if constexpr (!ALIGNED) {
+#pragma unroll
+        for (int i = 0; i < HI; ++i) {
+            const int jh = q + i * GC, jt = tl0 + q + i * GC;
+            const bool ih = jh < hd && jh < L, it = jt < Sk && jt < L;
+            const float a = Elem<T>::to_f(p[ih ? jh : 0]);
+            const float b = Elem<T>::to_f(p[it ? jt : 0]);
+            hv[i] = ih ? a : sent;
+            tv[i] = it ? b : sent;
+        }
+    }
+
+    // ---- SM-3: row max of the scaled logits, c * (max or min of raw x)
+    float m[1];
+    {
+        float a = sent;
+        if (up) {
+#pragma unroll
+            for (int k = 0; k < NVC; ++k)
+#pragma unroll
+                for (int e = 0; e < VE; ++e) a = fmaxf(a, v[k][e]);
+            if constexpr (!ALIGNED) {
+#pragma unroll
+                for (int i = 0; i < HI; ++i) a = fmaxf(a, fmaxf(hv[i], tv[i]));
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < NVC; ++k)
+#pragma unroll
+                for (int e = 0; e < VE; ++e) a = fminf(a, v[k][e]);
+            if constexpr (!ALIGNED) {
+#pragma unroll
+                for (int i = 0; i < HI; ++i) a = fminf(a, fminf(hv[i], tv[i]));
+            }
+        }
+        m[0] = up ? a : -a;
+    }
+    group_max<GC, 1>(m, nullptr);
+    float nm = -((up ? m[0] : -m[0]) * c);  // -max_j (c * x_j)
+    if (!(fabsf(nm) <= 3.0e38f)) nm = 0.f;  // empty row (L = 0)
+
+    // ---- SM-4: e_j = 2^(c x_j - m), once (sentinel -> +0.0); s = sum e_j
+    float s[1] = {0.f};
+#pragma unroll
+    for (int k = 0; k < NVC; ++k)
+#pragma unroll
+        for (int e = 0; e < VE; ++e) {
+            v[k][e] = ex2_approx(fmaf(v[k][e], c, nm));
+            s[0] += v[k][e];
+        }
+    if constexpr (!ALIGNED) {
+#pragma unroll
+        for (int i = 0; i < HI; ++i) {
+            hv[i] = ex2_approx(fmaf(hv[i], c, nm));
+            tv[i] = ex2_approx(fmaf(tv[i], c, nm));
+            s[0] += hv[i] + tv[i];
+        }
+    }
+    group_sum<GC, 1>(s, nullptr);
+    // masked keys hold e = +0.0, so y = e * inv is +0.0 there; L = 0 -> inv = 0.
+    // For L > 0, s >= 1 (the max key contributes 1) or NaN (NaN keys propagate).
+    const float inv = L > 0 ? rcp_approx(s[0]) : 0.f;
+    if (!live) return;
+
+    // ---- SM-5: normalise and store every column
+#pragma unroll
+    for (int k = 0; k < NVC; ++k) {
+        const int vi = q + k * GC;
+        if (vi < nv) {
+            float y[VE];
+#pragma unroll
+            for (int e = 0; e < VE; ++e) y[e] = v[k][e] * inv;
+            Raw<VB> w;
+            Elem<T>::template pack<VB>(y, w);
+            st_stream<VB>(p + hd + vi * VE, w);
+        }
+    }
+    if constexpr (NARROW) {
+        Raw<VB> z;
+#pragma unroll
+        for (int i = 0; i < Raw<VB>::W; ++i) z.w[i] = 0u;
+        for (int vi = GC * NVC + q; vi < nv; vi += GC) st_stream<VB>(p + hd + vi * VE, z);
+    }
+    if constexpr (!ALIGNED) {
+#pragma unroll
+        for (int i = 0; i < HI; ++i) {
+            const int jh = q + i * GC, jt = tl0 + q + i * GC;
+            if (jh < hd) p[jh] = Elem<T>::from_f(hv[i] * inv);
+            if (jt < Sk) p[jt] = Elem<T>::from_f(tv[i] * inv);
+        }
+    }
+}
+
+}  // namespace tt

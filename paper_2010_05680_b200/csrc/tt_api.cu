@@ -135,6 +135,43 @@ tt_status ln_any(int dtype, void* out, const void* x, const void* residual, cons
     return cuda_status(e);
 }
 
+// ------------------------------------------------------------------- packed
+tt_status packed_validate(int dtype, const void* scores, const int32_t* cu, const int64_t* blocks,
+                          int64_t num_req, int64_t H, int64_t total_tokens, int64_t max_len,
+                          float scale, bool check_ptrs, bool* empty) {
+    if (dtype < 0 || dtype > 2) return TT_ERROR_INVALID_VALUE;
+    if (num_req < 0 || H < 0 || total_tokens < 0 || max_len < 0) return TT_ERROR_INVALID_VALUE;
+    if (!isfinite(scale)) return TT_ERROR_INVALID_VALUE;
+    if (num_req > 0x7fffffffLL) return TT_ERROR_INVALID_VALUE;
+    *empty = (num_req == 0 || H == 0 || total_tokens == 0 || max_len == 0);
+    if (*empty) return TT_SUCCESS;
+    if (check_ptrs) {
+        if (!scores || !cu || !blocks) return TT_ERROR_INVALID_VALUE;
+        if (!aligned16(scores) || (reinterpret_cast<uintptr_t>(cu) & 3u) ||
+            (reinterpret_cast<uintptr_t>(blocks) & 7u))
+            return TT_ERROR_NOT_SUPPORTED;
+    }
+    int64_t rows;
+    if (mul_overflows(H, total_tokens, &rows) || rows >= (int64_t)0xffffffffLL)
+        return TT_ERROR_NOT_SUPPORTED;
+    if (max_len > tt::softmax_packed_max_len(dtype)) return TT_ERROR_NOT_SUPPORTED;
+    return TT_SUCCESS;
+}
+
+tt_status packed_any(int dtype, void* scores, const int32_t* cu, const int64_t* blocks,
+                     int64_t num_req, int64_t H, int64_t total_tokens, int64_t max_len,
+                     float scale, cudaStream_t stream) {
+    bool empty = false;
+    tt_status s = packed_validate(dtype, scores, cu, blocks, num_req, H, total_tokens, max_len,
+                                  scale, true, &empty);
+    if (s != TT_SUCCESS || empty) return s;
+    bool supported = false;
+    cudaError_t e = tt::softmax_packed_launch(dtype, scores, cu, blocks, num_req, H, total_tokens,
+                                              max_len, scale, stream, &supported);
+    if (!supported) return TT_ERROR_NOT_SUPPORTED;
+    return cuda_status(e);
+}
+
 void copy_name(const char* name, char* buf, int cap) {
     if (!buf || cap <= 0) return;
     snprintf(buf, (size_t)cap, "%s", name ? name : "");
@@ -155,6 +192,26 @@ tt_status tt_softmax_masked_f16(void* scores, const int32_t* lengths, int64_t B,
 tt_status tt_softmax_masked_bf16(void* scores, const int32_t* lengths, int64_t B, int64_t H,
                                  int64_t Sq, int64_t Sk, float scale, cudaStream_t stream) {
     return softmax_any(2, scores, lengths, B, H, Sq, Sk, scale, stream);
+}
+
+tt_status tt_softmax_packed_f32(float* scores, const int32_t* cu_seqlens, const int64_t* cu_blocks,
+                                int64_t num_req, int64_t H, int64_t total_tokens,
+                                int64_t max_seqlen, float scale, cudaStream_t stream) {
+    return packed_any(0, scores, cu_seqlens, cu_blocks, num_req, H, total_tokens, max_seqlen,
+                      scale, stream);
+}
+tt_status tt_softmax_packed_f16(void* scores, const int32_t* cu_seqlens, const int64_t* cu_blocks,
+                                int64_t num_req, int64_t H, int64_t total_tokens,
+                                int64_t max_seqlen, float scale, cudaStream_t stream) {
+    return packed_any(1, scores, cu_seqlens, cu_blocks, num_req, H, total_tokens, max_seqlen,
+                      scale, stream);
+}
+tt_status tt_softmax_packed_bf16(void* scores, const int32_t* cu_seqlens,
+                                 const int64_t* cu_blocks, int64_t num_req, int64_t H,
+                                 int64_t total_tokens, int64_t max_seqlen, float scale,
+                                 cudaStream_t stream) {
+    return packed_any(2, scores, cu_seqlens, cu_blocks, num_req, H, total_tokens, max_seqlen,
+                      scale, stream);
 }
 
 tt_status tt_add_bias_layernorm_f32(float* out, const float* x, const float* residual,
@@ -263,6 +320,18 @@ tt_status tt_add_bias_layernorm_plan(int dtype, int64_t rows, int64_t hidden, ch
             break;
         }
     copy_name(tt::layernorm_tier_name(dtype, hidden, vb), buf, cap);
+    return TT_SUCCESS;
+}
+
+tt_status tt_softmax_packed_plan(int dtype, int64_t max_seqlen, char* buf, int cap) {
+    bool empty = false;
+    tt_status s = packed_validate(dtype, nullptr, nullptr, nullptr, 1, 1, 1, max_seqlen, 1.0f,
+                                  false, &empty);
+    if (s != TT_SUCCESS) {
+        copy_name("", buf, cap);
+        return s;
+    }
+    copy_name(empty ? "none" : tt::softmax_packed_tier_name(dtype, max_seqlen), buf, cap);
     return TT_SUCCESS;
 }
 

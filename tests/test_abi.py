@@ -156,3 +156,24 @@ def test_tier_enumeration_and_force(ttlib):
         assert ttlib.softmax_plan(torch.bfloat16, 1, 1, 1, 8) == ttlib.tiers("softmax", torch.bfloat16)[0]
     finally:
         ttlib.force_tier("softmax", torch.bfloat16, -1)
+
+
+@pytest.mark.parametrize("dtype", DT)
+def test_packed_validation(ttlib, dtype):
+    L = ttlib.lib()
+    f = getattr(L, f"tt_softmax_packed_{ {torch.float32: 'f32', torch.float16: 'f16', torch.bfloat16: 'bf16'}[dtype]}")
+    INV, NS, OK = 1, 2, 0
+    cap = 1024 if dtype == torch.float32 else 2048
+    assert f(0, FAKE, FAKE, 4, 12, 100, 50, 1.0, 0) == INV              # null scores
+    assert f(FAKE, 0, FAKE, 4, 12, 100, 50, 1.0, 0) == INV
+    assert f(FAKE, FAKE, 0, 4, 12, 100, 50, 1.0, 0) == INV
+    assert f(FAKE, FAKE, FAKE, -1, 12, 100, 50, 1.0, 0) == INV
+    assert f(FAKE, FAKE, FAKE, 4, 12, 100, 50, float("nan"), 0) == INV
+    assert f(FAKE + 2, FAKE, FAKE, 4, 12, 100, 50, 1.0, 0) == NS
+    assert f(FAKE, FAKE + 2, FAKE, 4, 12, 100, 50, 1.0, 0) == NS
+    assert f(FAKE, FAKE, FAKE + 4, 4, 12, 100, 50, 1.0, 0) == NS
+    assert f(FAKE, FAKE, FAKE, 4, 12, 100, cap + 1, 1.0, 0) == NS
+    assert f(FAKE, FAKE, FAKE, 4, 1 << 20, 1 << 13, 50, 1.0, 0) == NS   # rows >= 2^32
+    for args in ((0, 12, 100, 50), (4, 0, 100, 50), (4, 12, 0, 50), (4, 12, 100, 0)):
+        assert f(0, 0, 0, *args, 1.0, 0) == OK
+    assert ttlib.softmax_packed_plan(dtype, 512).startswith("softmax_packed<")

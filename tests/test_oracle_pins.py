@@ -275,3 +275,18 @@ def test_oracle_argument_errors():
         oracle.widen(torch.zeros(3, dtype=torch.int32))
     # empty shapes are no-ops
     assert oracle.softmax_masked(torch.zeros(0, 2, 2, 2), [], 1.0).numel() == 0
+
+
+def test_packed_equals_padded_valid_blocks():
+    """The packed layout holds exactly the valid
+    [H, L_r, L_r] blocks of the padded masked softmax (P:l.576 padding)."""
+    lens = [5, 1, 0, 9, 3, 9]
+    H, S = 2, 9
+    x = W.scores(len(lens), H, S, S, torch.float32, seed=17)
+    padded = oracle.softmax_masked(W.poison_masked(x, lens), lens, 0.125)
+    flat = torch.cat([x[b, :, :L, :L].reshape(-1) for b, L in enumerate(lens)])
+    packed = oracle.softmax_packed(flat, lens, H, 0.125)
+    ref = torch.cat([padded[b, :, :L, :L].reshape(-1) for b, L in enumerate(lens)])
+    assert torch.equal(packed, ref)
+    with pytest.raises(ValueError):
+        oracle.softmax_packed(flat[:-1], lens, H, 0.125)
