@@ -47,24 +47,38 @@ UNIT = "GB/s"
 class Workload:
     """A list of (softmax batch, LN batch) units resident on one device."""
 
-    def __init__(self, name, dtype, heads, hidden, batches, scale=W.SCALE_BERT, eps=W.EPS_BERT):
+    def __init__(self, name, dtype, heads, hidden, batches, scale=W.SCALE_BERT, eps=W.EPS_BERT,
+                 packed=False):
         self.name, self.dtype, self.heads, self.hidden = name, dtype, heads, hidden
         self.batches = batches          # list of np.int32 length arrays (one per batch)
         self.scale, self.eps = scale, eps
         self.e = W.ELEM_BYTES[dtype]
+        # packed: padding-free layout (SURVEY §8(f) NEXT-1): request r is a dense
+        # [H, L_r, L_r] block; LayerNorm runs on sum(L_r) tokens
+        self.packed = packed
 
     def shapes(self, lens):
         S = int(lens.max())
+        if self.packed:
+            return (int(self.heads * (lens.astype(np.int64) ** 2).sum()),), (int(lens.sum()),
+                                                                              self.hidden)
         return (len(lens), self.heads, S, S), (len(lens) * S, self.hidden)
 
     def bytes_softmax(self, lens):
+        if self.packed:   # every key read once and written once, + cu_seqlens / cu_blocks
+            return int(2 * self.heads * (lens.astype(np.int64) ** 2).sum() * self.e
+                       + 12 * len(lens) + 4)
         S = int(lens.max())
         return W.softmax_bytes_alg(lens, self.heads, S, S, self.e)
 
     def bytes_ln(self, lens):
+        if self.packed:
+            return W.ln_bytes_alg(int(lens.sum()), self.hidden, self.e)
         return W.ln_bytes_alg(len(lens) * int(lens.max()), self.hidden, self.e)
 
     def rows(self, lens):
+        if self.packed:
+            return self.heads * int(lens.sum()), int(lens.sum())
         S = int(lens.max())
         return len(lens) * self.heads * S, len(lens) * S
 
@@ -103,6 +117,13 @@ def make_workload(name: str, rank: int, world: int):
                 "global_batch": 4096, "heads": 12, "hidden": 768,
                 "l2": "inputs larger than L2", "parallelism": f"dp{world} (LPT batch shards)"}
         return wl, desc, "strong"
+    if name in ("c3p", "c5p"):
+        wl, desc, scaling = make_workload(name[:2], rank, world)
+        wl.packed = True
+        wl.name += "p"
+        desc["workload"] = desc["workload"].replace("padded to Smax", "packed") + \
+            " -- packed, padding-free layout (NEXT-1: tt_softmax_packed + LN on sum(L) tokens)"
+        return wl, desc, scaling
     raise SystemExit(f"unknown workload {name}")
 
 
@@ -213,13 +234,21 @@ def run_ours(args, rank, world, local_rank):
             sshape, lshape = wl.shapes(lens)
             bid = wl.batch_ids[bi] if hasattr(wl, "batch_ids") else bi
             seed = W.SEED + 10007 * bid + (7919 * rank if scaling == "weak" else 0)
-            x = W.scores(*sshape, wl.dtype, device=dev, seed=seed)
+            x = (W.scores(1, 1, 1, sshape[0], wl.dtype, device=dev, seed=seed) if wl.packed
+                 else W.scores(*sshape, wl.dtype, device=dev, seed=seed))
             d = W.ln_inputs(lshape[0], lshape[1], wl.dtype, device=dev, seed=seed + 1)
-            units.append(dict(lens=lens, scores=x, L=torch.as_tensor(lens).to(dev),
+            if wl.packed:
+                cu, blocks, total, _ = tt.packed_offsets(lens, wl.heads, device=dev)
+                x = x.reshape(-1)
+            else:
+                cu = blocks = total = None
+            units.append(dict(lens=lens, scores=x, L=torch.as_tensor(lens).to(dev), cu=cu,
+                              blocks=blocks, total=total, maxlen=int(lens.max()),
                               out=torch.empty_like(d["x"]), **d))
     stream.synchronize()
 
-    plan_sm = tt.softmax_plan(wl.dtype, *units[0]["scores"].shape)
+    plan_sm = (tt.softmax_packed_plan(wl.dtype, max(u["maxlen"] for u in units)) if wl.packed
+               else tt.softmax_plan(wl.dtype, *units[0]["scores"].shape))
     plan_ln = tt.layernorm_plan(wl.dtype, *units[0]["x"].shape)
     b_sm = sum(wl.bytes_softmax(u["lens"]) for u in units)
     b_ln = sum(wl.bytes_ln(u["lens"]) for u in units)
@@ -230,7 +259,11 @@ def run_ours(args, rank, world, local_rank):
         for u in units:
             if ev is not None:
                 ev[0].record(stream)
-            tt.tt_softmax_masked(u["scores"], u["L"], wl.scale, stream=stream)
+            if wl.packed:
+                tt.tt_softmax_packed(u["scores"], u["cu"], u["blocks"], wl.heads, u["total"],
+                                     u["maxlen"], wl.scale, stream=stream)
+            else:
+                tt.tt_softmax_masked(u["scores"], u["L"], wl.scale, stream=stream)
             if ev is not None:
                 ev[1].record(stream)
             tt.tt_add_bias_layernorm(u["out"], u["x"], u["residual"], u["bias"], u["gamma"],
@@ -279,7 +312,8 @@ def run_ours(args, rank, world, local_rank):
     tot_rows_sm, tot_rows_ln = (float(v) for v in tot_rows.tolist())
 
     # ---- end to end through the staged C-ABI call with pinned host buffers
-    e2e = run_e2e(args, tt, wl, units, stream, dist, dev, world) if args.e2e_steps > 0 else None
+    e2e = (run_e2e(args, tt, wl, units, stream, dist, dev, world)
+           if args.e2e_steps > 0 and not wl.packed else None)
 
     if rank != 0:
         if dist:
@@ -383,11 +417,19 @@ def _oracle_sample(wl, frac, seed=0):
     softmax rows and of the LN rows of each batch (same shapes/distributions)."""
     samples = []
     for bi, lens in enumerate(wl.batches):
-        (B, H, S, _), (R, hid) = wl.shapes(lens)
-        nrows_sm = max(1, int(round(B * H * S * frac)))
+        B, H, S = len(lens), wl.heads, int(lens.max())
+        R, hid = wl.shapes(lens)[1]
+        rng = np.random.Generator(np.random.PCG64(seed + bi))
+        if wl.packed:
+            # rows of the packed layout: request r contributes H*L_r rows of L_r keys
+            nrows_sm = max(1, int(round(H * int(lens.sum()) * frac)))
+            w = lens.astype(np.float64) / lens.sum()
+            rb = rng.choice(B, size=nrows_sm, p=w)
+        else:
+            nrows_sm = max(1, int(round(B * H * S * frac)))
+            # rows keep their request's length: pick the batch index of each sampled row
+            rb = rng.integers(0, B, size=nrows_sm)
         nrows_ln = max(1, int(round(R * frac)))
-        # rows keep their request's length: pick the batch index of each sampled row
-        rb = np.random.Generator(np.random.PCG64(seed + bi)).integers(0, B, size=nrows_sm)
         x = W.scores(nrows_sm, 1, 1, S, wl.dtype, seed=W.SEED + bi)
         d = W.ln_inputs(nrows_ln, hid, wl.dtype, seed=W.SEED + bi + 1)
         samples.append(dict(x=x.reshape(nrows_sm, S), lens=lens[rb], d=d, S=S, hid=hid,
@@ -424,7 +466,10 @@ def _oracle_run(samples, wl, cores):
     rows = 0
     for s in samples:
         L = np.clip(s["lens"].astype(np.int64), 0, s["S"])
-        nbytes += int(L.sum()) * wl.e + s["nrows_sm"] * s["S"] * wl.e
+        if wl.packed:
+            nbytes += 2 * int(L.sum()) * wl.e
+        else:
+            nbytes += int(L.sum()) * wl.e + s["nrows_sm"] * s["S"] * wl.e
         nbytes += W.ln_bytes_alg(s["nrows_ln"], s["hid"], wl.e)
         rows += s["nrows_sm"] + s["nrows_ln"]
     return dt, nbytes, rows
@@ -497,7 +542,7 @@ def main():
     ap.add_argument("--steps", type=int, default=1000)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--workload", choices=["c4", "c3", "c5"], default="c4")
+    ap.add_argument("--workload", choices=["c4", "c3", "c5", "c3p", "c5p"], default="c4")
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--kernel-events", type=int, default=1000000,
                     help="per-kernel CUDA events for the first N timed steps")
