@@ -29,7 +29,7 @@ cudaError_t layernorm_launch(int dtype, void* out, const void* x, const void* re
                              const void* bias, const void* gamma, const void* beta, int64_t rows,
                              int64_t hidden, float eps, int vec_bytes, cudaStream_t stream,
                              bool* supported);
-const char* layernorm_tier_name(int dtype, int64_t hidden, int vec_bytes);
+const char* layernorm_tier_name(int dtype, int64_t hidden, int vec_bytes, int64_t rows);
 
 // Tuning / test hooks (include/tt_tune.h): enumerate every compiled tier and
 // force one (-1 = automatic selection).  A forced tier that cannot serve the

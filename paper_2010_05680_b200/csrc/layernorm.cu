@@ -47,6 +47,16 @@ __global__ void __launch_bounds__(NT, MINB)
         live[r] = row < rows;
         off[r] = (live[r] ? row : 0) * (int64_t)hidden;
     }
+    // gamma / beta are needed only after the reductions: pull them into L1 now
+    // so that dependent load does not add an L2 round trip to the row's latency
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+        const int vi = q + k * G;
+        if (vi < nvec) {
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(gamma + vi * VE));
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(beta + vi * VE));
+        }
+    }
 
     // ---- LN-1: v = (x + bias) + residual
     float v[R][NV][VE];
@@ -761,6 +771,17 @@ struct Pref {
     int min_hidden, max_hidden;  // applies to min_hidden < hidden <= max_hidden
     const char* name;
 };
+// up to kSmallRows rows the problem is latency-bound: no per-CTA parameter
+// staging, one row per group, gamma / beta prefetched to L1 (ln_rows tiers)
+constexpr int64_t kSmallRows = 4096;
+const Pref kLnPrefSmall[] = {
+    {0, 512, 768, "ln_rows<f32,V32,G32,NV3,R1,T256,M1>"},
+    {0, 768, 1024, "ln_rows<f32,V32,G32,NV4,R1,T256,M1>"},
+    {1, 512, 768, "ln_rows<f16,V16,G32,NV3,R1,T256,M1>"},
+    {1, 768, 1024, "ln_rows<f16,V32,G32,NV2,R1,T256,M1>"},
+    {2, 512, 768, "ln_rows<bf16,V16,G32,NV3,R1,T256,M1>"},
+    {2, 768, 1024, "ln_rows<bf16,V32,G32,NV2,R1,T256,M1>"},
+};
 const Pref kLnPref[] = {
     {0, 512, 768, "ln_rows<f32,V32,G32,NV3,R1,T256,M1>"},
     {0, 768, 1024, "ln_rows<f32,V32,G32,NV4,R1,T256,M1>"},
@@ -776,30 +797,34 @@ const LnTier* by_name(const LnTier* tab, const char* name) {
     return nullptr;
 }
 
-const LnTier* pick_dtype(int dtype, int64_t hidden, int vec_bytes) {
+template <size_t N>
+const LnTier* from_prefs(const Pref (&prefs)[N], int dtype, int64_t hidden, int vec_bytes) {
+    // the preference whose (min_hidden, max_hidden] holds this row
+    // name -> tier resolved once per entry (benign race: every thread stores
+    // the same index)
+    static std::atomic<int> idx[N];
+    for (size_t i = 0; i < N; ++i) {
+        const Pref& pr = prefs[i];
+        if (pr.dtype != dtype || hidden <= pr.min_hidden || hidden > pr.max_hidden) continue;
+        int k = idx[i].load(std::memory_order_relaxed);
+        if (k == 0) {
+            const LnTier* found = by_name(table(dtype), pr.name);
+            k = found ? (int)(found - table(dtype)) + 1 : -1;
+            idx[i].store(k, std::memory_order_relaxed);
+        }
+        const LnTier* t = k > 0 ? table(dtype) + (k - 1) : nullptr;
+        if (t && fits(*t, hidden, vec_bytes)) return t;
+    }
+    return nullptr;
+}
+
+const LnTier* pick_dtype(int dtype, int64_t hidden, int vec_bytes, int64_t rows) {
     const LnTier* tab = table(dtype);
     if (!tab) return nullptr;
     const int f = g_force[dtype].load(std::memory_order_relaxed);
     if (f >= 0 && f < kLnN && fits(tab[f], hidden, vec_bytes)) return &tab[f];
-    // preferred tiers: the one whose (min_hidden, max_hidden] holds this row
-    static const LnTier* pref_tier[sizeof(kLnPref) / sizeof(kLnPref[0])] = {};
-    static std::atomic<bool> pref_init{false};
-    if (!pref_init.load(std::memory_order_acquire)) {
-        for (size_t i = 0; i < sizeof(kLnPref) / sizeof(kLnPref[0]); ++i)
-            pref_tier[i] = by_name(table(kLnPref[i].dtype), kLnPref[i].name);
-        pref_init.store(true, std::memory_order_release);
-    }
-    const LnTier* pbest = nullptr;
-    int pmax = 1 << 30;
-    for (size_t i = 0; i < sizeof(kLnPref) / sizeof(kLnPref[0]); ++i) {
-        const LnTier* t = pref_tier[i];
-        if (kLnPref[i].dtype == dtype && t && hidden <= kLnPref[i].max_hidden &&
-            hidden > kLnPref[i].min_hidden &&
-            kLnPref[i].max_hidden < pmax && fits(*t, hidden, vec_bytes)) {
-            pbest = t;
-            pmax = kLnPref[i].max_hidden;
-        }
-    }
+    const LnTier* pbest = rows <= kSmallRows ? from_prefs(kLnPrefSmall, dtype, hidden, vec_bytes)
+                                             : from_prefs(kLnPref, dtype, hidden, vec_bytes);
     if (pbest) return pbest;
     const LnTier* best = nullptr;
     for (int i = 0; i < kLnN; ++i) {
@@ -828,8 +853,8 @@ bool layernorm_force_tier(int dtype, int i) {
     return true;
 }
 
-const char* layernorm_tier_name(int dtype, int64_t hidden, int vec_bytes) {
-    const LnTier* t = pick_dtype(dtype, hidden, vec_bytes);
+const char* layernorm_tier_name(int dtype, int64_t hidden, int vec_bytes, int64_t rows) {
+    const LnTier* t = pick_dtype(dtype, hidden, vec_bytes, rows);
     return t ? t->name : nullptr;
 }
 
@@ -837,7 +862,7 @@ cudaError_t layernorm_launch(int dtype, void* out, const void* x, const void* re
                              const void* bias, const void* gamma, const void* beta, int64_t rows,
                              int64_t hidden, float eps, int vec_bytes, cudaStream_t stream,
                              bool* supported) {
-    const LnTier* t = pick_dtype(dtype, hidden, vec_bytes);
+    const LnTier* t = pick_dtype(dtype, hidden, vec_bytes, rows);
     *supported = t != nullptr;
     if (!t) return cudaSuccess;
     return t->fn(out, x, residual, bias, gamma, beta, rows, (int)hidden, eps, stream);

@@ -513,6 +513,13 @@ cudaError_t launch_softmax_warp(void* scores, const int32_t* lengths, int64_t nr
         }
         const int64_t slots = (int64_t)sm_count() * occ * GPB;
         rpg = (int)((nrows + slots - 1) / slots);
+    } else {
+        // small problems are latency-bound: give every group a single row
+        // rather than a few CTAs walking RPG rows each (at least 2 CTAs of
+        // work per SM before rows are chained)
+        const int64_t spread = (int64_t)sm_count() * 2 * GPB;
+        const int64_t need = (nrows + spread - 1) / spread;
+        if (need < rpg) rpg = need > 0 ? (int)need : 1;
     }
     const int64_t per_cta = (int64_t)GPB * rpg;
     const int64_t grid = (nrows + per_cta - 1) / per_cta;

@@ -319,7 +319,7 @@ tt_status tt_add_bias_layernorm_plan(int dtype, int64_t rows, int64_t hidden, ch
             vb = c;
             break;
         }
-    copy_name(tt::layernorm_tier_name(dtype, hidden, vb), buf, cap);
+    copy_name(tt::layernorm_tier_name(dtype, hidden, vb, rows), buf, cap);
     return TT_SUCCESS;
 }
 

@@ -130,16 +130,19 @@ def test_softmax_tier_plan(ttlib, dtype, Sk, tier):
     assert ttlib.softmax_plan(dtype, 2, 12, 3, Sk) == tier
 
 
-@pytest.mark.parametrize("dtype,hidden,tier", [
-    (torch.float32, 768, "ln_rows<f32,V32,G32,NV3,R1,T256,M1>"),
-    (torch.float16, 768, "ln_warp<f16,V16,G32,NV4,T256,M2,PF1>"),
-    (torch.bfloat16, 1024, "ln_warp<bf16,V16,G32,NV4,T256,M2,PF1>"),
-    (torch.float32, 37, "ln_rows<f32,V4,G32,NV4,R1,T256,M1>"),
-    (torch.float16, 16, "ln_warp<f16,V16,G4,NV1,T256,M4,PF0>"),
-    (torch.float32, 4096, "ln_rows<f32,V32,G128,NV4,R1,T128,M1>"),
+@pytest.mark.parametrize("dtype,rows,hidden,tier", [
+    (torch.float32, 10, 768, "ln_rows<f32,V32,G32,NV3,R1,T256,M1>"),
+    (torch.float32, 30000, 768, "ln_rows<f32,V32,G32,NV3,R1,T256,M1>"),
+    (torch.float16, 10, 768, "ln_rows<f16,V16,G32,NV3,R1,T256,M1>"),
+    (torch.float16, 30000, 768, "ln_warp<f16,V16,G32,NV4,T256,M2,PF1>"),
+    (torch.bfloat16, 10, 1024, "ln_rows<bf16,V32,G32,NV2,R1,T256,M1>"),
+    (torch.bfloat16, 32768, 1024, "ln_warp<bf16,V16,G32,NV4,T256,M2,PF1>"),
+    (torch.float32, 10, 37, "ln_rows<f32,V4,G32,NV4,R1,T256,M1>"),
+    (torch.float16, 10, 16, "ln_warp<f16,V16,G4,NV1,T256,M4,PF0>"),
+    (torch.float32, 10, 4096, "ln_rows<f32,V32,G128,NV4,R1,T128,M1>"),
 ])
-def test_layernorm_tier_plan(ttlib, dtype, hidden, tier):
-    assert ttlib.layernorm_plan(dtype, 10, hidden) == tier
+def test_layernorm_tier_plan(ttlib, dtype, rows, hidden, tier):
+    assert ttlib.layernorm_plan(dtype, rows, hidden) == tier
 
 
 def test_tier_enumeration_and_force(ttlib):

@@ -1,0 +1,123 @@
+#!/usr/bin/env python
+"""Sweep BASELINE.json's configurations through both operations; one JSON line
+per (config, op, dtype, lengths) with time per call, algorithmic GB/s, % of
+the measured copy peak and the same-traffic torch reference, plus an
+empty-kernel launch floor for the launch-bound small shapes.
+
+  python tools/sweep.py > gpurun_out/sweep.jsonl
+"""
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import paper_2010_05680_b200 as tt  # noqa: E402
+import workloads as W  # noqa: E402
+
+L2 = 126 * 1024 * 1024
+
+
+def peak():
+    try:
+        return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
+    except Exception:
+        return 6650.0
+
+
+def timeit(fn, nbufs, reps):
+    """Device time per call: the calls are captured once into a CUDA graph and
+    the graph is replayed, so host-side launch overhead (Python + ctypes) does
+    not leak into small shapes; CUDA events on the replay stream."""
+    st = torch.cuda.Stream()
+    with torch.cuda.stream(st):
+        for i in range(3):
+            fn(i % nbufs)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=st):
+        for i in range(reps):
+            fn(i % nbufs)
+    with torch.cuda.stream(st):
+        g.replay()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(st):
+        a.record(st)
+        g.replay()
+        b.record(st)
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / reps * 1e3  # us
+
+
+def nbufs_for(nbytes):
+    return int(max(1, min(64, -(-4 * L2 // max(nbytes, 1)))))
+
+
+def softmax_case(cfg, dtype, B, H, S, lens, pk):
+    e = W.ELEM_BYTES[dtype]
+    nbytes = B * H * S * S * e
+    nb = nbufs_for(nbytes)
+    bufs = [W.scores(B, H, S, S, dtype, device="cuda", seed=i) for i in range(nb)]
+    L = torch.as_tensor(np.asarray(lens, dtype=np.int32)).cuda()
+    reps = 200 if nbytes < 64 << 20 else 50
+    us = timeit(lambda i: tt.tt_softmax_masked(bufs[i], L, 0.125), nb, reps)
+    other = [torch.empty_like(b) for b in bufs]
+    us_copy = timeit(lambda i: other[i].copy_(bufs[i]), nb, reps)
+    alg = W.softmax_bytes_alg(lens, H, S, S, e)
+    return dict(config=cfg, op="softmax", dtype=W.DTYPE_NAMES[dtype], shape=[B, H, S, S],
+                ragged=bool(np.any(np.asarray(lens) < S)), us=round(us, 2),
+                GBps=round(alg / us / 1e3, 1), pct_peak=round(100 * alg / us / 1e3 / pk, 1),
+                copy_same_bytes_us=round(us_copy * alg / (2 * nbytes), 2),
+                tier=tt.softmax_plan(dtype, B, H, S, S))
+
+
+def ln_case(cfg, dtype, rows, hidden, pk):
+    e = W.ELEM_BYTES[dtype]
+    nbytes = 3 * rows * hidden * e
+    nb = nbufs_for(nbytes)
+    ds = [W.ln_inputs(rows, hidden, dtype, device="cuda", seed=i) for i in range(nb)]
+    outs = [torch.empty_like(d["x"]) for d in ds]
+    reps = 200 if nbytes < 64 << 20 else 50
+    us = timeit(lambda i: tt.tt_add_bias_layernorm(outs[i], ds[i]["x"], ds[i]["residual"],
+                                                   ds[i]["bias"], ds[i]["gamma"], ds[i]["beta"],
+                                                   1e-12), nb, reps)
+    us_add = timeit(lambda i: torch.add(ds[i]["x"], ds[i]["residual"], out=outs[i]), nb, reps)
+    alg = W.ln_bytes_alg(rows, hidden, e)
+    return dict(config=cfg, op="layernorm", dtype=W.DTYPE_NAMES[dtype], shape=[rows, hidden],
+                ragged=False, us=round(us, 2), GBps=round(alg / us / 1e3, 1),
+                pct_peak=round(100 * alg / us / 1e3 / pk, 1), torch_add_same_traffic_us=round(us_add, 2),
+                tier=tt.layernorm_plan(dtype, rows, hidden))
+
+
+def main():
+    pk = peak()
+    # per-kernel floor inside a graph: torch's smallest kernel (1-element add)
+    z = torch.zeros(1, device="cuda")
+    floor = timeit(lambda i: z.add_(0), 1, 500)
+    print(json.dumps({"launch_floor_us": round(floor, 2), "peak_GBps": pk}), flush=True)
+    out = []
+    out.append(softmax_case("C1", torch.float32, 1, 12, 40, [40], pk))
+    out.append(ln_case("C1", torch.float32, 40, 768, pk))
+    for dtype in (torch.float16, torch.float32):
+        for S in W.C2.extra["seqs"]:
+            out.append(softmax_case("C2", dtype, 20, 12, S, W.lengths_full(20, S), pk))
+            out.append(softmax_case("C2", dtype, 20, 12, S, W.lengths_ragged(20, S), pk))
+            out.append(ln_case("C2", dtype, 20 * S, 768, pk))
+    for dtype in (torch.float16, torch.float32):
+        lens = W.c3_lengths()
+        S = int(lens.max())
+        out.append(softmax_case("C3", dtype, 64, 12, S, lens, pk))
+        out.append(ln_case("C3", dtype, 64 * S, 768, pk))
+    out.append(softmax_case("C4", torch.bfloat16, 64, 16, 512, W.lengths_full(64, 512), pk))
+    out.append(softmax_case("C4", torch.bfloat16, 64, 16, 512, W.lengths_ragged(64, 512, 4), pk))
+    out.append(ln_case("C4", torch.bfloat16, 32768, 1024, pk))
+    for r in out:
+        print(json.dumps(r), flush=True)
+
+
+if __name__ == "__main__":
+    main()
