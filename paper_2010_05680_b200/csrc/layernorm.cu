@@ -47,17 +47,6 @@ __global__ void __launch_bounds__(NT, MINB)
         live[r] = row < rows;
         off[r] = (live[r] ? row : 0) * (int64_t)hidden;
     }
-    // gamma / beta are needed only after the reductions: pull them into L1 now
-    // so that dependent load does not add an L2 round trip to the row's latency
-#pragma unroll
-    for (int k = 0; k < NV; ++k) {
-        const int vi = q + k * G;
-        if (vi < nvec) {
-            asm volatile("prefetch.global.L1 [%0];" ::"l"(gamma + vi * VE));
-            asm volatile("prefetch.global.L1 [%0];" ::"l"(beta + vi * VE));
-        }
-    }
-
     // ---- LN-1: v = (x + bias) + residual
     float v[R][NV][VE];
 #pragma unroll
@@ -798,11 +787,9 @@ const LnTier* by_name(const LnTier* tab, const char* name) {
 }
 
 template <size_t N>
-const LnTier* from_prefs(const Pref (&prefs)[N], int dtype, int64_t hidden, int vec_bytes) {
+const LnTier* from_prefs(const Pref (&prefs)[N], std::atomic<int> (&idx)[N], int dtype,
+                         int64_t hidden, int vec_bytes) {
     // the preference whose (min_hidden, max_hidden] holds this row
-    // name -> tier resolved once per entry (benign race: every thread stores
-    // the same index)
-    static std::atomic<int> idx[N];
     for (size_t i = 0; i < N; ++i) {
         const Pref& pr = prefs[i];
         if (pr.dtype != dtype || hidden <= pr.min_hidden || hidden > pr.max_hidden) continue;
@@ -823,8 +810,13 @@ const LnTier* pick_dtype(int dtype, int64_t hidden, int vec_bytes, int64_t rows)
     if (!tab) return nullptr;
     const int f = g_force[dtype].load(std::memory_order_relaxed);
     if (f >= 0 && f < kLnN && fits(tab[f], hidden, vec_bytes)) return &tab[f];
-    const LnTier* pbest = rows <= kSmallRows ? from_prefs(kLnPrefSmall, dtype, hidden, vec_bytes)
-                                             : from_prefs(kLnPref, dtype, hidden, vec_bytes);
+    // name -> tier index caches, one per preference table (benign race: every
+    // thread stores the same index)
+    static std::atomic<int> idx_small[sizeof(kLnPrefSmall) / sizeof(Pref)];
+    static std::atomic<int> idx_large[sizeof(kLnPref) / sizeof(Pref)];
+    const LnTier* pbest = rows <= kSmallRows
+                              ? from_prefs(kLnPrefSmall, idx_small, dtype, hidden, vec_bytes)
+                              : from_prefs(kLnPref, idx_large, dtype, hidden, vec_bytes);
     if (pbest) return pbest;
     const LnTier* best = nullptr;
     for (int i = 0; i < kLnN; ++i) {
