@@ -22,7 +22,10 @@
 
 namespace tt {
 
-template <typename T, int VB, int G, int NV, int R, int NT, int MINB>
+// EARLY: gamma / beta are loaded into registers together with the row (for
+// small, latency-bound problems: no dependent parameter load after the
+// reductions); otherwise they are loaded (L1-cached) after them.
+template <typename T, int VB, int G, int NV, int R, int NT, int MINB, bool EARLY = false>
 __global__ void __launch_bounds__(NT, MINB)
     ln_rows_kernel(T* out, const T* x, const T* residual, const T* __restrict__ bias,
                    const T* __restrict__ gamma, const T* __restrict__ beta, int64_t rows,
@@ -46,6 +49,17 @@ __global__ void __launch_bounds__(NT, MINB)
         const int64_t row = base + (int64_t)r * GPB + gi;
         live[r] = row < rows;
         off[r] = (live[r] ? row : 0) * (int64_t)hidden;
+    }
+    Raw<VB> eg[EARLY ? NV : 1], eb[EARLY ? NV : 1];
+    if constexpr (EARLY) {
+#pragma unroll
+        for (int k = 0; k < NV; ++k) {
+            const int vi = q + k * G;
+            if (vi < nvec) {
+                ld_param<VB>(gamma + vi * VE, eg[k]);
+                ld_param<VB>(beta + vi * VE, eb[k]);
+            }
+        }
     }
     // ---- LN-1: v = (x + bias) + residual
     float v[R][NV][VE];
@@ -129,8 +143,13 @@ __global__ void __launch_bounds__(NT, MINB)
             const int vi = q + k * G;
             if (vi < nvec) {
                 Raw<VB> wg, wb;
-                ld_param<VB>(gamma + vi * VE, wg);
-                ld_param<VB>(beta + vi * VE, wb);
+                if constexpr (EARLY) {
+                    wg = eg[k];
+                    wb = eb[k];
+                } else {
+                    ld_param<VB>(gamma + vi * VE, wg);
+                    ld_param<VB>(beta + vi * VE, wb);
+                }
                 float fg[VE], fb[VE], y[VE];
                 Elem<T>::template unpack<VB>(wg, fg);
                 Elem<T>::template unpack<VB>(wb, fb);
@@ -605,7 +624,7 @@ cudaError_t launch_ln_tma(void* out, const void* x, const void* res, const void*
 
 namespace {
 
-template <typename T, int VB, int G, int NV, int R, int NT, int MINB>
+template <typename T, int VB, int G, int NV, int R, int NT, int MINB, bool EARLY = false>
 cudaError_t launch_ln(void* out, const void* x, const void* res, const void* bias,
                       const void* gamma, const void* beta, int64_t rows, int hidden, float eps,
                       cudaStream_t st) {
@@ -613,7 +632,7 @@ cudaError_t launch_ln(void* out, const void* x, const void* res, const void* bia
     const int64_t rows_per_cta = (int64_t)GPB * R;
     const int64_t grid = (rows + rows_per_cta - 1) / rows_per_cta;
     if (grid > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
-    ln_rows_kernel<T, VB, G, NV, R, NT, MINB><<<(unsigned)grid, NT, 0, st>>>(
+    ln_rows_kernel<T, VB, G, NV, R, NT, MINB, EARLY><<<(unsigned)grid, NT, 0, st>>>(
         static_cast<T*>(out), static_cast<const T*>(x), static_cast<const T*>(res),
         static_cast<const T*>(bias), static_cast<const T*>(gamma), static_cast<const T*>(beta),
         rows, hidden, eps);
@@ -670,6 +689,12 @@ struct LnTier {
         VB, (VB) / (int)sizeof(T), (G) * (NV) * ((VB) / (int)sizeof(T)), AUTO,             \
             &launch_ln<T, VB, G, NV, R, NT, MINB>,                                         \
             "ln_rows<" TN ",V" #VB ",G" #G ",NV" #NV ",R" #R ",T" #NT ",M" #MINB ">"      \
+    }
+#define TT_LN_EARLY(AUTO, T, TN, VB, G, NV, NT)                                            \
+    LnTier {                                                                               \
+        VB, (VB) / (int)sizeof(T), (G) * (NV) * ((VB) / (int)sizeof(T)), AUTO,             \
+            &launch_ln<T, VB, G, NV, 1, NT, 1, true>,                                      \
+            "ln_rows<" TN ",V" #VB ",G" #G ",NV" #NV ",R1,T" #NT ",M1,E>"                 \
     }
 
 #define TT_LN_WARP_P(AUTO, T, TN, VB, G, NV, NT, MINB, PF)                                 \
@@ -728,7 +753,10 @@ struct LnTier {
     TT_LN_WARP_P(false, T, TN, 32, 32, 2, 128, 6, 1), TT_LN_WARP_P(false, T, TN, 16, 32, 3, 256, 3, 1), \
     TT_LN_WARP_P(false, T, TN, 16, 32, 3, 256, 2, 1), TT_LN_WARP_P(false, T, TN, 32, 32, 3, 256, 2, 1), \
     TT_LN_WARP_P(false, T, TN, 32, 32, 3, 128, 4, 1), TT_LN_WARP_P(false, T, TN, 16, 32, 4, 256, 2, 1), \
-    TT_LN_WARP_P(false, T, TN, 32, 32, 1, 256, 4, 1), TT_LN_WARP_P(false, T, TN, 32, 32, 4, 256, 2, 1)
+    TT_LN_WARP_P(false, T, TN, 32, 32, 1, 256, 4, 1), TT_LN_WARP_P(false, T, TN, 32, 32, 4, 256, 2, 1), \
+    TT_LN_EARLY(false, T, TN, 16, 32, 3, 256), TT_LN_EARLY(false, T, TN, 32, 32, 2, 256),        \
+    TT_LN_EARLY(false, T, TN, 32, 32, 3, 256), TT_LN_EARLY(false, T, TN, 32, 32, 4, 256),        \
+    TT_LN_EARLY(false, T, TN, 16, 32, 3, 128), TT_LN_EARLY(false, T, TN, 32, 32, 2, 128)
 
 // MA / MB / MC: min CTAs/SM (register cap) for warp tiers holding about
 // 16 / 24-32 / 48-64 fp32 row values per lane.
@@ -761,15 +789,16 @@ struct Pref {
     const char* name;
 };
 // up to kSmallRows rows the problem is latency-bound: no per-CTA parameter
-// staging, one row per group, gamma / beta prefetched to L1 (ln_rows tiers)
-constexpr int64_t kSmallRows = 4096;
+// staging, one row per group, gamma / beta loaded together with the row
+// (ln_rows EARLY tiers), so no dependent load follows the reductions
+constexpr int64_t kSmallRows = 8192;
 const Pref kLnPrefSmall[] = {
-    {0, 512, 768, "ln_rows<f32,V32,G32,NV3,R1,T256,M1>"},
-    {0, 768, 1024, "ln_rows<f32,V32,G32,NV4,R1,T256,M1>"},
-    {1, 512, 768, "ln_rows<f16,V16,G32,NV3,R1,T256,M1>"},
-    {1, 768, 1024, "ln_rows<f16,V32,G32,NV2,R1,T256,M1>"},
-    {2, 512, 768, "ln_rows<bf16,V16,G32,NV3,R1,T256,M1>"},
-    {2, 768, 1024, "ln_rows<bf16,V32,G32,NV2,R1,T256,M1>"},
+    {0, 512, 768, "ln_rows<f32,V32,G32,NV3,R1,T256,M1,E>"},
+    {0, 768, 1024, "ln_rows<f32,V32,G32,NV4,R1,T256,M1,E>"},
+    {1, 512, 768, "ln_rows<f16,V16,G32,NV3,R1,T256,M1,E>"},
+    {1, 768, 1024, "ln_rows<f16,V32,G32,NV2,R1,T256,M1,E>"},
+    {2, 512, 768, "ln_rows<bf16,V16,G32,NV3,R1,T256,M1,E>"},
+    {2, 768, 1024, "ln_rows<bf16,V32,G32,NV2,R1,T256,M1,E>"},
 };
 const Pref kLnPref[] = {
     {0, 512, 768, "ln_rows<f32,V32,G32,NV3,R1,T256,M1>"},
