@@ -791,8 +791,17 @@ struct Pref {
 // up to kSmallRows rows the problem is latency-bound: no per-CTA parameter
 // staging, one row per group, gamma / beta loaded together with the row
 // (ln_rows EARLY tiers), so no dependent load follows the reductions
-constexpr int64_t kSmallRows = 8192;
+// (EARLY costs registers, so only for the tiniest problems)
+constexpr int64_t kTinyRows = 2048, kSmallRows = 8192;
 const Pref kLnPrefSmall[] = {
+    {0, 512, 768, "ln_rows<f32,V32,G32,NV3,R1,T256,M1>"},
+    {0, 768, 1024, "ln_rows<f32,V32,G32,NV4,R1,T256,M1>"},
+    {1, 512, 768, "ln_rows<f16,V16,G32,NV3,R1,T256,M1>"},
+    {1, 768, 1024, "ln_rows<f16,V32,G32,NV2,R1,T256,M1>"},
+    {2, 512, 768, "ln_rows<bf16,V16,G32,NV3,R1,T256,M1>"},
+    {2, 768, 1024, "ln_rows<bf16,V32,G32,NV2,R1,T256,M1>"},
+};
+const Pref kLnPrefTiny[] = {
     {0, 512, 768, "ln_rows<f32,V32,G32,NV3,R1,T256,M1,E>"},
     {0, 768, 1024, "ln_rows<f32,V32,G32,NV4,R1,T256,M1,E>"},
     {1, 512, 768, "ln_rows<f16,V16,G32,NV3,R1,T256,M1,E>"},
@@ -841,11 +850,13 @@ const LnTier* pick_dtype(int dtype, int64_t hidden, int vec_bytes, int64_t rows)
     if (f >= 0 && f < kLnN && fits(tab[f], hidden, vec_bytes)) return &tab[f];
     // name -> tier index caches, one per preference table (benign race: every
     // thread stores the same index)
+    static std::atomic<int> idx_tiny[sizeof(kLnPrefTiny) / sizeof(Pref)];
     static std::atomic<int> idx_small[sizeof(kLnPrefSmall) / sizeof(Pref)];
     static std::atomic<int> idx_large[sizeof(kLnPref) / sizeof(Pref)];
-    const LnTier* pbest = rows <= kSmallRows
-                              ? from_prefs(kLnPrefSmall, idx_small, dtype, hidden, vec_bytes)
-                              : from_prefs(kLnPref, idx_large, dtype, hidden, vec_bytes);
+    const LnTier* pbest =
+        rows <= kTinyRows    ? from_prefs(kLnPrefTiny, idx_tiny, dtype, hidden, vec_bytes)
+        : rows <= kSmallRows ? from_prefs(kLnPrefSmall, idx_small, dtype, hidden, vec_bytes)
+                             : from_prefs(kLnPref, idx_large, dtype, hidden, vec_bytes);
     if (pbest) return pbest;
     const LnTier* best = nullptr;
     for (int i = 0; i < kLnN; ++i) {
