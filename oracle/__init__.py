@@ -58,8 +58,14 @@ def _load():
                                                    _i64, ctypes.c_float, _vp]
             lib.tto_layernorm_onepass_eq1.argtypes = [_vp, _vp, _vp, ctypes.c_int, _i64, _i64,
                                                       ctypes.c_float, _vp]
+            lib.tto_add_bias_gelu.argtypes = [_vp, _vp, ctypes.c_int, _i64, _i64, ctypes.c_int,
+                                              _vp]
+            lib.tto_split_qkv_add_bias.argtypes = [_vp, _vp, ctypes.c_int, _i64, _i64, _i64,
+                                                   _i64, _vp]
+            lib.tto_merge_heads.argtypes = [_vp, ctypes.c_int, _i64, _i64, _i64, _i64, _vp]
             for f in (lib.tto_widen, lib.tto_softmax_masked, lib.tto_add_bias_layernorm,
-                      lib.tto_layernorm_onepass_eq1):
+                      lib.tto_layernorm_onepass_eq1, lib.tto_add_bias_gelu,
+                      lib.tto_split_qkv_add_bias, lib.tto_merge_heads):
                 f.restype = ctypes.c_int
             _lib = lib
     return _lib
@@ -157,4 +163,44 @@ def softmax_packed(flat: torch.Tensor, lengths, H: int, scale: float) -> torch.T
         off += n
     if off != src.numel():
         raise ValueError("flat size does not match the lengths")
+    return out
+
+
+# ---------------------------------------------------------------- NEXT-2 ops
+def add_bias_gelu(x, bias, approximate: bool = False) -> torch.Tensor:
+    """gelu(x + bias) over the last dim, float64 (exact erf form, or tanh form)."""
+    xs, bs = _host(x), _host(bias)
+    if xs.dtype != bs.dtype:
+        raise TypeError("x and bias share one dtype")
+    n = xs.shape[-1]
+    rows = xs.numel() // n if n else 0
+    if bs.numel() != n:
+        raise ValueError("bias must have n elements")
+    out = torch.empty(xs.shape, dtype=torch.float64)
+    rc = _load().tto_add_bias_gelu(_ptr(xs), _ptr(bs), DTYPE_CODE[xs.dtype], rows, n,
+                                   int(bool(approximate)), _ptr(out))
+    assert rc == 0
+    return out
+
+
+def split_qkv_add_bias(qkv, bias, B: int, S: int, H: int, D: int):
+    """qkv [B*S, 3*H*D] + bias [3*H*D] -> (q, k, v), each float64 [B, H, S, D]."""
+    qs, bs = _host(qkv), _host(bias)
+    if qs.numel() != B * S * 3 * H * D or bs.numel() != 3 * H * D:
+        raise ValueError("shape mismatch")
+    out = torch.empty((3, B, H, S, D), dtype=torch.float64)
+    rc = _load().tto_split_qkv_add_bias(_ptr(qs), _ptr(bs), DTYPE_CODE[qs.dtype], B, S, H, D,
+                                        _ptr(out))
+    assert rc == 0
+    return out[0], out[1], out[2]
+
+
+def merge_heads(x, B: int, S: int, H: int, D: int) -> torch.Tensor:
+    """[B, H, S, D] -> [B*S, H*D] float64 (exact)."""
+    xs = _host(x)
+    if xs.numel() != B * H * S * D:
+        raise ValueError("shape mismatch")
+    out = torch.empty((B * S, H * D), dtype=torch.float64)
+    rc = _load().tto_merge_heads(_ptr(xs), DTYPE_CODE[xs.dtype], B, S, H, D, _ptr(out))
+    assert rc == 0
     return out

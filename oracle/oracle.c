@@ -210,3 +210,75 @@ int tto_layernorm_onepass_eq1(const void* x, const void* gamma, const void* beta
     }
     return 0;
 }
+
+/* ---------------------------------------------------------------------------
+ * NEXT-2: the element-wise non-GEMM kernels of the fused graph,
+ * "fused activation functions and fused transpose operations" (PAPER.md
+ * l.304-308; K4/K5 in SURVEY §2.2).
+ * ------------------------------------------------------------------------- */
+
+/* out[r, j] = gelu(x[r, j] + bias[j]) over [rows, n], double.
+ * approximate = 0: exact GELU, v * Phi(v) = 0.5 v (1 + erf(v / sqrt 2))
+ * approximate = 1: tanh form, 0.5 v (1 + tanh(sqrt(2/pi) (v + 0.044715 v^3)))
+ * (BERT's definition is the exact form; the tanh form is PyTorch's
+ * approximate='tanh'.  DESIGN R17.) */
+int tto_add_bias_gelu(const void* x, const void* bias, int dtype, int64_t rows, int64_t n,
+                      int approximate, double* out) {
+    if (rows < 0 || n < 0 || dtype < 0 || dtype > 2 || approximate < 0 || approximate > 1)
+        return -1;
+    if (rows * n == 0) return 0;
+    if (!x || !bias || !out) return -1;
+    const double k = sqrt(2.0 / 3.14159265358979323846);
+    for (int64_t r = 0; r < rows; ++r) {
+        for (int64_t j = 0; j < n; ++j) {
+            const double v = load_elem(x, dtype, r * n + j) + load_elem(bias, dtype, j);
+            double y;
+            if (approximate)
+                y = 0.5 * v * (1.0 + tanh(k * (v + 0.044715 * v * v * v)));
+            else
+                y = 0.5 * v * (1.0 + erf(v / sqrt(2.0)));
+            out[r * n + j] = y;
+        }
+    }
+    return 0;
+}
+
+/* QKV split with bias (the "add bias + transpose" after the QKV GEMM):
+ * qkv [B*S, 3, H, D] (token-major, the GEMM's output row layout), bias [3, H, D]
+ * -> q, k, v, each [B, H, S, D]:
+ *   out_t[b, h, s, d] = qkv[(b*S + s), t, h, d] + bias[t, h, d],  t = 0, 1, 2
+ * out is double [3, B, H, S, D] (q block, then k, then v). */
+int tto_split_qkv_add_bias(const void* qkv, const void* bias, int dtype, int64_t B, int64_t S,
+                           int64_t H, int64_t D, double* out) {
+    if (B < 0 || S < 0 || H < 0 || D < 0 || dtype < 0 || dtype > 2) return -1;
+    if (B * S * H * D == 0) return 0;
+    if (!qkv || !bias || !out) return -1;
+    const int64_t per = B * H * S * D;
+    for (int64_t t = 0; t < 3; ++t)
+        for (int64_t b = 0; b < B; ++b)
+            for (int64_t h = 0; h < H; ++h)
+                for (int64_t s = 0; s < S; ++s)
+                    for (int64_t d = 0; d < D; ++d) {
+                        const int64_t src = (((b * S + s) * 3 + t) * H + h) * D + d;
+                        const int64_t dst = t * per + ((b * H + h) * S + s) * D + d;
+                        out[dst] = load_elem(qkv, dtype, src) +
+                                   load_elem(bias, dtype, (t * H + h) * D + d);
+                    }
+    return 0;
+}
+
+/* Head merge (the transpose after P.V): in [B, H, S, D] -> out [B*S, H*D]:
+ *   out[(b*S + s), h*D + d] = in[b, h, s, d]      (double; exact copy) */
+int tto_merge_heads(const void* in, int dtype, int64_t B, int64_t S, int64_t H, int64_t D,
+                    double* out) {
+    if (B < 0 || S < 0 || H < 0 || D < 0 || dtype < 0 || dtype > 2) return -1;
+    if (B * S * H * D == 0) return 0;
+    if (!in || !out) return -1;
+    for (int64_t b = 0; b < B; ++b)
+        for (int64_t s = 0; s < S; ++s)
+            for (int64_t h = 0; h < H; ++h)
+                for (int64_t d = 0; d < D; ++d)
+                    out[((b * S + s) * H + h) * D + d] =
+                        load_elem(in, dtype, ((b * H + h) * S + s) * D + d);
+    return 0;
+}
