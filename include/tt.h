@@ -151,6 +151,33 @@ TT_API tt_status tt_add_bias_layernorm_bf16(void* out, const void* x, const void
                                      int64_t rows, int64_t hidden, float eps, cudaStream_t stream);
 
 /* ------------------------------------------------------------------------
+ * NEXT-2: the element-wise kernels of the fused graph,
+ * "fused activation functions and fused transpose operations" (PAPER.md
+ * l.304-308).  dtype: 0 = fp32, 1 = fp16, 2 = bf16; fp32 arithmetic.  Same
+ * conventions and error codes as above; vectorised when every base pointer
+ * and row pitch is 16-byte aligned (element-wise otherwise).
+ *
+ * tt_add_bias_gelu:  out[r, j] = gelu(x[r, j] + bias[j]) over [rows, n];
+ *   approximate = 0: exact 0.5 v (1 + erf(v / sqrt 2)) (BERT's definition);
+ *   approximate = 1: 0.5 v (1 + tanh(sqrt(2/pi) (v + 0.044715 v^3))).
+ *   out may alias x exactly; bias must not overlap out.
+ * tt_split_qkv_add_bias:  qkv [B*S, 3*H*D] (token-major QKV GEMM output,
+ *   parts ordered q, k, v, then heads) + bias [3*H*D] ->
+ *   q, k, v each [B, H, S, D]:  out_t[b,h,s,d] = qkv[b*S+s, (t*H+h)*D+d] + bias[(t*H+h)*D+d].
+ *   Outputs must not overlap the inputs or each other.
+ * tt_merge_heads:  in [B, H, S, D] -> out [B*S, H*D]: out[b*S+s, h*D+d] = in[b,h,s,d].
+ *   out must not overlap in.
+ * Index spaces must fit 32 bits (B*S*3*H*D < 2^32), else TT_ERROR_NOT_SUPPORTED.
+ * ---------------------------------------------------------------------- */
+TT_API tt_status tt_add_bias_gelu(int dtype, void* out, const void* x, const void* bias,
+                                  int64_t rows, int64_t n, int approximate, cudaStream_t stream);
+TT_API tt_status tt_split_qkv_add_bias(int dtype, void* q, void* k, void* v, const void* qkv,
+                                       const void* bias, int64_t B, int64_t S, int64_t H,
+                                       int64_t D, cudaStream_t stream);
+TT_API tt_status tt_merge_heads(int dtype, void* out, const void* in, int64_t B, int64_t S,
+                                int64_t H, int64_t D, cudaStream_t stream);
+
+/* ------------------------------------------------------------------------
  * Staged (host-buffer) variants: the end-to-end serving call.  On `stream`:
  * copy the HOST inputs into the caller's DEVICE buffers, run the kernel, copy
  * the result back into the HOST buffer.  Host buffers should be pinned

@@ -34,6 +34,7 @@ EXPORTS = (
     "tt_status_string", "tt_last_cuda_error", "tt_version",
     "tt_softmax_masked_plan", "tt_add_bias_layernorm_plan", "tt_softmax_packed_plan",
     "ttx_tier_count", "ttx_tier_name", "ttx_force_tier",
+    "tt_add_bias_gelu", "tt_split_qkv_add_bias", "tt_merge_heads",
 )
 
 
@@ -75,6 +76,10 @@ def lib() -> ctypes.CDLL:
                                                        _vp, _i64, _i64, _f, _vp]
             L.tt_softmax_masked_plan.argtypes = [_i, _i64, _i64, _i64, _i64, ctypes.c_char_p, _i]
             L.tt_add_bias_layernorm_plan.argtypes = [_i, _i64, _i64, ctypes.c_char_p, _i]
+            L.tt_add_bias_gelu.argtypes = [_i, _vp, _vp, _vp, _i64, _i64, _i, _vp]
+            L.tt_split_qkv_add_bias.argtypes = [_i, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64,
+                                                _i64, _vp]
+            L.tt_merge_heads.argtypes = [_i, _vp, _vp, _i64, _i64, _i64, _i64, _vp]
             L.ttx_tier_count.argtypes = [_i]
             L.ttx_tier_name.argtypes = [_i, _i, _i]
             L.ttx_tier_name.restype = ctypes.c_char_p
@@ -251,6 +256,50 @@ def layernorm_plan(dtype: torch.dtype, rows: int, hidden: int) -> str:
     _check(lib().tt_add_bias_layernorm_plan(DTYPE_CODE[dtype], rows, hidden, buf, 128),
            "tt_add_bias_layernorm_plan")
     return buf.value.decode()
+
+
+# --------------------------------------------------------------------- NEXT-2
+def tt_add_bias_gelu(out: torch.Tensor, x: torch.Tensor, bias: torch.Tensor,
+                     approximate: bool = False, stream=None):
+    """out <- gelu(x + bias) over the last dim (tt_add_bias_gelu)."""
+    for t, nm in ((out, "out"), (x, "x"), (bias, "bias")):
+        _dev(t, nm)
+        if t.dtype != x.dtype:
+            raise ValueError("all operands share one dtype")
+    n = x.shape[-1]
+    rows = x.numel() // n if n else 0
+    if out.shape != x.shape or bias.numel() != n:
+        raise ValueError("shape mismatch")
+    _check(lib().tt_add_bias_gelu(DTYPE_CODE[x.dtype], out.data_ptr(), x.data_ptr(),
+                                  bias.data_ptr(), rows, n, int(bool(approximate)),
+                                  _stream_ptr(stream)), "tt_add_bias_gelu")
+    return out
+
+
+def tt_split_qkv_add_bias(q, k, v, qkv, bias, B: int, S: int, H: int, D: int, stream=None):
+    """qkv [B*S, 3*H*D] + bias -> q, k, v [B, H, S, D] (tt_split_qkv_add_bias)."""
+    for t, nm in ((q, "q"), (k, "k"), (v, "v"), (qkv, "qkv"), (bias, "bias")):
+        _dev(t, nm)
+        if t.dtype != qkv.dtype:
+            raise ValueError("all operands share one dtype")
+    if qkv.numel() != B * S * 3 * H * D or bias.numel() != 3 * H * D or \
+            any(t.numel() != B * H * S * D for t in (q, k, v)):
+        raise ValueError("shape mismatch")
+    _check(lib().tt_split_qkv_add_bias(DTYPE_CODE[qkv.dtype], q.data_ptr(), k.data_ptr(),
+                                       v.data_ptr(), qkv.data_ptr(), bias.data_ptr(), B, S, H, D,
+                                       _stream_ptr(stream)), "tt_split_qkv_add_bias")
+    return q, k, v
+
+
+def tt_merge_heads(out, x, B: int, S: int, H: int, D: int, stream=None):
+    """[B, H, S, D] -> [B*S, H*D] (tt_merge_heads)."""
+    _dev(out, "out")
+    _dev(x, "in")
+    if out.dtype != x.dtype or out.numel() != x.numel() or x.numel() != B * H * S * D:
+        raise ValueError("shape mismatch")
+    _check(lib().tt_merge_heads(DTYPE_CODE[x.dtype], out.data_ptr(), x.data_ptr(), B, S, H, D,
+                                _stream_ptr(stream)), "tt_merge_heads")
+    return out
 
 
 # --------------------------------------------------------------------- tuning

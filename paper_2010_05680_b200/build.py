@@ -20,7 +20,7 @@ CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(PKG, "libtt.so")
 BUILD_DIR = os.path.join(PKG, "_build")
-SOURCES = ["tt_api.cu", "softmax.cu", "softmax_packed.cu", "layernorm.cu"]
+SOURCES = ["tt_api.cu", "softmax.cu", "softmax_packed.cu", "layernorm.cu", "elementwise.cu"]
 HEADERS = ["common.cuh", "launch.h", "softmax_row.cuh"]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

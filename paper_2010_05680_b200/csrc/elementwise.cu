@@ -1,0 +1,251 @@
+// elementwise.cu -- NEXT-2: the element-wise non-GEMM kernels of
+// the fused transformer graph, "fused activation functions and fused
+// transpose operations" (K4 / K5 in SURVEY §2.2):
+//
+//   add_bias_gelu      out = gelu(x + bias) over [rows, n]   (FFN-up epilogue)
+//   split_qkv_add_bias qkv [B*S, 3*H*D] + bias -> q, k, v [B, H, S, D]
+//   merge_heads        [B, H, S, D] -> [B*S, H*D]            (after P.V)
+//
+// All three are pure streaming kernels (every byte read once, written once),
+// HBM-bound like the reductions.  They move VB-byte vectors (16 B, or the
+// element size when alignment / pitch forbid), fp32 arithmetic, RNE narrowing.
+#include <atomic>
+
+#include "common.cuh"
+#include "launch.h"
+
+namespace tt {
+
+namespace {
+
+template <typename T, int VB>
+__device__ __forceinline__ void add_vec(Raw<VB>& w, const Raw<VB>& b) {
+    constexpr int VE = VB / (int)sizeof(T);
+    float f[VE], g[VE];
+    Elem<T>::template unpack<VB>(w, f);
+    Elem<T>::template unpack<VB>(b, g);
+#pragma unroll
+    for (int e = 0; e < VE; ++e) f[e] += g[e];
+    Elem<T>::template pack<VB>(f, w);
+}
+
+int sm_count_e() {
+    static int cached[64] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) dev = 0;
+    if (!cached[dev]) {
+        int n = 0;
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        cached[dev] = n > 0 ? n : 148;
+    }
+    return cached[dev];
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------- GELU
+// One CTA walks RPB rows; each thread takes the row's vectors tid, tid + NT, ...
+// (bias vectors are the same for every row, so they stay in L1).
+template <typename T, int VB, bool APPROX, int NT>
+__global__ void __launch_bounds__(NT) add_bias_gelu_kernel(T* out, const T* x,
+                                                           const T* __restrict__ bias,
+                                                           int64_t rows, int n, int rpb) {
+    constexpr int VE = VB / (int)sizeof(T);
+    const int nvec = n / VE;
+    const int64_t r0 = (int64_t)blockIdx.x * rpb;
+    const int64_t r1 = min(rows, r0 + rpb);
+    for (int64_t r = r0; r < r1; ++r) {
+        const T* xr = x + r * (int64_t)n;
+        T* orow = out + r * (int64_t)n;
+        for (int vi = threadIdx.x; vi < nvec; vi += NT) {
+            Raw<VB> wx, wb;
+            ld_stream<VB>(xr + vi * VE, wx);
+            ld_param<VB>(bias + vi * VE, wb);
+            float f[VE], g[VE];
+            Elem<T>::template unpack<VB>(wx, f);
+            Elem<T>::template unpack<VB>(wb, g);
+#pragma unroll
+            for (int e = 0; e < VE; ++e) {
+                const float v = f[e] + g[e];
+                if constexpr (APPROX)
+                    f[e] = 0.5f * v *
+                           (1.0f + tanhf(0.7978845608028654f * fmaf(0.044715f * v, v * v, v)));
+                else
+                    f[e] = 0.5f * v * (1.0f + erff(v * 0.7071067811865476f));
+            }
+            Raw<VB> wy;
+            Elem<T>::template pack<VB>(f, wy);
+            st_stream<VB>(orow + vi * VE, wy);
+        }
+    }
+}
+
+template <typename T, int VB, bool APPROX>
+cudaError_t launch_gelu(void* out, const void* x, const void* bias, int64_t rows, int64_t n,
+                        cudaStream_t st) {
+    constexpr int NT = 256;
+    const int64_t nvec = n / (VB / (int)sizeof(T));
+    // rows per CTA: enough vectors per CTA to amortise, enough CTAs to fill
+    // the SMs several times over
+    int64_t rpb = (4 * NT + nvec - 1) / nvec;
+    const int64_t max_rpb = (rows + 4 * (int64_t)sm_count_e() - 1) / (4 * (int64_t)sm_count_e());
+    if (rpb > max_rpb) rpb = max_rpb > 0 ? max_rpb : 1;
+    const int64_t grid = (rows + rpb - 1) / rpb;
+    if (grid > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
+    add_bias_gelu_kernel<T, VB, APPROX, NT><<<(unsigned)grid, NT, 0, st>>>(
+        static_cast<T*>(out), static_cast<const T*>(x), static_cast<const T*>(bias), rows,
+        (int)n, (int)rpb);
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- QKV split
+// work item = one D-vector (token, t, h): GD = D / VE lanes per item; items in
+// token-major order so the qkv reads are contiguous.
+template <typename T, int VB, int NT>
+__global__ void __launch_bounds__(NT) split_qkv_kernel(T* q, T* k, T* v, const T* qkv,
+                                                       const T* __restrict__ bias, uint32_t S,
+                                                       uint32_t H, uint32_t D, uint64_t total,
+                                                       FastDivU32 div_gd, FastDivU32 div_3h,
+                                                       FastDivU32 div_s) {
+    constexpr int VE = VB / (int)sizeof(T);
+    const uint32_t gd = D / VE;
+    for (uint64_t i = (uint64_t)blockIdx.x * NT + threadIdx.x; i < total;
+         i += (uint64_t)gridDim.x * NT) {
+        const uint32_t item = div_gd.div((uint32_t)i);
+        const uint32_t lane = (uint32_t)i - item * gd;
+        const uint32_t token = div_3h.div(item);
+        const uint32_t th = item - token * 3 * H;  // t * H + h
+        const uint32_t t = th >= 2 * H ? 2 : (th >= H ? 1 : 0);
+        const uint32_t h = th - t * H;
+        const uint32_t b = div_s.div(token);
+        const uint32_t s = token - b * S;
+        Raw<VB> w, wb;
+        ld_stream<VB>(qkv + (uint64_t)item * D + lane * VE, w);
+        ld_param<VB>(bias + (uint64_t)th * D + lane * VE, wb);
+        add_vec<T, VB>(w, wb);
+        T* dst = t == 0 ? q : (t == 1 ? k : v);
+        st_stream<VB>(dst + (((uint64_t)b * H + h) * S + s) * D + lane * VE, w);
+    }
+}
+
+template <typename T, int VB>
+cudaError_t launch_split(void* q, void* k, void* v, const void* qkv, const void* bias,
+                         int64_t B, int64_t S, int64_t H, int64_t D, cudaStream_t st) {
+    constexpr int NT = 256;
+    const uint64_t gd = (uint64_t)(D / (VB / (int)sizeof(T)));
+    const uint64_t total = (uint64_t)B * S * 3 * H * gd;
+    if (total >= 0xffffffffull) return cudaErrorInvalidConfiguration;
+    const uint64_t want = (total + NT - 1) / NT;
+    const uint64_t cap = (uint64_t)sm_count_e() * 16;
+    const unsigned grid = (unsigned)(want < cap ? want : cap);
+    split_qkv_kernel<T, VB, NT><<<grid, NT, 0, st>>>(
+        static_cast<T*>(q), static_cast<T*>(k), static_cast<T*>(v), static_cast<const T*>(qkv),
+        static_cast<const T*>(bias), (uint32_t)S, (uint32_t)H, (uint32_t)D, total,
+        FastDivU32::make((uint32_t)gd), FastDivU32::make((uint32_t)(3 * H)),
+        FastDivU32::make((uint32_t)S));
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- head merge
+// work item = one D-vector (token, h) in output order (token-major, h inner)
+template <typename T, int VB, int NT>
+__global__ void __launch_bounds__(NT) merge_heads_kernel(T* out, const T* in, uint32_t S,
+                                                         uint32_t H, uint32_t D, uint64_t total,
+                                                         FastDivU32 div_gd, FastDivU32 div_h,
+                                                         FastDivU32 div_s) {
+    constexpr int VE = VB / (int)sizeof(T);
+    const uint32_t gd = D / VE;
+    for (uint64_t i = (uint64_t)blockIdx.x * NT + threadIdx.x; i < total;
+         i += (uint64_t)gridDim.x * NT) {
+        const uint32_t item = div_gd.div((uint32_t)i);
+        const uint32_t lane = (uint32_t)i - item * gd;
+        const uint32_t token = div_h.div(item);
+        const uint32_t h = item - token * H;
+        const uint32_t b = div_s.div(token);
+        const uint32_t s = token - b * S;
+        Raw<VB> w;
+        ld_stream<VB>(in + (((uint64_t)b * H + h) * S + s) * D + lane * VE, w);
+        st_stream<VB>(out + (uint64_t)item * D + lane * VE, w);
+    }
+}
+
+template <typename T, int VB>
+cudaError_t launch_merge(void* out, const void* in, int64_t B, int64_t S, int64_t H, int64_t D,
+                         cudaStream_t st) {
+    constexpr int NT = 256;
+    const uint64_t gd = (uint64_t)(D / (VB / (int)sizeof(T)));
+    const uint64_t total = (uint64_t)B * S * H * gd;
+    if (total >= 0xffffffffull) return cudaErrorInvalidConfiguration;
+    const uint64_t want = (total + NT - 1) / NT;
+    const uint64_t cap = (uint64_t)sm_count_e() * 16;
+    const unsigned grid = (unsigned)(want < cap ? want : cap);
+    merge_heads_kernel<T, VB, NT><<<grid, NT, 0, st>>>(
+        static_cast<T*>(out), static_cast<const T*>(in), (uint32_t)S, (uint32_t)H, (uint32_t)D,
+        total, FastDivU32::make((uint32_t)gd), FastDivU32::make((uint32_t)H),
+        FastDivU32::make((uint32_t)S));
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- dispatch
+// vec_bytes (host-computed from pointer alignment and pitches) picks 16-byte
+// vectors or the element-size fallback.
+namespace {
+
+template <typename T>
+cudaError_t gelu_t(void* out, const void* x, const void* bias, int64_t rows, int64_t n,
+                   int approximate, int vec_bytes, cudaStream_t st) {
+    if (vec_bytes >= 16)
+        return approximate ? launch_gelu<T, 16, true>(out, x, bias, rows, n, st)
+                           : launch_gelu<T, 16, false>(out, x, bias, rows, n, st);
+    return approximate ? launch_gelu<T, sizeof(T), true>(out, x, bias, rows, n, st)
+                       : launch_gelu<T, sizeof(T), false>(out, x, bias, rows, n, st);
+}
+
+template <typename T>
+cudaError_t split_t(void* q, void* k, void* v, const void* qkv, const void* bias, int64_t B,
+                    int64_t S, int64_t H, int64_t D, int vec_bytes, cudaStream_t st) {
+    if (vec_bytes >= 16) return launch_split<T, 16>(q, k, v, qkv, bias, B, S, H, D, st);
+    return launch_split<T, sizeof(T)>(q, k, v, qkv, bias, B, S, H, D, st);
+}
+
+template <typename T>
+cudaError_t merge_t(void* out, const void* in, int64_t B, int64_t S, int64_t H, int64_t D,
+                    int vec_bytes, cudaStream_t st) {
+    if (vec_bytes >= 16) return launch_merge<T, 16>(out, in, B, S, H, D, st);
+    return launch_merge<T, sizeof(T)>(out, in, B, S, H, D, st);
+}
+
+}  // namespace
+
+cudaError_t gelu_launch(int dtype, void* out, const void* x, const void* bias, int64_t rows,
+                        int64_t n, int approximate, int vec_bytes, cudaStream_t stream) {
+    switch (dtype) {
+        case 0: return gelu_t<float>(out, x, bias, rows, n, approximate, vec_bytes, stream);
+        case 1: return gelu_t<__half>(out, x, bias, rows, n, approximate, vec_bytes, stream);
+        default:
+            return gelu_t<__nv_bfloat16>(out, x, bias, rows, n, approximate, vec_bytes, stream);
+    }
+}
+
+cudaError_t split_qkv_launch(int dtype, void* q, void* k, void* v, const void* qkv,
+                             const void* bias, int64_t B, int64_t S, int64_t H, int64_t D,
+                             int vec_bytes, cudaStream_t stream) {
+    switch (dtype) {
+        case 0: return split_t<float>(q, k, v, qkv, bias, B, S, H, D, vec_bytes, stream);
+        case 1: return split_t<__half>(q, k, v, qkv, bias, B, S, H, D, vec_bytes, stream);
+        default:
+            return split_t<__nv_bfloat16>(q, k, v, qkv, bias, B, S, H, D, vec_bytes, stream);
+    }
+}
+
+cudaError_t merge_heads_launch(int dtype, void* out, const void* in, int64_t B, int64_t S,
+                               int64_t H, int64_t D, int vec_bytes, cudaStream_t stream) {
+    switch (dtype) {
+        case 0: return merge_t<float>(out, in, B, S, H, D, vec_bytes, stream);
+        case 1: return merge_t<__half>(out, in, B, S, H, D, vec_bytes, stream);
+        default: return merge_t<__nv_bfloat16>(out, in, B, S, H, D, vec_bytes, stream);
+    }
+}
+
+}  // namespace tt

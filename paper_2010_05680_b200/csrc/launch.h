@@ -31,6 +31,16 @@ cudaError_t layernorm_launch(int dtype, void* out, const void* x, const void* re
                              bool* supported);
 const char* layernorm_tier_name(int dtype, int64_t hidden, int vec_bytes, int64_t rows);
 
+// NEXT-2 element-wise kernels (elementwise.cu).  vec_bytes: 16 when every
+// operand base and row pitch is 16-byte aligned, else the element size.
+cudaError_t gelu_launch(int dtype, void* out, const void* x, const void* bias, int64_t rows,
+                        int64_t n, int approximate, int vec_bytes, cudaStream_t stream);
+cudaError_t split_qkv_launch(int dtype, void* q, void* k, void* v, const void* qkv,
+                             const void* bias, int64_t B, int64_t S, int64_t H, int64_t D,
+                             int vec_bytes, cudaStream_t stream);
+cudaError_t merge_heads_launch(int dtype, void* out, const void* in, int64_t B, int64_t S,
+                               int64_t H, int64_t D, int vec_bytes, cudaStream_t stream);
+
 // Tuning / test hooks (include/tt_tune.h): enumerate every compiled tier and
 // force one (-1 = automatic selection).  A forced tier that cannot serve the
 // call's shape is ignored.

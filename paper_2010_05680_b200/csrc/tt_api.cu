@@ -135,6 +135,84 @@ tt_status ln_any(int dtype, void* out, const void* x, const void* residual, cons
     return cuda_status(e);
 }
 
+// ------------------------------------------------------------------- NEXT-2
+// 16 when every pointer and every pitch (bytes) is a multiple of 16, else 0
+int vec16(const void* const* ptrs, int nptrs, const int64_t* pitches, int npitch) {
+    for (int i = 0; i < nptrs; ++i)
+        if (reinterpret_cast<uintptr_t>(ptrs[i]) & 15u) return 0;
+    for (int i = 0; i < npitch; ++i)
+        if (pitches[i] % 16) return 0;
+    return 16;
+}
+
+tt_status gelu_any(int dtype, void* out, const void* x, const void* bias, int64_t rows, int64_t n,
+                   int approximate, cudaStream_t stream) {
+    if (dtype < 0 || dtype > 2 || rows < 0 || n < 0 || approximate < 0 || approximate > 1)
+        return TT_ERROR_INVALID_VALUE;
+    int64_t cnt, nb;
+    if (mul_overflows(rows, n, &cnt) || mul_overflows(cnt, elem_bytes(dtype), &nb))
+        return TT_ERROR_INVALID_VALUE;
+    if (cnt == 0) return TT_SUCCESS;
+    if (!out || !x || !bias) return TT_ERROR_INVALID_VALUE;
+    const int64_t pb = n * elem_bytes(dtype);
+    if (out != x && overlaps(out, nb, x, nb)) return TT_ERROR_INVALID_VALUE;
+    if (overlaps(out, nb, bias, pb)) return TT_ERROR_INVALID_VALUE;
+    if ((reinterpret_cast<uintptr_t>(out) | reinterpret_cast<uintptr_t>(x) |
+         reinterpret_cast<uintptr_t>(bias)) & (uintptr_t)(elem_bytes(dtype) - 1))
+        return TT_ERROR_NOT_SUPPORTED;
+    if (n > 0x7fffffffLL) return TT_ERROR_NOT_SUPPORTED;
+    const void* ps[3] = {out, x, bias};
+    const int vb = vec16(ps, 3, &pb, 1);
+    return cuda_status(tt::gelu_launch(dtype, out, x, bias, rows, n, approximate, vb, stream));
+}
+
+tt_status split_any(int dtype, void* q, void* k, void* v, const void* qkv, const void* bias,
+                    int64_t B, int64_t S, int64_t H, int64_t D, cudaStream_t stream) {
+    if (dtype < 0 || dtype > 2 || B < 0 || S < 0 || H < 0 || D < 0) return TT_ERROR_INVALID_VALUE;
+    int64_t bs, n, nb;
+    if (mul_overflows(B, S, &bs) || mul_overflows(bs, 3 * H, &n) || mul_overflows(n, D, &n) ||
+        mul_overflows(n, elem_bytes(dtype), &nb))
+        return TT_ERROR_INVALID_VALUE;
+    if (n == 0) return TT_SUCCESS;
+    if (!q || !k || !v || !qkv || !bias) return TT_ERROR_INVALID_VALUE;
+    const int64_t part = nb / 3, pb = 3 * H * D * elem_bytes(dtype);
+    const void* outs[3] = {q, k, v};
+    for (int i = 0; i < 3; ++i) {
+        if (overlaps(outs[i], part, qkv, nb) || overlaps(outs[i], part, bias, pb))
+            return TT_ERROR_INVALID_VALUE;
+        for (int j = i + 1; j < 3; ++j)
+            if (overlaps(outs[i], part, outs[j], part)) return TT_ERROR_INVALID_VALUE;
+    }
+    const void* ps[5] = {q, k, v, qkv, bias};
+    for (const void* p : ps)
+        if (reinterpret_cast<uintptr_t>(p) & (uintptr_t)(elem_bytes(dtype) - 1))
+            return TT_ERROR_NOT_SUPPORTED;
+    if (n >= (int64_t)0xffffffffLL) return TT_ERROR_NOT_SUPPORTED;
+    const int64_t pitch = D * elem_bytes(dtype);
+    const int vb = vec16(ps, 5, &pitch, 1);
+    return cuda_status(tt::split_qkv_launch(dtype, q, k, v, qkv, bias, B, S, H, D, vb, stream));
+}
+
+tt_status merge_any(int dtype, void* out, const void* in, int64_t B, int64_t S, int64_t H,
+                    int64_t D, cudaStream_t stream) {
+    if (dtype < 0 || dtype > 2 || B < 0 || S < 0 || H < 0 || D < 0) return TT_ERROR_INVALID_VALUE;
+    int64_t bs, n, nb;
+    if (mul_overflows(B, S, &bs) || mul_overflows(bs, H, &n) || mul_overflows(n, D, &n) ||
+        mul_overflows(n, elem_bytes(dtype), &nb))
+        return TT_ERROR_INVALID_VALUE;
+    if (n == 0) return TT_SUCCESS;
+    if (!out || !in) return TT_ERROR_INVALID_VALUE;
+    if (overlaps(out, nb, in, nb)) return TT_ERROR_INVALID_VALUE;
+    if ((reinterpret_cast<uintptr_t>(out) | reinterpret_cast<uintptr_t>(in)) &
+        (uintptr_t)(elem_bytes(dtype) - 1))
+        return TT_ERROR_NOT_SUPPORTED;
+    if (n >= (int64_t)0xffffffffLL) return TT_ERROR_NOT_SUPPORTED;
+    const void* ps[2] = {out, in};
+    const int64_t pitch = D * elem_bytes(dtype);
+    const int vb = vec16(ps, 2, &pitch, 1);
+    return cuda_status(tt::merge_heads_launch(dtype, out, in, B, S, H, D, vb, stream));
+}
+
 // ------------------------------------------------------------------- packed
 tt_status packed_validate(int dtype, const void* scores, const int32_t* cu, const int64_t* blocks,
                           int64_t num_req, int64_t H, int64_t total_tokens, int64_t max_len,
@@ -228,6 +306,22 @@ tt_status tt_add_bias_layernorm_bf16(void* out, const void* x, const void* resid
                                      const void* bias, const void* gamma, const void* beta,
                                      int64_t rows, int64_t hidden, float eps, cudaStream_t stream) {
     return ln_any(2, out, x, residual, bias, gamma, beta, rows, hidden, eps, stream);
+}
+
+tt_status tt_add_bias_gelu(int dtype, void* out, const void* x, const void* bias, int64_t rows,
+                           int64_t n, int approximate, cudaStream_t stream) {
+    return gelu_any(dtype, out, x, bias, rows, n, approximate, stream);
+}
+
+tt_status tt_split_qkv_add_bias(int dtype, void* q, void* k, void* v, const void* qkv,
+                                const void* bias, int64_t B, int64_t S, int64_t H, int64_t D,
+                                cudaStream_t stream) {
+    return split_any(dtype, q, k, v, qkv, bias, B, S, H, D, stream);
+}
+
+tt_status tt_merge_heads(int dtype, void* out, const void* in, int64_t B, int64_t S, int64_t H,
+                         int64_t D, cudaStream_t stream) {
+    return merge_any(dtype, out, in, B, S, H, D, stream);
 }
 
 tt_status tt_softmax_masked_staged(int dtype, void* host_scores, const int32_t* host_lengths,

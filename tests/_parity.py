@@ -21,6 +21,10 @@ def ulp_bf16(ref: torch.Tensor) -> torch.Tensor:
 def bound(op: str, dtype, ref: torch.Tensor) -> torch.Tensor:
     one = torch.ones_like(ref)
     mag = torch.maximum(one, ref.abs())
+    if op == "gelu":   # NEXT-2 element-wise: fp32 1e-5 relative, 16-bit as LayerNorm
+        if dtype == torch.float32:
+            return 1e-5 * mag
+        op = "layernorm"
     if op == "softmax":
         if dtype == torch.float32:
             return torch.full_like(ref, 1e-5)
