@@ -32,7 +32,8 @@ def test_split_merge_validation(ttlib, dt):
     assert s(dt, P[0], P[1], P[3], P[3], P[4], 1, 2, 3, 8, 0) == INV       # v over qkv
     assert s(dt, *P, -1, 2, 3, 8, 0) == INV
     assert s(dt, P[0] + 1, P[1], P[2], P[3], P[4], 1, 2, 3, 8, 0) == NS
-    assert s(dt, *P, 1 << 12, 1 << 12, 64, 64, 0) == NS                    # > 2^32 items
+    huge = [FAKE + i * (1 << 42) for i in range(5)]                        # no overlap
+    assert s(dt, *huge, 1 << 12, 1 << 12, 64, 64, 0) == NS                 # > 2^32 items
     assert s(dt, 0, 0, 0, 0, 0, 0, 2, 3, 8, 0) == OK
     assert m(dt, 0, P[1], 1, 2, 3, 8, 0) == INV
     assert m(dt, P[0], P[0] + 8, 1, 2, 3, 8, 0) == INV                     # overlap
