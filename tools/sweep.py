@@ -93,8 +93,57 @@ def ln_case(cfg, dtype, rows, hidden, pk):
                 tier=tt.layernorm_plan(dtype, rows, hidden))
 
 
+def next2_cases(pk):
+    """NEXT-2 element-wise kernels on BERT shapes (read + write every byte once)."""
+    out = []
+    for dtype, B, S, H, D in ((torch.float16, 20, 128, 12, 64), (torch.bfloat16, 64, 512, 16, 64)):
+        e = W.ELEM_BYTES[dtype]
+        rows, hid = B * S, H * D
+        # GELU on the FFN-up output [rows, 4*hidden]
+        n = 4 * hid
+        nb = nbufs_for(2 * rows * n * e)
+        xs = [W.scores(1, 1, rows, n, dtype, device="cuda", seed=i, std=2.0).reshape(rows, n)
+              for i in range(nb)]
+        b = torch.zeros(n, dtype=dtype, device="cuda")
+        ys = [torch.empty_like(x) for x in xs]
+        us = timeit(lambda i: tt.tt_add_bias_gelu(ys[i], xs[i], b), nb, 50)
+        us_c = timeit(lambda i: ys[i].copy_(xs[i]), nb, 50)
+        alg = 2 * rows * n * e + n * e
+        out.append(dict(config=f"BERT b{B} s{S}", op="add_bias_gelu", dtype=W.DTYPE_NAMES[dtype],
+                        shape=[rows, n], ragged=False, us=round(us, 2),
+                        GBps=round(alg / us / 1e3, 1), pct_peak=round(100 * alg / us / 1e3 / pk, 1),
+                        copy_same_bytes_us=round(us_c, 2), tier="add_bias_gelu<V16>"))
+        # QKV split [rows, 3*hid] -> 3 x [B, H, S, D]; head merge [B, H, S, D] -> [rows, hid]
+        nb = nbufs_for(2 * rows * 3 * hid * e)
+        qkv = [W.scores(1, 1, rows, 3 * hid, dtype, device="cuda", seed=i).reshape(rows, 3 * hid)
+               for i in range(nb)]
+        bias = torch.zeros(3 * hid, dtype=dtype, device="cuda")
+        outs = [[torch.empty(B, H, S, D, dtype=dtype, device="cuda") for _ in range(3)]
+                for _ in range(nb)]
+        us = timeit(lambda i: tt.tt_split_qkv_add_bias(*outs[i], qkv[i], bias, B, S, H, D), nb, 50)
+        us_c = timeit(lambda i: outs[i][0].view(-1).copy_(qkv[i].view(-1)[:rows * hid]), nb, 50)
+        alg = 2 * rows * 3 * hid * e + 3 * hid * e
+        out.append(dict(config=f"BERT b{B} s{S}", op="split_qkv_add_bias", dtype=W.DTYPE_NAMES[dtype],
+                        shape=[rows, 3 * hid], ragged=False, us=round(us, 2),
+                        GBps=round(alg / us / 1e3, 1), pct_peak=round(100 * alg / us / 1e3 / pk, 1),
+                        copy_same_bytes_us=round(3 * us_c, 2), tier="split_qkv<V16>"))
+        ms = [torch.empty(rows, hid, dtype=dtype, device="cuda") for _ in range(nb)]
+        us = timeit(lambda i: tt.tt_merge_heads(ms[i], outs[i][0], B, S, H, D), nb, 50)
+        us_c = timeit(lambda i: ms[i].view(-1).copy_(outs[i][0].view(-1)), nb, 50)
+        alg = 2 * rows * hid * e
+        out.append(dict(config=f"BERT b{B} s{S}", op="merge_heads", dtype=W.DTYPE_NAMES[dtype],
+                        shape=[B, H, S, D], ragged=False, us=round(us, 2),
+                        GBps=round(alg / us / 1e3, 1), pct_peak=round(100 * alg / us / 1e3 / pk, 1),
+                        copy_same_bytes_us=round(us_c, 2), tier="merge_heads<V16>"))
+    return out
+
+
 def main():
     pk = peak()
+    if "--next2" in sys.argv:
+        for r in next2_cases(pk):
+            print(json.dumps(r), flush=True)
+        return
     # per-kernel floor inside a graph: torch's smallest kernel (1-element add)
     z = torch.zeros(1, device="cuda")
     floor = timeit(lambda i: z.add_(0), 1, 500)
