@@ -204,3 +204,38 @@ def merge_heads(x, B: int, S: int, H: int, D: int) -> torch.Tensor:
     rc = _load().tto_merge_heads(_ptr(xs), DTYPE_CODE[xs.dtype], B, S, H, D, _ptr(out))
     assert rc == 0
     return out
+
+
+# ------------------------------------------------------ NEXT-4 (Alg. 2) oracle
+def plan_cost(lengths, cost, batches) -> float:
+    """Alg. 2's objective: sum over batches of
+    cached_cost[max length][count] * count (plain Python)."""
+    total = 0.0
+    for b in batches:
+        L = max(int(lengths[i]) for i in b)
+        total += float(cost[L][len(b)]) * len(b)
+    return total
+
+
+def schedule_bruteforce(lengths, cost, max_batch: int):
+    """Exhaustive minimum of Alg. 2's objective over every contiguous partition
+    of the length-sorted request list (2^(n-1) plans; small n only).  Returns
+    (min_cost, one optimal plan as lists of request indices)."""
+    n = len(lengths)
+    order = sorted(range(n), key=lambda i: (int(lengths[i]), i))
+    best, best_plan = float("inf"), None
+    for mask in range(1 << max(n - 1, 0)):
+        plan, cur = [], [order[0]] if n else []
+        for k in range(1, n):
+            if mask >> (k - 1) & 1:
+                plan.append(cur)
+                cur = []
+            cur.append(order[k])
+        if cur:
+            plan.append(cur)
+        if any(len(b) > max_batch for b in plan):
+            continue
+        c = plan_cost(lengths, cost, plan)
+        if c < best:
+            best, best_plan = c, plan
+    return best, best_plan

@@ -35,6 +35,7 @@ EXPORTS = (
     "tt_softmax_masked_plan", "tt_add_bias_layernorm_plan", "tt_softmax_packed_plan",
     "ttx_tier_count", "ttx_tier_name", "ttx_force_tier",
     "tt_add_bias_gelu", "tt_split_qkv_add_bias", "tt_merge_heads",
+    "tt_dp_schedule", "tt_schedule_cost",
 )
 
 
@@ -80,6 +81,8 @@ def lib() -> ctypes.CDLL:
             L.tt_split_qkv_add_bias.argtypes = [_i, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64,
                                                 _i64, _vp]
             L.tt_merge_heads.argtypes = [_i, _vp, _vp, _i64, _i64, _i64, _i64, _vp]
+            L.tt_dp_schedule.argtypes = [_vp, _i64, _vp, _i64, _i64, _vp, _vp, _vp, _vp]
+            L.tt_schedule_cost.argtypes = [_vp, _i64, _vp, _i64, _i64, _vp, _vp, _i64, _vp]
             L.ttx_tier_count.argtypes = [_i]
             L.ttx_tier_name.argtypes = [_i, _i, _i]
             L.ttx_tier_name.restype = ctypes.c_char_p
@@ -300,6 +303,48 @@ def tt_merge_heads(out, x, B: int, S: int, H: int, D: int, stream=None):
     _check(lib().tt_merge_heads(DTYPE_CODE[x.dtype], out.data_ptr(), x.data_ptr(), B, S, H, D,
                                 _stream_ptr(stream)), "tt_merge_heads")
     return out
+
+
+# ------------------------------------------------------------------ scheduler
+def _cost_array(cost):
+    import numpy as np
+    c = np.ascontiguousarray(np.asarray(cost, dtype=np.float64))
+    if c.ndim != 2 or c.shape[0] < 2 or c.shape[1] < 2:
+        raise ValueError("cost table must be [max_len + 1, max_batch + 1]")
+    return c
+
+
+def dp_schedule(lengths, cost):
+    """Alg. 2 (tt_dp_schedule): returns (batches, total_cost), each batch a list
+    of request indices (queue order), batches in increasing padded length."""
+    import numpy as np
+    lens = np.ascontiguousarray(np.asarray(lengths, dtype=np.int32))
+    c = _cost_array(cost)
+    n = lens.size
+    order = np.zeros(max(n, 1), dtype=np.int32)
+    starts = np.zeros(n + 1, dtype=np.int32)
+    nb = ctypes.c_int64(0)
+    tot = ctypes.c_double(0.0)
+    _check(lib().tt_dp_schedule(lens.ctypes.data, n, c.ctypes.data, c.shape[0] - 1,
+                                c.shape[1] - 1, order.ctypes.data, starts.ctypes.data,
+                                ctypes.addressof(nb), ctypes.addressof(tot)), "tt_dp_schedule")
+    batches = [order[starts[b]:starts[b + 1]].tolist() for b in range(nb.value)]
+    return batches, tot.value
+
+
+def schedule_cost(lengths, cost, batches) -> float:
+    """Cost of a given plan under Alg. 2's model (tt_schedule_cost)."""
+    import numpy as np
+    lens = np.ascontiguousarray(np.asarray(lengths, dtype=np.int32))
+    c = _cost_array(cost)
+    idx = np.ascontiguousarray(np.asarray([i for b in batches for i in b] or [0],
+                                          dtype=np.int32))
+    starts = np.ascontiguousarray(np.cumsum([0] + [len(b) for b in batches]).astype(np.int32))
+    tot = ctypes.c_double(0.0)
+    _check(lib().tt_schedule_cost(lens.ctypes.data, lens.size, c.ctypes.data, c.shape[0] - 1,
+                                  c.shape[1] - 1, idx.ctypes.data, starts.ctypes.data,
+                                  len(batches), ctypes.addressof(tot)), "tt_schedule_cost")
+    return tot.value
 
 
 # --------------------------------------------------------------------- tuning

@@ -20,7 +20,8 @@ CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(PKG, "libtt.so")
 BUILD_DIR = os.path.join(PKG, "_build")
-SOURCES = ["tt_api.cu", "softmax.cu", "softmax_packed.cu", "layernorm.cu", "elementwise.cu"]
+SOURCES = ["tt_api.cu", "softmax.cu", "softmax_packed.cu", "layernorm.cu", "elementwise.cu",
+           "scheduler.cpp"]
 HEADERS = ["common.cuh", "launch.h", "softmax_row.cuh"]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
@@ -31,7 +32,7 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-fvisibility=hid
 
 def _inputs():
     srcs = [os.path.join(CSRC, s) for s in SOURCES]
-    deps = srcs + [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(INCLUDE, h) for h in ("tt.h", "tt_tune.h")]
+    deps = srcs + [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(INCLUDE, h) for h in ("tt.h", "tt_tune.h", "tt_sched.h")]
     return srcs, deps
 
 
