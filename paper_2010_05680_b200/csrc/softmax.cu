@@ -580,23 +580,19 @@ struct SoftmaxTier {
     TT_SM_TIER(true, T, TN, 32, 64, NVC, 1, 64, 1), TT_SM_TIER(true, T, TN, 32, 128, NVC, 1, 128, 1), \
     TT_SM_TIER(true, T, TN, 32, 256, NVC, 1, 256, 1), TT_SM_TIER(true, T, TN, 32, 512, NVC, 1, 512, 1), \
     TT_SM_TIER(true, T, TN, 32, 1024, NVC, 1, 1024, 1),                                     \
-    TT_SM_TIER(false, T, TN, 32, 32, 1, 1, 256, 6), TT_SM_TIER(false, T, TN, 32, 32, 1, 2, 256, 1), \
-    TT_SM_TIER(false, T, TN, 32, 32, 2, 1, 256, 1), TT_SM_TIER(false, T, TN, 16, 32, 1, 2, 256, 1), \
-    TT_SM_TMA(false, T, TN, 2, 8), TT_SM_TMA(false, T, TN, 2, 4), TT_SM_TMA(false, T, TN, 4, 8),     \
-    TT_SM_TMA(false, T, TN, 4, 4), TT_SM_TMA(false, T, TN, 8, 4), TT_SM_TMA(false, T, TN, 1, 8),     \
-    TT_SM_WARP(false, T, TN, 32, 32, 1, 256, 4), TT_SM_WARP(false, T, TN, 32, 32, 1, 256, 5),   \
-    TT_SM_WARP(false, T, TN, 32, 32, 1, 256, 7), TT_SM_WARP(false, T, TN, 32, 32, 1, 256, 8),   \
-    TT_SM_WARP(false, T, TN, 32, 32, 1, 128, 12), TT_SM_WARP(false, T, TN, 32, 32, 1, 128, 16), \
-    TT_SM_WARP(false, T, TN, 32, 32, 1, 512, 4), TT_SM_WARP(false, T, TN, 32, 32, 2, 256, 3),   \
-    TT_SM_WARP(false, T, TN, 32, 32, 2, 256, 5), TT_SM_WARP(false, T, TN, 32, 32, 2, 128, 10),  \
-    TT_SM_WARP(false, T, TN, 16, 32, 2, 256, 6), TT_SM_WARP(false, T, TN, 16, 32, 2, 256, 8),   \
-    TT_SM_WARP(false, T, TN, 16, 32, 1, 256, 8), TT_SM_WARP(false, T, TN, 32, 32, 3, 256, 2),   \
-    TT_SM_WARP_R(false, T, TN, 32, 32, 1, 256, 5, 0), TT_SM_WARP_R(false, T, TN, 32, 32, 1, 256, 5, 1), \
-    TT_SM_WARP_R(false, T, TN, 32, 32, 1, 256, 5, 2), TT_SM_WARP_R(false, T, TN, 32, 32, 1, 256, 5, 8), \
-    TT_SM_WARP_R(false, T, TN, 32, 32, 1, 256, 5, 16), TT_SM_WARP_R(false, T, TN, 32, 32, 1, 256, 6, 0), \
-    TT_SM_WARP_R(false, T, TN, 32, 32, 1, 256, 6, 1), TT_SM_WARP_R(false, T, TN, 32, 32, 1, 256, 6, 2), \
-    TT_SM_WARP_R(false, T, TN, 32, 32, 1, 256, 6, 8), TT_SM_WARP_R(false, T, TN, 32, 32, 2, 256, 3, 0), \
-    TT_SM_WARP_R(false, T, TN, 32, 32, 2, 256, 3, 2), TT_SM_WARP_R(false, T, TN, 32, 32, 2, 256, 3, 8)
+    TT_SM_TIER(false, T, TN, 32, 32, 1, 1, 256, 6), TT_SM_TMA(false, T, TN, 2, 4),             \
+    TT_SM_TMA(false, T, TN, 4, 8),                                                             \
+    TT_SM_WARP(false, T, TN, 32, 32, 1, 256, 5), TT_SM_WARP(false, T, TN, 32, 32, 1, 128, 12),  \
+    TT_SM_WARP(false, T, TN, 32, 32, 2, 256, 3), TT_SM_WARP(false, T, TN, 32, 32, 2, 256, 5),   \
+    TT_SM_WARP(false, T, TN, 16, 32, 2, 256, 6), TT_SM_WARP(false, T, TN, 32, 32, 3, 256, 2),   \
+    TT_SM_WARP_R(false, T, TN, 32, 32, 1, 256, 6, 2), TT_SM_WARP_R(false, T, TN, 32, 32, 1, 256, 6, 8), \
+    TT_SM_WARP_R(false, T, TN, 32, 32, 2, 256, 3, 2),                                         \
+    TT_SM_WARP(false, T, TN, 16, 8, 4, 256, 4), TT_SM_WARP(false, T, TN, 16, 8, 5, 256, 3),     \
+    TT_SM_WARP(false, T, TN, 16, 8, 6, 256, 3), TT_SM_WARP(false, T, TN, 16, 8, 7, 256, 2),     \
+    TT_SM_WARP(false, T, TN, 16, 16, 3, 256, 4), TT_SM_WARP(false, T, TN, 16, 16, 4, 256, 3),   \
+    TT_SM_WARP(false, T, TN, 32, 8, 3, 256, 3), TT_SM_WARP(false, T, TN, 32, 8, 2, 256, 4),     \
+    TT_SM_WARP(false, T, TN, 32, 16, 2, 256, 3), TT_SM_WARP(false, T, TN, 16, 8, 5, 256, 4),    \
+    TT_SM_WARP(false, T, TN, 16, 16, 3, 256, 5), TT_SM_WARP(false, T, TN, 16, 8, 3, 256, 5)
 
 // M2..M4: min CTAs/SM (register cap) of the NV = 2..4 warp tiers, chosen so
 // the row (NV * VE fp32 values per lane) fits without spilling.
