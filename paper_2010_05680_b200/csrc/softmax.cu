@@ -592,7 +592,8 @@ struct SoftmaxTier {
     TT_SM_WARP(false, T, TN, 16, 16, 3, 256, 4), TT_SM_WARP(false, T, TN, 16, 16, 4, 256, 3),   \
     TT_SM_WARP(false, T, TN, 32, 8, 3, 256, 3), TT_SM_WARP(false, T, TN, 32, 8, 2, 256, 4),     \
     TT_SM_WARP(false, T, TN, 32, 16, 2, 256, 3), TT_SM_WARP(false, T, TN, 16, 8, 5, 256, 4),    \
-    TT_SM_WARP(false, T, TN, 16, 16, 3, 256, 5), TT_SM_WARP(false, T, TN, 16, 8, 3, 256, 5)
+    TT_SM_WARP(false, T, TN, 16, 16, 3, 256, 5), TT_SM_WARP(false, T, TN, 16, 8, 3, 256, 5),   \
+    TT_SM_WARP(false, T, TN, 16, 8, 2, 256, 6)
 
 // M2..M4: min CTAs/SM (register cap) of the NV = 2..4 warp tiers, chosen so
 // the row (NV * VE fp32 values per lane) fits without spilling.
@@ -619,8 +620,20 @@ struct Pref {
     int min_cols, max_cols;
     const char* name;
 };
+// Capacity-fitting sub-warp tiers (G8 with several vectors per lane) win where
+// the warp-per-row tier would leave lanes idle; see profiles/*_tune.txt.
 const Pref kSmPref[] = {
-    {0, 256, 512, "softmax_warp<f32,V32,G32,NV2,T256,M3,P2>"},
+    {0, 128, 256, "softmax_warp<f32,V32,G32,NV1,T256,M6,P2>"},
+    {0, 256, 384, "softmax_warp<f32,V32,G32,NV2,T256,M6,P4>"},
+    {0, 384, 512, "softmax_warp<f32,V32,G32,NV2,T256,M3,P2>"},
+    {1, 64, 128, "softmax_warp<f16,V16,G8,NV2,T256,M6,P4>"},
+    {1, 128, 256, "softmax_warp<f16,V16,G8,NV4,T256,M4,P4>"},
+    {1, 256, 320, "softmax_warp<f16,V16,G8,NV5,T256,M4,P4>"},
+    {1, 320, 384, "softmax_warp<f16,V32,G8,NV3,T256,M3,P4>"},
+    {2, 64, 128, "softmax_warp<bf16,V16,G8,NV2,T256,M6,P4>"},
+    {2, 128, 256, "softmax_warp<bf16,V16,G8,NV4,T256,M4,P4>"},
+    {2, 256, 320, "softmax_warp<bf16,V16,G8,NV5,T256,M4,P4>"},
+    {2, 320, 384, "softmax_warp<bf16,V32,G8,NV3,T256,M3,P4>"},
 };
 
 const SoftmaxTier* pick_dtype(int dtype, int64_t Sk) {
@@ -628,10 +641,20 @@ const SoftmaxTier* pick_dtype(int dtype, int64_t Sk) {
     if (!t) return nullptr;
     const int f = g_force[dtype].load(std::memory_order_relaxed);
     if (f >= 0 && f < kSmN && Sk <= t[f].max_cols) return &t[f];
-    for (const Pref& pr : kSmPref) {
+    // name -> tier index, resolved once per entry (benign race: same value)
+    constexpr int NP = (int)(sizeof(kSmPref) / sizeof(kSmPref[0]));
+    static std::atomic<int> pidx[NP];
+    for (int p = 0; p < NP; ++p) {
+        const Pref& pr = kSmPref[p];
         if (pr.dtype != dtype || Sk <= pr.min_cols || Sk > pr.max_cols) continue;
-        for (int i = 0; i < kSmN; ++i)
-            if (!strcmp(t[i].name, pr.name) && Sk <= t[i].max_cols) return &t[i];
+        int k = pidx[p].load(std::memory_order_relaxed);
+        if (k == 0) {
+            k = -1;
+            for (int i = 0; i < kSmN; ++i)
+                if (!strcmp(t[i].name, pr.name)) k = i + 1;
+            pidx[p].store(k, std::memory_order_relaxed);
+        }
+        if (k > 0 && Sk <= t[k - 1].max_cols) return &t[k - 1];
     }
     for (int i = 0; i < kSmN; ++i)
         if (t[i].automatic && Sk <= t[i].max_cols) return &t[i];
