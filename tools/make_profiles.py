@@ -94,6 +94,24 @@ def main():
             "# tools/tune.py sweeps (GB/s algorithmic, CUDA events, inputs > 4x L2); * = automatic tier\n"
             + tune)
     shutil.copy(os.path.join(OUT, "bench.json"), os.path.join(PROF, f"{rnd}_bench.json"))
+    for src, dst, title in (("sweep.jsonl", f"{rnd}_sweep.txt", "tools/sweep.py"),
+                            ("sweep_next2.jsonl", f"{rnd}_sweep_next2.txt",
+                             "tools/sweep.py --next2 (NEXT-2 kernels)")):
+        p = os.path.join(OUT, src)
+        if not os.path.exists(p):
+            continue
+        rows = [json.loads(l) for l in open(p) if l.strip()]
+        out = [f"# {title}: device time per call (CUDA-graph replay), algorithmic GB/s, "
+               "% of the measured copy peak; ref = same-traffic torch kernel in the same mode"]
+        for r in rows:
+            if "op" not in r:
+                out.append("# " + json.dumps(r))
+                continue
+            ref = r.get("copy_same_bytes_us") or r.get("torch_add_same_traffic_us")
+            out.append(f"{r['config']:14s} {r['op']:19s} {r['dtype']:4s} {str(r['shape']):22s} "
+                       f"{'ragged' if r['ragged'] else 'full  '} {r['us']:9.2f} us "
+                       f"{r['GBps']:8.1f} GB/s {r['pct_peak']:5.1f}%  ref {ref} us  {r['tier']}")
+        open(os.path.join(PROF, dst), "w").write("\n".join(out) + "\n")
     print("\n".join(lines))
 
 
