@@ -63,9 +63,11 @@ def _load():
             lib.tto_split_qkv_add_bias.argtypes = [_vp, _vp, ctypes.c_int, _i64, _i64, _i64,
                                                    _i64, _vp]
             lib.tto_merge_heads.argtypes = [_vp, ctypes.c_int, _i64, _i64, _i64, _i64, _vp]
+            lib.tto_attention.argtypes = [_vp, _vp, _vp, ctypes.c_int, _vp, _i64, _i64, _i64,
+                                          _i64, ctypes.c_float, _vp]
             for f in (lib.tto_widen, lib.tto_softmax_masked, lib.tto_add_bias_layernorm,
                       lib.tto_layernorm_onepass_eq1, lib.tto_add_bias_gelu,
-                      lib.tto_split_qkv_add_bias, lib.tto_merge_heads):
+                      lib.tto_split_qkv_add_bias, lib.tto_merge_heads, lib.tto_attention):
                 f.restype = ctypes.c_int
             _lib = lib
     return _lib
@@ -202,6 +204,25 @@ def merge_heads(x, B: int, S: int, H: int, D: int) -> torch.Tensor:
         raise ValueError("shape mismatch")
     out = torch.empty((B * S, H * D), dtype=torch.float64)
     rc = _load().tto_merge_heads(_ptr(xs), DTYPE_CODE[xs.dtype], B, S, H, D, _ptr(out))
+    assert rc == 0
+    return out
+
+
+def attention(q, k, v, lengths, scale: float) -> torch.Tensor:
+    """NEXT-3: o = softmax_masked(scale * q k^T) v per (b, h), [B, H, S, D] float64;
+    keys j >= clamp(lengths[b], 0, S) masked, o = 0 for an empty request."""
+    qs, ks, vs = _host(q), _host(k), _host(v)
+    if not (qs.shape == ks.shape == vs.shape) or qs.dim() != 4:
+        raise ValueError("q, k, v must share one [B, H, S, D] shape")
+    if not (qs.dtype == ks.dtype == vs.dtype):
+        raise TypeError("q, k, v share one dtype")
+    B, H, S, D = qs.shape
+    lens = torch.as_tensor(np.asarray(lengths, dtype=np.int32)).contiguous()
+    if lens.numel() != B:
+        raise ValueError("lengths must have B entries")
+    out = torch.empty((B, H, S, D), dtype=torch.float64)
+    rc = _load().tto_attention(_ptr(qs), _ptr(ks), _ptr(vs), DTYPE_CODE[qs.dtype], _ptr(lens),
+                               B, H, S, D, ctypes.c_float(scale), _ptr(out))
     assert rc == 0
     return out
 

@@ -28,6 +28,7 @@
  */
 #include <math.h>
 #include <stdint.h>
+#include <stdlib.h>
 #include <string.h>
 
 #define TTO_F32 0
@@ -280,5 +281,56 @@ int tto_merge_heads(const void* in, int dtype, int64_t B, int64_t S, int64_t H, 
                 for (int64_t d = 0; d < D; ++d)
                     out[((b * S + s) * H + h) * D + d] =
                         load_elem(in, dtype, ((b * H + h) * S + s) * D + d);
+    return 0;
+}
+
+/* ---------------------------------------------------------------------------
+ * NEXT-3: the attention the masked softmax sits in (PAPER.md
+ * l.179-182: "the scaled dot-product attention computes the dot products of the
+ * query with all keys, and applies a Softmax function to obtain the weights on
+ * the values"), with the padding mask of tto_softmax_masked:
+ *   q, k, v: [B, H, S, D]; lengths int32[B]; L_b = clamp(lengths[b], 0, S)
+ *   p_ij = softmax_j(scale * q_i . k_j) over j < L_b  (tto_softmax_masked)
+ *   o_i  = sum_{j < L_b} p_ij v_j                       (o_i = 0 when L_b = 0)
+ * out: double [B, H, S, D]. */
+int tto_attention(const void* q, const void* k, const void* v, int dtype,
+                  const int32_t* lengths, int64_t B, int64_t H, int64_t S, int64_t D,
+                  float scale, double* out) {
+    if (B < 0 || H < 0 || S < 0 || D < 0 || dtype < 0 || dtype > 2) return -1;
+    if (B * H * S * D == 0) return 0;
+    if (!q || !k || !v || !lengths || !out) return -1;
+    const double sc = (double)scale;
+    double* z = (double*)malloc(sizeof(double) * (size_t)S);
+    if (!z) return -1;
+    for (int64_t b = 0; b < B; ++b) {
+        int64_t L = lengths[b];
+        if (L < 0) L = 0;
+        if (L > S) L = S;
+        for (int64_t h = 0; h < H; ++h) {
+            const int64_t base = (b * H + h) * S * D;
+            for (int64_t i = 0; i < S; ++i) {
+                double* o = out + base + i * D;
+                for (int64_t d = 0; d < D; ++d) o[d] = 0.0;
+                if (L == 0) continue;
+                double m = -INFINITY;
+                for (int64_t j = 0; j < L; ++j) {
+                    double dot = 0.0;
+                    for (int64_t d = 0; d < D; ++d)
+                        dot += load_elem(q, dtype, base + i * D + d) *
+                               load_elem(k, dtype, base + j * D + d);
+                    z[j] = sc * dot;
+                    if (z[j] > m) m = z[j];
+                }
+                double s = 0.0;
+                for (int64_t j = 0; j < L; ++j) s += exp(z[j] - m);
+                for (int64_t j = 0; j < L; ++j) {
+                    const double p = exp(z[j] - m) / s;
+                    for (int64_t d = 0; d < D; ++d)
+                        o[d] += p * load_elem(v, dtype, base + j * D + d);
+                }
+            }
+        }
+    }
+    free(z);
     return 0;
 }
