@@ -178,6 +178,26 @@ TT_API tt_status tt_merge_heads(int dtype, void* out, const void* in, int64_t B,
                                 int64_t H, int64_t D, cudaStream_t stream);
 
 /* ------------------------------------------------------------------------
+ * NEXT-3: the masked softmax fused into its GEMMs, on the
+ * tcgen05 tensor cores -- "the scaled dot-product attention computes the dot
+ * products of the query with all keys, and applies a Softmax function to
+ * obtain the weights on the values":
+ *   out[b,h,i,:] = sum_{j < L_b} softmax_j(scale * q[b,h,i,:] . k[b,h,j,:]) v[b,h,j,:]
+ * with L_b = clamp(lengths[b], 0, S) (the padding mask of tt_softmax_masked);
+ * out rows are 0 when L_b = 0.  The [B,H,S,S] scores never reach HBM.
+ *
+ * q, k, v, out  DEVICE [B, H, S, D] row-major (the layout tt_split_qkv_add_bias
+ *               produces), dtype 1 = fp16 or 2 = bf16 (fp32 accumulation;
+ *               the probabilities enter the second GEMM rounded to the storage
+ *               dtype, as in flash attention).  16-byte aligned bases.
+ * lengths       DEVICE int32[B].   D must be 64 (BERT), else NOT_SUPPORTED.
+ * out must not overlap q, k or v.
+ * ---------------------------------------------------------------------- */
+TT_API tt_status tt_attention_fwd(int dtype, void* out, const void* q, const void* k,
+                                  const void* v, const int32_t* lengths, int64_t B, int64_t H,
+                                  int64_t S, int64_t D, float scale, cudaStream_t stream);
+
+/* ------------------------------------------------------------------------
  * Staged (host-buffer) variants: the end-to-end serving call.  On `stream`:
  * copy the HOST inputs into the caller's DEVICE buffers, run the kernel, copy
  * the result back into the HOST buffer.  Host buffers should be pinned

@@ -35,7 +35,7 @@ EXPORTS = (
     "tt_softmax_masked_plan", "tt_add_bias_layernorm_plan", "tt_softmax_packed_plan",
     "ttx_tier_count", "ttx_tier_name", "ttx_force_tier",
     "tt_add_bias_gelu", "tt_split_qkv_add_bias", "tt_merge_heads",
-    "tt_dp_schedule", "tt_schedule_cost",
+    "tt_dp_schedule", "tt_schedule_cost", "tt_attention_fwd",
 )
 
 
@@ -81,6 +81,8 @@ def lib() -> ctypes.CDLL:
             L.tt_split_qkv_add_bias.argtypes = [_i, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64,
                                                 _i64, _vp]
             L.tt_merge_heads.argtypes = [_i, _vp, _vp, _i64, _i64, _i64, _i64, _vp]
+            L.tt_attention_fwd.argtypes = [_i, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _i64,
+                                           _f, _vp]
             L.tt_dp_schedule.argtypes = [_vp, _i64, _vp, _i64, _i64, _vp, _vp, _vp, _vp]
             L.tt_schedule_cost.argtypes = [_vp, _i64, _vp, _i64, _i64, _vp, _vp, _i64, _vp]
             L.ttx_tier_count.argtypes = [_i]
@@ -302,6 +304,23 @@ def tt_merge_heads(out, x, B: int, S: int, H: int, D: int, stream=None):
         raise ValueError("shape mismatch")
     _check(lib().tt_merge_heads(DTYPE_CODE[x.dtype], out.data_ptr(), x.data_ptr(), B, S, H, D,
                                 _stream_ptr(stream)), "tt_merge_heads")
+    return out
+
+
+# ------------------------------------------------------------------ attention
+def tt_attention_fwd(out, q, k, v, lengths, scale: float, stream=None):
+    """NEXT-3: out <- softmax_masked(scale * q k^T) v on tcgen05 (tt_attention_fwd);
+    q, k, v, out [B, H, S, 64] fp16/bf16, lengths int32[B] on the device."""
+    for t, nm in ((out, "out"), (q, "q"), (k, "k"), (v, "v"), (lengths, "lengths")):
+        _dev(t, nm)
+    if not (q.shape == k.shape == v.shape == out.shape) or q.dim() != 4:
+        raise ValueError("q, k, v, out must share one [B, H, S, D] shape")
+    if not (q.dtype == k.dtype == v.dtype == out.dtype) or lengths.dtype != torch.int32:
+        raise ValueError("dtype mismatch")
+    B, H, S, D = q.shape
+    _check(lib().tt_attention_fwd(DTYPE_CODE[q.dtype], out.data_ptr(), q.data_ptr(),
+                                  k.data_ptr(), v.data_ptr(), lengths.data_ptr(), B, H, S, D,
+                                  float(scale), _stream_ptr(stream)), "tt_attention_fwd")
     return out
 
 

@@ -21,7 +21,7 @@ INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(PKG, "libtt.so")
 BUILD_DIR = os.path.join(PKG, "_build")
 SOURCES = ["tt_api.cu", "softmax.cu", "softmax_packed.cu", "layernorm.cu", "elementwise.cu",
-           "scheduler.cpp"]
+           "scheduler.cpp", "attention.cu"]
 HEADERS = ["common.cuh", "launch.h", "softmax_row.cuh"]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

@@ -1,0 +1,351 @@
+// attention.cu -- NEXT-3: the masked softmax fused into its two
+// GEMMs, o = softmax_masked(scale * q k^T) v, on the 5th-generation tensor
+// cores (tcgen05.mma, accumulators in TMEM).  The [B, H, S, S] score tensor
+// never reaches HBM (PAPER.md l.179-182 for the attention, l.302 for "fusing
+// all the kernels between two GEMM kernels").
+//
+// One CTA = 128 query rows of one (b, h); 4 warps, thread t owns query row t
+// (TMEM lane t).  Per 128-key tile:
+//   1. K / V tiles arrive in shared memory by cp.async (16-byte chunks written
+//      in the SWIZZLE_128B layout UMMA reads), double-buffered; keys >= L_b are
+//      zero-filled, never read (masked keys cannot inject NaN into the MMA).
+//   2. one thread issues S = Q K^T: 4 x tcgen05.mma M128 N128 K16 (bf16/f16 in,
+//      fp32 out) into TMEM columns [0, 128); tcgen05.commit -> mbarrier.
+//   3. every thread tcgen05.ld's its row of S, masks keys >= L_b, runs the online
+//      max / exp2 / sum in registers (no shuffles: a row is one thread) and
+//      writes P (16-bit) into shared memory, again in the UMMA layout.
+//   4. one thread issues O_tile = P V: 8 x tcgen05.mma M128 N64 K16 (V as an
+//      MN-major operand) into TMEM columns [128, 192); each thread then folds
+//      O_tile into its register accumulator O = O * alpha + O_tile.
+// Finally o = O / l, narrowed, stored row-per-thread.  Head dim D = 64.
+#include <atomic>
+#include <type_traits>
+
+#include "common.cuh"
+#include "launch.h"
+
+namespace tt {
+
+namespace {
+
+constexpr int kBM = 128, kBN = 128, kD = 64, kNT = 128;
+constexpr int kTile = kBM * kD * 2;  // 16 KB: 128 rows x 128 B
+
+// ---- PTX wrappers (tcgen05 / cp.async) -------------------------------------
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint32_t src_bytes) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src),
+                 "r"(src_bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+    asm volatile("cp.async.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_mma(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
+                                       uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+    asm volatile(
+        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+            smem_u32(bar))
+        : "memory");
+}
+// 32 consecutive TMEM columns of this thread's lane
+__device__ __forceinline__ void tc_ld32(uint32_t taddr, float (&v)[32]) {
+    uint32_t r[32];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+        "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+          "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]),
+          "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+          "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),
+          "=r"(r[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// bounded wait: a fault in the async units traps instead of hanging the GPU
+__device__ __forceinline__ void mbar_wait_bounded(uint64_t* bar, uint32_t parity) {
+    uint32_t done = 0, spins = 0;
+    while (true) {
+        asm volatile(
+            "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+            "selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(done)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+        if (done) return;
+        if (++spins > (1u << 26)) __trap();
+    }
+}
+
+// SWIZZLE_128B shared-memory matrix descriptor (version 1, base offset 0):
+// start >> 4 in [0,14), LBO >> 4 in [16,30), SBO >> 4 in [32,46), layout in [61,64)
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+    return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
+           ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46) | (2ull << 61);
+}
+
+// instruction descriptor, kind::f16: fp32 accumulate, A/B format (0 f16, 1 bf16),
+// A K-major, B K- or MN-major, N >> 3 at [17,23), M >> 4 at [24,29)
+__host__ __device__ constexpr uint32_t f16_idesc(int ab_fmt, int b_mn_major, int M, int N) {
+    return (1u << 4) | ((uint32_t)ab_fmt << 7) | ((uint32_t)ab_fmt << 10) |
+           ((uint32_t)b_mn_major << 16) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+// tile row r (128 B = 64 x 16-bit), 16-byte chunk c -> swizzled smem offset
+__device__ __forceinline__ uint32_t sw_off(int r, int c) {
+    return (uint32_t)((r >> 3) * 1024 + (r & 7) * 128 + ((c ^ (r & 7)) << 4));
+}
+
+// rows [row0, row0 + 128) of a [S, 64] 16-bit matrix into a swizzled tile;
+// rows >= valid are zero-filled without reading global memory
+template <typename T>
+__device__ __forceinline__ void load_tile(uint32_t tile, const T* g, int row0, int valid) {
+#pragma unroll
+    for (int i = 0; i < (kBM * 8) / kNT; ++i) {
+        const int idx = threadIdx.x + i * kNT;
+        const int r = idx >> 3, c = idx & 7;
+        const bool in = row0 + r < valid;
+        const T* src = g + (size_t)(in ? row0 + r : 0) * kD + c * 8;
+        cp_async16(tile + sw_off(r, c), src, in ? 16u : 0u);
+    }
+}
+
+}  // namespace
+
+template <typename T>
+__global__ void __launch_bounds__(kNT, 1)
+    attention_tc_kernel(T* __restrict__ out, const T* __restrict__ q, const T* __restrict__ k,
+                        const T* __restrict__ v, const int32_t* __restrict__ lengths, int H,
+                        int S, float c) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    // 1024-aligned carve-up: Q | K0 K1 | V0 V1 | P0 P1 | barriers + TMEM slot
+    const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;
+    unsigned char* sbase = smem_raw + (base - smem_u32(smem_raw));
+    const uint32_t sQ = base, sK = base + kTile, sV = base + 3 * kTile, sP = base + 5 * kTile;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sbase + 7 * kTile);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sbase + 7 * kTile + 16);
+
+    const int qt = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    const int L = min(max(__ldg(lengths + b), 0), S);
+    const size_t head = ((size_t)b * H + h) * (size_t)S * kD;
+    const int row = qt * kBM + tid;  // this thread's query row
+
+    if (L == 0) {  // no valid key: the output rows are zero
+        if (row < S) {
+            uint4 z = make_uint4(0, 0, 0, 0);
+#pragma unroll
+            for (int i = 0; i < kD * 2 / 16; ++i)
+                reinterpret_cast<uint4*>(out + head + (size_t)row * kD)[i] = z;
+        }
+        return;
+    }
+
+    if (warp == 0) {  // TMEM: S in columns [0,128), O tile in [128,192)
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(
+                         smem_u32(tmem_slot))
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    if (tid == 0) {
+        mbar_init(&bars[0], 1);
+        mbar_init(&bars[1], 1);
+        fence_mbar_init();
+    }
+    const int nkt = (L + kBN - 1) / kBN;
+    load_tile<T>(sQ, q + head, qt * kBM, S);
+    load_tile<T>(sK, k + head, 0, L);
+    load_tile<T>(sV, v + head, 0, L);
+    cp_async_commit();
+    if (nkt > 1) {
+        load_tile<T>(sK + kTile, k + head, kBN, L);
+        load_tile<T>(sV + kTile, v + head, kBN, L);
+    }
+    cp_async_commit();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    const uint32_t t_s = tmem, t_o = tmem + 128;
+    const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
+
+    constexpr int kFmt = sizeof(T) == 2 && std::is_same<T, __nv_bfloat16>::value ? 1 : 0;
+    constexpr uint32_t idesc_s = f16_idesc(kFmt, 0, kBM, kBN);
+    constexpr uint32_t idesc_o = f16_idesc(kFmt, 1, kBM, kD);
+
+    float o[kD];
+#pragma unroll
+    for (int i = 0; i < kD; ++i) o[i] = 0.f;
+    float m_run = -INFINITY, l_run = 0.f;
+    uint32_t ph_s = 0, ph_o = 0;
+
+    for (int kt = 0; kt < nkt; ++kt) {
+        const int st = kt & 1;
+        if (kt + 1 < nkt)
+            cp_async_wait<1>();
+        else
+            cp_async_wait<0>();
+        fence_proxy_async_smem();  // cp.async writes -> visible to the tensor core (async proxy)
+        tc_fence_before();
+        __syncthreads();
+        tc_fence_after();
+
+        // ---- S = Q K^T (K-major A and B, 4 K-steps of 16)
+        if (tid == 0) {
+            const uint32_t kbase = sK + st * kTile;
+#pragma unroll
+            for (int ks = 0; ks < kD / 16; ++ks)
+                tc_mma(t_s, sw128_desc(sQ + ks * 32, 16, 1024),
+                       sw128_desc(kbase + ks * 32, 16, 1024), idesc_s, ks > 0);
+            tc_commit(&bars[0]);
+        }
+        mbar_wait_bounded(&bars[0], ph_s);
+        ph_s ^= 1;
+        tc_fence_after();
+
+        // ---- online softmax on this thread's row of S
+        const int key0 = kt * kBN;
+        float tmax = -INFINITY;
+#pragma unroll
+        for (int ch = 0; ch < 4; ++ch) {
+            float sv[32];
+            tc_ld32(t_s + lane_off + ch * 32, sv);
+#pragma unroll
+            for (int e = 0; e < 32; ++e) {
+                const float t = (key0 + ch * 32 + e < L) ? sv[e] * c : -INFINITY;
+                tmax = fmaxf(tmax, t);
+            }
+        }
+        const float m_new = fmaxf(m_run, tmax);
+        const float alpha = ex2_approx(m_run - m_new);  // m_run = -inf -> 0
+        float psum = 0.f;
+        unsigned char* prow = sbase + (sP - base);
+#pragma unroll
+        for (int ch = 0; ch < 4; ++ch) {
+            float sv[32];
+            tc_ld32(t_s + lane_off + ch * 32, sv);
+            float p[32];
+#pragma unroll
+            for (int e = 0; e < 32; ++e) {
+                p[e] = (key0 + ch * 32 + e < L) ? ex2_approx(sv[e] * c - m_new) : 0.f;
+                psum += p[e];
+            }
+            // keys ch*32 .. ch*32+31 -> P half (ch / 2), 16-byte chunks (ch % 2) * 4 + j
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                Raw<16> w;
+                Elem<T>::template pack<16>(p + 8 * j, w);
+                const uint32_t off = (uint32_t)(ch >> 1) * kTile + sw_off(tid, (ch & 1) * 4 + j);
+                *reinterpret_cast<uint4*>(prow + off) = make_uint4(w.w[0], w.w[1], w.w[2], w.w[3]);
+            }
+        }
+        l_run = l_run * alpha + psum;
+        m_run = m_new;
+        fence_proxy_async_smem();  // P (generic stores) -> tensor core
+        tc_fence_before();
+        __syncthreads();
+        tc_fence_after();
+
+        // ---- O_tile = P V (P K-major; V MN-major: 16 keys = 2048 B per K-step)
+        if (tid == 0) {
+            const uint32_t vbase = sV + st * kTile;
+#pragma unroll
+            for (int ks = 0; ks < kBN / 16; ++ks)
+                tc_mma(t_o, sw128_desc(sP + (ks >> 2) * kTile + (ks & 3) * 32, 16, 1024),
+                       sw128_desc(vbase + ks * 2048, 16384, 1024), idesc_o, ks > 0);
+            tc_commit(&bars[1]);
+        }
+        mbar_wait_bounded(&bars[1], ph_o);
+        ph_o ^= 1;
+        tc_fence_after();
+#pragma unroll
+        for (int ch = 0; ch < 2; ++ch) {
+            float ov[32];
+            tc_ld32(t_o + lane_off + ch * 32, ov);
+#pragma unroll
+            for (int e = 0; e < 32; ++e) o[ch * 32 + e] = fmaf(o[ch * 32 + e], alpha, ov[e]);
+        }
+        // stage st is free again: prefetch tile kt + 2 into it
+        if (kt + 2 < nkt) {
+            __syncthreads();
+            load_tile<T>(sK + st * kTile, k + head, (kt + 2) * kBN, L);
+            load_tile<T>(sV + st * kTile, v + head, (kt + 2) * kBN, L);
+        }
+        cp_async_commit();
+    }
+
+    // ---- o = O / l, narrowed, one 128-byte row per thread
+    if (row < S) {
+        const float inv = 1.0f / l_run;
+        T* orow = out + head + (size_t)row * kD;
+#pragma unroll
+        for (int j = 0; j < kD / 8; ++j) {
+            float y[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) y[e] = o[8 * j + e] * inv;
+            Raw<16> w;
+            Elem<T>::template pack<16>(y, w);
+            reinterpret_cast<uint4*>(orow)[j] = make_uint4(w.w[0], w.w[1], w.w[2], w.w[3]);
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem)
+                     : "memory");
+    }
+}
+
+namespace {
+constexpr size_t kSmem = 7 * kTile + 64 + 1024;
+
+template <typename T>
+cudaError_t launch_attn(void* out, const void* q, const void* k, const void* v,
+                        const int32_t* lengths, int64_t B, int64_t H, int64_t S, float scale,
+                        cudaStream_t st) {
+    static std::atomic<int> attr{0};
+    if (!attr.load()) {
+        cudaError_t e = cudaFuncSetAttribute(attention_tc_kernel<T>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)kSmem);
+        if (e != cudaSuccess) return e;
+        attr.store(1);
+    }
+    dim3 grid((unsigned)((S + kBM - 1) / kBM), (unsigned)H, (unsigned)B);
+    attention_tc_kernel<T><<<grid, kNT, kSmem, st>>>(
+        static_cast<T*>(out), static_cast<const T*>(q), static_cast<const T*>(k),
+        static_cast<const T*>(v), lengths, (int)H, (int)S, scale * 1.4426950408889634f);
+    return cudaGetLastError();
+}
+}  // namespace
+
+cudaError_t attention_launch(int dtype, void* out, const void* q, const void* k, const void* v,
+                             const int32_t* lengths, int64_t B, int64_t H, int64_t S,
+                             float scale, cudaStream_t stream) {
+    if (dtype == 1)
+        return launch_attn<__half>(out, q, k, v, lengths, B, H, S, scale, stream);
+    return launch_attn<__nv_bfloat16>(out, q, k, v, lengths, B, H, S, scale, stream);
+}
+
+}  // namespace tt

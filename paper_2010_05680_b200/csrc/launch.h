@@ -41,6 +41,11 @@ cudaError_t split_qkv_launch(int dtype, void* q, void* k, void* v, const void* q
 cudaError_t merge_heads_launch(int dtype, void* out, const void* in, int64_t B, int64_t S,
                                int64_t H, int64_t D, int vec_bytes, cudaStream_t stream);
 
+// NEXT-3 fused attention on tcgen05 (attention.cu); dtype 1 = fp16, 2 = bf16, D = 64
+cudaError_t attention_launch(int dtype, void* out, const void* q, const void* k, const void* v,
+                             const int32_t* lengths, int64_t B, int64_t H, int64_t S,
+                             float scale, cudaStream_t stream);
+
 // Tuning / test hooks (include/tt_tune.h): enumerate every compiled tier and
 // force one (-1 = automatic selection).  A forced tier that cannot serve the
 // call's shape is ignored.

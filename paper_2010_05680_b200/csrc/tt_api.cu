@@ -213,6 +213,29 @@ tt_status merge_any(int dtype, void* out, const void* in, int64_t B, int64_t S, 
     return cuda_status(tt::merge_heads_launch(dtype, out, in, B, S, H, D, vb, stream));
 }
 
+tt_status attention_any(int dtype, void* out, const void* q, const void* k, const void* v,
+                        const int32_t* lengths, int64_t B, int64_t H, int64_t S, int64_t D,
+                        float scale, cudaStream_t stream) {
+    if (dtype < 0 || dtype > 2 || B < 0 || H < 0 || S < 0 || D < 0 || !isfinite(scale))
+        return TT_ERROR_INVALID_VALUE;
+    int64_t bh, n, nb;
+    if (mul_overflows(B, H, &bh) || mul_overflows(bh, S, &n) || mul_overflows(n, D, &n) ||
+        mul_overflows(n, elem_bytes(dtype), &nb))
+        return TT_ERROR_INVALID_VALUE;
+    if (n == 0) return TT_SUCCESS;
+    if (!out || !q || !k || !v || !lengths) return TT_ERROR_INVALID_VALUE;
+    const void* ins[3] = {q, k, v};
+    for (const void* p : ins)
+        if (overlaps(out, nb, p, nb)) return TT_ERROR_INVALID_VALUE;
+    if (dtype == 0 || D != 64) return TT_ERROR_NOT_SUPPORTED;
+    const void* ps[4] = {out, q, k, v};
+    for (const void* p : ps)
+        if (!aligned16(p)) return TT_ERROR_NOT_SUPPORTED;
+    if (reinterpret_cast<uintptr_t>(lengths) & 3u) return TT_ERROR_NOT_SUPPORTED;
+    if (B > 65535 || H > 65535 || S > 0x7fffffffLL) return TT_ERROR_NOT_SUPPORTED;
+    return cuda_status(tt::attention_launch(dtype, out, q, k, v, lengths, B, H, S, scale, stream));
+}
+
 // ------------------------------------------------------------------- packed
 tt_status packed_validate(int dtype, const void* scores, const int32_t* cu, const int64_t* blocks,
                           int64_t num_req, int64_t H, int64_t total_tokens, int64_t max_len,
@@ -306,6 +329,12 @@ tt_status tt_add_bias_layernorm_bf16(void* out, const void* x, const void* resid
                                      const void* bias, const void* gamma, const void* beta,
                                      int64_t rows, int64_t hidden, float eps, cudaStream_t stream) {
     return ln_any(2, out, x, residual, bias, gamma, beta, rows, hidden, eps, stream);
+}
+
+tt_status tt_attention_fwd(int dtype, void* out, const void* q, const void* k, const void* v,
+                           const int32_t* lengths, int64_t B, int64_t H, int64_t S, int64_t D,
+                           float scale, cudaStream_t stream) {
+    return attention_any(dtype, out, q, k, v, lengths, B, H, S, D, scale, stream);
 }
 
 tt_status tt_add_bias_gelu(int dtype, void* out, const void* x, const void* bias, int64_t rows,

@@ -1,0 +1,75 @@
+"""GPU parity: tt_attention_fwd (NEXT-3, tcgen05 fused attention) vs the fp64
+attention oracle.  Tolerance (DESIGN R20): |g - r| <= 8e-3 * max(1, |r|) for
+bf16 and 4e-3 * max(1, |r|) for fp16 -- the probabilities enter the P.V GEMM
+rounded to the storage dtype (flash-attention practice), on top of the
+output's own rounding."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import workloads as W
+
+pytestmark = pytest.mark.gpu
+DT = [torch.float16, torch.bfloat16]
+TOL = {torch.float16: 4e-3, torch.bfloat16: 8e-3}
+
+
+def _qkv(B, H, S, D, dtype, seed, std=1.0):
+    g = torch.Generator().manual_seed(seed)
+    return [(torch.randn(B, H, S, D, generator=g) * std).to(dtype) for _ in range(3)]
+
+
+def _run(tt, q, k, v, lens, scale):
+    out = torch.empty_like(q, device="cuda")
+    tt.tt_attention_fwd(out, q.cuda(), k.cuda(), v.cuda(),
+                        torch.as_tensor(np.asarray(lens, dtype=np.int32)).cuda(), scale)
+    torch.cuda.synchronize()
+    return out.cpu()
+
+
+def _check(dtype, got, ref, what):
+    g, r = got.double(), ref
+    err = (g - r).abs()
+    bound = TOL[dtype] * torch.maximum(torch.ones_like(r), r.abs())
+    bad = ~(err <= bound)
+    assert not bad.any(), f"{what}: {int(bad.sum())} bad, max err {err.max().item():.3e}"
+
+
+@pytest.mark.parametrize("dtype", DT)
+@pytest.mark.parametrize("S,lens", [(128, [128]), (40, [40, 17]), (256, [256, 200, 129, 1]),
+                                    (512, [512, 300]), (300, [300, 0, 255])])
+def test_attention_parity(ttlib, dtype, S, lens):
+    B, H, D = len(lens), 2, 64
+    q, k, v = _qkv(B, H, S, D, dtype, S + B)
+    got = _run(ttlib, q, k, v, lens, 0.125)
+    _check(dtype, got, oracle.attention(q, k, v, lens, 0.125), f"S={S} lens={lens}")
+
+
+@pytest.mark.parametrize("dtype", DT)
+def test_attention_bert_base_shape_and_poison(ttlib, dtype):
+    """BERT-base (12 heads, d 64), ragged C2-style lengths; NaN/Inf in the masked
+    keys / values must not leak into any output."""
+    B, H, S, D = 4, 12, 100, 64
+    lens = [100, 37, 64, 1]
+    q, k, v = _qkv(B, H, S, D, dtype, 7)
+    k2, v2 = k.clone(), v.clone()
+    for b, L in enumerate(lens):
+        k2[b, :, L:] = float("nan")
+        v2[b, :, L:] = float("inf")
+    got = _run(ttlib, q, k2, v2, lens, 0.125)
+    _check(dtype, got, oracle.attention(q, k, v, lens, 0.125), "bert-base poison")
+
+
+def test_attention_deterministic(ttlib):
+    q, k, v = _qkv(2, 3, 200, 64, torch.bfloat16, 9)
+    a = _run(ttlib, q, k, v, [200, 150], 0.125)
+    b = _run(ttlib, q, k, v, [200, 150], 0.125)
+    assert torch.equal(a.view(torch.int16), b.view(torch.int16))
+
+
+def test_attention_rejects_unsupported(ttlib):
+    q = torch.zeros(1, 1, 8, 32, dtype=torch.float16, device="cuda")
+    with pytest.raises(ttlib.TTError):
+        ttlib.tt_attention_fwd(torch.empty_like(q), q, q, q,
+                               torch.ones(1, dtype=torch.int32, device="cuda"), 1.0)
