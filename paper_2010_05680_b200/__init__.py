@@ -10,7 +10,8 @@ from ._lib import (  # noqa: F401
     tt_add_bias_layernorm, tt_add_bias_layernorm_raw, tt_add_bias_layernorm_staged,
     tt_softmax_masked, tt_softmax_masked_raw, tt_softmax_masked_staged, tiers, version,
     packed_offsets, tt_softmax_packed, softmax_packed_plan, tt_add_bias_gelu,
-    tt_split_qkv_add_bias, tt_merge_heads, dp_schedule, schedule_cost, tt_attention_fwd)
+    tt_split_qkv_add_bias, tt_merge_heads, dp_schedule, schedule_cost, tt_attention_fwd,
+    attention_variant)
 
 __all__ = [
     "tt_softmax_masked", "tt_softmax_packed", "packed_offsets", "tt_add_bias_layernorm", "tt_softmax_masked_staged",

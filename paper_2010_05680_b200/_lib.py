@@ -35,7 +35,7 @@ EXPORTS = (
     "tt_softmax_masked_plan", "tt_add_bias_layernorm_plan", "tt_softmax_packed_plan",
     "ttx_tier_count", "ttx_tier_name", "ttx_force_tier",
     "tt_add_bias_gelu", "tt_split_qkv_add_bias", "tt_merge_heads",
-    "tt_dp_schedule", "tt_schedule_cost", "tt_attention_fwd",
+    "tt_dp_schedule", "tt_schedule_cost", "tt_attention_fwd", "ttx_attention_variant",
 )
 
 
@@ -83,6 +83,7 @@ def lib() -> ctypes.CDLL:
             L.tt_merge_heads.argtypes = [_i, _vp, _vp, _i64, _i64, _i64, _i64, _vp]
             L.tt_attention_fwd.argtypes = [_i, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _i64,
                                            _f, _vp]
+            L.ttx_attention_variant.argtypes = [_i]
             L.tt_dp_schedule.argtypes = [_vp, _i64, _vp, _i64, _i64, _vp, _vp, _vp, _vp]
             L.tt_schedule_cost.argtypes = [_vp, _i64, _vp, _i64, _i64, _vp, _vp, _i64, _vp]
             L.ttx_tier_count.argtypes = [_i]
@@ -322,6 +323,11 @@ def tt_attention_fwd(out, q, k, v, lengths, scale: float, stream=None):
                                   k.data_ptr(), v.data_ptr(), lengths.data_ptr(), B, H, S, D,
                                   float(scale), _stream_ptr(stream)), "tt_attention_fwd")
     return out
+
+
+def attention_variant(v: int):
+    """0 = automatic, 1 = single-buffered K/V (2 CTAs/SM), 2 = double-buffered."""
+    _check(lib().ttx_attention_variant(int(v)), "ttx_attention_variant")
 
 
 # ------------------------------------------------------------------ scheduler

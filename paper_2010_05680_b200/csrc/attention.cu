@@ -132,18 +132,27 @@ __device__ __forceinline__ void load_tile(uint32_t tile, const T* g, int row0, i
 
 }  // namespace
 
-template <typename T>
-__global__ void __launch_bounds__(kNT, 1)
+// NBUF = 2: K / V double-buffered (112 KB smem, 1 CTA per SM);
+// NBUF = 1: single-buffered (80 KB, 2 CTAs per SM, so one CTA's softmax runs
+// while the other's MMAs and loads are in flight).
+template <int NBUF>
+constexpr size_t attn_smem() {
+    return (size_t)(3 + 2 * NBUF) * kTile + 64 + 1024;
+}
+
+template <typename T, int NBUF>
+__global__ void __launch_bounds__(kNT, 3 - NBUF)
     attention_tc_kernel(T* __restrict__ out, const T* __restrict__ q, const T* __restrict__ k,
                         const T* __restrict__ v, const int32_t* __restrict__ lengths, int H,
                         int S, float c) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
-    // 1024-aligned carve-up: Q | K0 K1 | V0 V1 | P0 P1 | barriers + TMEM slot
+    // 1024-aligned carve-up: Q | K[NBUF] | V[NBUF] | P0 P1 | barriers + TMEM slot
     const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;
     unsigned char* sbase = smem_raw + (base - smem_u32(smem_raw));
-    const uint32_t sQ = base, sK = base + kTile, sV = base + 3 * kTile, sP = base + 5 * kTile;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sbase + 7 * kTile);
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sbase + 7 * kTile + 16);
+    const uint32_t sQ = base, sK = base + kTile, sV = base + (1 + NBUF) * kTile,
+                   sP = base + (1 + 2 * NBUF) * kTile;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sbase + (3 + 2 * NBUF) * kTile);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sbase + (3 + 2 * NBUF) * kTile + 16);
 
     const int qt = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
     const int tid = threadIdx.x, warp = tid >> 5;
@@ -177,7 +186,7 @@ __global__ void __launch_bounds__(kNT, 1)
     load_tile<T>(sK, k + head, 0, L);
     load_tile<T>(sV, v + head, 0, L);
     cp_async_commit();
-    if (nkt > 1) {
+    if (NBUF == 2 && nkt > 1) {
         load_tile<T>(sK + kTile, k + head, kBN, L);
         load_tile<T>(sV + kTile, v + head, kBN, L);
     }
@@ -200,8 +209,8 @@ __global__ void __launch_bounds__(kNT, 1)
     uint32_t ph_s = 0, ph_o = 0;
 
     for (int kt = 0; kt < nkt; ++kt) {
-        const int st = kt & 1;
-        if (kt + 1 < nkt)
+        const int st = NBUF == 2 ? (kt & 1) : 0;
+        if (NBUF == 2 && kt + 1 < nkt)
             cp_async_wait<1>();
         else
             cp_async_wait<0>();
@@ -222,6 +231,10 @@ __global__ void __launch_bounds__(kNT, 1)
         mbar_wait_bounded(&bars[0], ph_s);
         ph_s ^= 1;
         tc_fence_after();
+        if (NBUF == 1 && kt + 1 < nkt) {  // K consumed: stream the next K tile in now
+            load_tile<T>(sK, k + head, (kt + 1) * kBN, L);
+            cp_async_commit();
+        }
 
         // ---- online softmax on this thread's row of S
         const int key0 = kt * kBN;
@@ -285,13 +298,17 @@ __global__ void __launch_bounds__(kNT, 1)
 #pragma unroll
             for (int e = 0; e < 32; ++e) o[ch * 32 + e] = fmaf(o[ch * 32 + e], alpha, ov[e]);
         }
-        // stage st is free again: prefetch tile kt + 2 into it
-        if (kt + 2 < nkt) {
-            __syncthreads();
-            load_tile<T>(sK + st * kTile, k + head, (kt + 2) * kBN, L);
-            load_tile<T>(sV + st * kTile, v + head, (kt + 2) * kBN, L);
+        if constexpr (NBUF == 2) {
+            // stage st is free again: prefetch tile kt + 2 into it
+            if (kt + 2 < nkt) {
+                load_tile<T>(sK + st * kTile, k + head, (kt + 2) * kBN, L);
+                load_tile<T>(sV + st * kTile, v + head, (kt + 2) * kBN, L);
+            }
+            cp_async_commit();
+        } else if (kt + 1 < nkt) {  // V consumed by the P.V MMA
+            load_tile<T>(sV, v + head, (kt + 1) * kBN, L);
+            cp_async_commit();
         }
-        cp_async_commit();
     }
 
     // ---- o = O / l, narrowed, one 128-byte row per thread
@@ -318,34 +335,50 @@ __global__ void __launch_bounds__(kNT, 1)
 }
 
 namespace {
-constexpr size_t kSmem = 7 * kTile + 64 + 1024;
+std::atomic<int> g_attn_nbuf{0};  // 0 = automatic (single-buffered, 2 CTAs / SM)
 
-template <typename T>
+template <typename T, int NBUF>
 cudaError_t launch_attn(void* out, const void* q, const void* k, const void* v,
                         const int32_t* lengths, int64_t B, int64_t H, int64_t S, float scale,
                         cudaStream_t st) {
+    constexpr size_t smem = attn_smem<NBUF>();
     static std::atomic<int> attr{0};
     if (!attr.load()) {
-        cudaError_t e = cudaFuncSetAttribute(attention_tc_kernel<T>,
+        cudaError_t e = cudaFuncSetAttribute(attention_tc_kernel<T, NBUF>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)kSmem);
+                                             (int)smem);
         if (e != cudaSuccess) return e;
         attr.store(1);
     }
     dim3 grid((unsigned)((S + kBM - 1) / kBM), (unsigned)H, (unsigned)B);
-    attention_tc_kernel<T><<<grid, kNT, kSmem, st>>>(
+    attention_tc_kernel<T, NBUF><<<grid, kNT, smem, st>>>(
         static_cast<T*>(out), static_cast<const T*>(q), static_cast<const T*>(k),
         static_cast<const T*>(v), lengths, (int)H, (int)S, scale * 1.4426950408889634f);
     return cudaGetLastError();
 }
+
+template <typename T>
+cudaError_t launch_attn_any(void* out, const void* q, const void* k, const void* v,
+                            const int32_t* lengths, int64_t B, int64_t H, int64_t S, float scale,
+                            cudaStream_t st) {
+    if (g_attn_nbuf.load(std::memory_order_relaxed) == 2)
+        return launch_attn<T, 2>(out, q, k, v, lengths, B, H, S, scale, st);
+    return launch_attn<T, 1>(out, q, k, v, lengths, B, H, S, scale, st);
+}
 }  // namespace
+
+bool attention_force_variant(int v) {
+    if (v < 0 || v > 2) return false;
+    g_attn_nbuf.store(v);
+    return true;
+}
 
 cudaError_t attention_launch(int dtype, void* out, const void* q, const void* k, const void* v,
                              const int32_t* lengths, int64_t B, int64_t H, int64_t S,
                              float scale, cudaStream_t stream) {
     if (dtype == 1)
-        return launch_attn<__half>(out, q, k, v, lengths, B, H, S, scale, stream);
-    return launch_attn<__nv_bfloat16>(out, q, k, v, lengths, B, H, S, scale, stream);
+        return launch_attn_any<__half>(out, q, k, v, lengths, B, H, S, scale, stream);
+    return launch_attn_any<__nv_bfloat16>(out, q, k, v, lengths, B, H, S, scale, stream);
 }
 
 }  // namespace tt

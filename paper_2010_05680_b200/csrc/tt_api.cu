@@ -467,6 +467,10 @@ const char* ttx_tier_name(int op, int dtype, int i) {
                    : op == 1 ? tt::layernorm_tier_name_at(dtype, i) : nullptr;
 }
 
+tt_status ttx_attention_variant(int v) {
+    return tt::attention_force_variant(v) ? TT_SUCCESS : TT_ERROR_INVALID_VALUE;
+}
+
 tt_status ttx_force_tier(int op, int dtype, int i) {
     bool ok = op == 0 ? tt::softmax_force_tier(dtype, i)
                       : op == 1 ? tt::layernorm_force_tier(dtype, i) : false;

@@ -15,6 +15,14 @@ DT = [torch.float16, torch.bfloat16]
 TOL = {torch.float16: 4e-3, torch.bfloat16: 8e-3}
 
 
+@pytest.fixture(params=[1, 2], ids=["nbuf1", "nbuf2"])
+def variant(ttlib, request):
+    """Both K/V buffering variants of the kernel (ttx_attention_variant)."""
+    ttlib.attention_variant(request.param)
+    yield request.param
+    ttlib.attention_variant(0)
+
+
 def _qkv(B, H, S, D, dtype, seed, std=1.0):
     g = torch.Generator().manual_seed(seed)
     return [(torch.randn(B, H, S, D, generator=g) * std).to(dtype) for _ in range(3)]
@@ -39,7 +47,7 @@ def _check(dtype, got, ref, what):
 @pytest.mark.parametrize("dtype", DT)
 @pytest.mark.parametrize("S,lens", [(128, [128]), (40, [40, 17]), (256, [256, 200, 129, 1]),
                                     (512, [512, 300]), (300, [300, 0, 255])])
-def test_attention_parity(ttlib, dtype, S, lens):
+def test_attention_parity(ttlib, variant, dtype, S, lens):
     B, H, D = len(lens), 2, 64
     q, k, v = _qkv(B, H, S, D, dtype, S + B)
     got = _run(ttlib, q, k, v, lens, 0.125)
@@ -47,7 +55,7 @@ def test_attention_parity(ttlib, dtype, S, lens):
 
 
 @pytest.mark.parametrize("dtype", DT)
-def test_attention_bert_base_shape_and_poison(ttlib, dtype):
+def test_attention_bert_base_shape_and_poison(ttlib, variant, dtype):
     """BERT-base (12 heads, d 64), ragged C2-style lengths; NaN/Inf in the masked
     keys / values must not leak into any output."""
     B, H, S, D = 4, 12, 100, 64
@@ -61,7 +69,7 @@ def test_attention_bert_base_shape_and_poison(ttlib, dtype):
     _check(dtype, got, oracle.attention(q, k, v, lens, 0.125), "bert-base poison")
 
 
-def test_attention_deterministic(ttlib):
+def test_attention_deterministic(ttlib, variant):
     q, k, v = _qkv(2, 3, 200, 64, torch.bfloat16, 9)
     a = _run(ttlib, q, k, v, [200, 150], 0.125)
     b = _run(ttlib, q, k, v, [200, 150], 0.125)
