@@ -191,7 +191,7 @@ __global__ void __launch_bounds__(NT, MINB) softmax_rows_kernel(T* __restrict__ 
 // ----------------------------------------------------------------------------
 // Rows [first, row_end) of this CTA, GC lanes per row, walked in warp-uniform
 // slabs (every lane of a warp runs the same number of passes).
-template <typename T, int VB, int GC, int NVC, int NT, bool ALIGNED, bool NARROW>
+template <typename T, int VB, int GC, int NVC, int NT, bool ALIGNED, bool NARROW, bool UP>
 __device__ __forceinline__ void softmax_cta_rows(T* __restrict__ scores,
                                                  const int32_t* __restrict__ lengths,
                                                  uint32_t first, uint32_t row_end, FastDivU32 rpb,
@@ -207,16 +207,16 @@ __device__ __forceinline__ void softmax_cta_rows(T* __restrict__ scores,
         const bool live = row < row_end;
         const int L = Lnext;
         if (!one_req && row + step < row_end) Lnext = len_of(row + step);
-        softmax_row_pass<T, VB, GC, NVC, ALIGNED, NARROW>(
+        softmax_row_pass<T, VB, GC, NVC, ALIGNED, NARROW, UP>(
             scores + (size_t)(live ? row : first) * (size_t)Sk, live, L, Sk, c, q);
     }
 }
 
-template <typename T, int VB, int G, int NV, int NT, int MINB, bool ALIGNED>
-__global__ void __launch_bounds__(NT, MINB) softmax_warp_kernel(T* __restrict__ scores,
-                                                                const int32_t* __restrict__ lengths,
-                                                                uint32_t nrows, FastDivU32 rpb,
-                                                                int Sk, float c, int rpg) {
+template <typename T, int VB, int G, int NV, int NT, bool ALIGNED, bool UP>
+__device__ __forceinline__ void softmax_warp_body(T* __restrict__ scores,
+                                                  const int32_t* __restrict__ lengths,
+                                                  uint32_t nrows, FastDivU32 rpb, int Sk, float c,
+                                                  int rpg) {
     constexpr int VE = VB / (int)sizeof(T);
     constexpr int GPB = NT / G;
     static_assert(G <= 32, "warp tier");
@@ -233,18 +233,29 @@ __global__ void __launch_bounds__(NT, MINB) softmax_warp_kernel(T* __restrict__ 
         constexpr bool ok4 = ALIGNED || 4 >= VE - 1, ok8 = ALIGNED || 8 >= VE - 1;
         if (one_req && Lcta < Sk) {
             if (ok4 && Lcta <= 4 * VE)
-                return softmax_cta_rows<T, VB, 4, 1, NT, ALIGNED, ok4>(
+                return softmax_cta_rows<T, VB, 4, 1, NT, ALIGNED, ok4, UP>(
                     scores, lengths, first, row_end, rpb, Sk, c, true, Lcta);
             if (ok8 && Lcta <= 8 * VE)
-                return softmax_cta_rows<T, VB, 8, 1, NT, ALIGNED, ok8>(
+                return softmax_cta_rows<T, VB, 8, 1, NT, ALIGNED, ok8, UP>(
                     scores, lengths, first, row_end, rpb, Sk, c, true, Lcta);
             if (Lcta <= 16 * VE)
-                return softmax_cta_rows<T, VB, 16, 1, NT, ALIGNED, true>(
+                return softmax_cta_rows<T, VB, 16, 1, NT, ALIGNED, true, UP>(
                     scores, lengths, first, row_end, rpb, Sk, c, true, Lcta);
         }
     }
-    softmax_cta_rows<T, VB, G, NV, NT, ALIGNED, false>(scores, lengths, first, row_end, rpb, Sk, c,
-                                                       one_req, Lcta);
+    softmax_cta_rows<T, VB, G, NV, NT, ALIGNED, false, UP>(scores, lengths, first, row_end, rpb, Sk,
+                                                           c, one_req, Lcta);
+}
+
+template <typename T, int VB, int G, int NV, int NT, int MINB, bool ALIGNED>
+__global__ void __launch_bounds__(NT, MINB) softmax_warp_kernel(T* __restrict__ scores,
+                                                                const int32_t* __restrict__ lengths,
+                                                                uint32_t nrows, FastDivU32 rpb,
+                                                                int Sk, float c, int rpg) {
+    if (c > 0.f)  // uniform: the sign of the scale picks the max or min reduction
+        softmax_warp_body<T, VB, G, NV, NT, ALIGNED, true>(scores, lengths, nrows, rpb, Sk, c, rpg);
+    else
+        softmax_warp_body<T, VB, G, NV, NT, ALIGNED, false>(scores, lengths, nrows, rpb, Sk, c, rpg);
 }
 
 // ----------------------------------------------------------------------------

@@ -39,7 +39,7 @@ __device__ __forceinline__ int find_req(const int32_t* __restrict__ cu, int num_
 
 // all rows of [first, row_end) belong to one request of length L whose block
 // starts at `base` and whose first row is row0
-template <typename T, int VB, int GC, int NVC, int NT>
+template <typename T, int VB, int GC, int NVC, int NT, bool UP>
 __device__ __forceinline__ void packed_rows(T* __restrict__ scores, uint32_t first,
                                             uint32_t row_end, int64_t base, uint32_t row0, int L,
                                             float c) {
@@ -51,15 +51,14 @@ __device__ __forceinline__ void packed_rows(T* __restrict__ scores, uint32_t fir
     for (uint32_t b = first + (threadIdx.x >> 5) * GPW; b < row_end; b += step, row += step) {
         const bool live = row < row_end;
         T* p = scores + base + (int64_t)((live ? row : first) - row0) * L;
-        softmax_row_pass<T, VB, GC, NVC, false, false>(p, live, L, L, c, q);
+        softmax_row_pass<T, VB, GC, NVC, false, false, UP>(p, live, L, L, c, q);
     }
 }
 
-template <typename T, int VB, int NV, int NT, int MINB>
-__global__ void __launch_bounds__(NT, MINB)
-    softmax_packed_kernel(T* __restrict__ scores, const int32_t* __restrict__ cu,
-                          const int64_t* __restrict__ blocks, int num_req, uint32_t H,
-                          uint32_t total_rows, float c, int rpg) {
+template <typename T, int VB, int NV, int NT, bool UP>
+__device__ __forceinline__ void packed_body(T* __restrict__ scores, const int32_t* __restrict__ cu,
+                                            const int64_t* __restrict__ blocks, int num_req,
+                                            uint32_t H, uint32_t total_rows, float c, int rpg) {
     constexpr int VE = VB / (int)sizeof(T);
     constexpr int GPB = NT / 32;
     constexpr int CAP = 32 * NV * VE;
@@ -82,14 +81,14 @@ __global__ void __launch_bounds__(NT, MINB)
         // fits one pass (GC >= VE - 1), as in the padded kernel
         constexpr bool ok4 = 4 >= VE - 1, ok8 = 8 >= VE - 1;
         if (ok4 && L <= 4 * VE)
-            return packed_rows<T, VB, ok4 ? 4 : 32, 1, NT>(scores, first, row_end, base, row0, L, c);
+            return packed_rows<T, VB, ok4 ? 4 : 32, 1, NT, UP>(scores, first, row_end, base, row0, L, c);
         if (ok8 && L <= 8 * VE)
-            return packed_rows<T, VB, ok8 ? 8 : 32, 1, NT>(scores, first, row_end, base, row0, L, c);
+            return packed_rows<T, VB, ok8 ? 8 : 32, 1, NT, UP>(scores, first, row_end, base, row0, L, c);
         if (L <= 16 * VE)
-            return packed_rows<T, VB, 16, 1, NT>(scores, first, row_end, base, row0, L, c);
+            return packed_rows<T, VB, 16, 1, NT, UP>(scores, first, row_end, base, row0, L, c);
         if (L <= 32 * VE)
-            return packed_rows<T, VB, 32, 1, NT>(scores, first, row_end, base, row0, L, c);
-        return packed_rows<T, VB, 32, NV, NT>(scores, first, row_end, base, row0, L, c);
+            return packed_rows<T, VB, 32, 1, NT, UP>(scores, first, row_end, base, row0, L, c);
+        return packed_rows<T, VB, 32, NV, NT, UP>(scores, first, row_end, base, row0, L, c);
     }
     // the CTA straddles requests: one row per warp, looked up per row
     const int lane = threadIdx.x & 31;
@@ -98,8 +97,19 @@ __global__ void __launch_bounds__(NT, MINB)
         const int L = min(__ldg(cu + r + 1) - __ldg(cu + r), CAP);
         const uint32_t row0 = H * (uint32_t)__ldg(cu + r);
         T* p = scores + __ldg(blocks + r) + (int64_t)(row - row0) * L;
-        softmax_row_pass<T, VB, 32, NV, false, false>(p, true, L, L, c, lane);
+        softmax_row_pass<T, VB, 32, NV, false, false, UP>(p, true, L, L, c, lane);
     }
+}
+
+template <typename T, int VB, int NV, int NT, int MINB>
+__global__ void __launch_bounds__(NT, MINB)
+    softmax_packed_kernel(T* __restrict__ scores, const int32_t* __restrict__ cu,
+                          const int64_t* __restrict__ blocks, int num_req, uint32_t H,
+                          uint32_t total_rows, float c, int rpg) {
+    if (c > 0.f)  // uniform: the sign of the scale picks the max or min reduction
+        packed_body<T, VB, NV, NT, true>(scores, cu, blocks, num_req, H, total_rows, c, rpg);
+    else
+        packed_body<T, VB, NV, NT, false>(scores, cu, blocks, num_req, H, total_rows, c, rpg);
 }
 
 namespace {

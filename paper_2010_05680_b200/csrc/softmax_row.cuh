@@ -17,14 +17,16 @@ __device__ __forceinline__ float rcp_approx(float x) {
 // false: the group has no row this step (it still joins the shuffles, which use
 // the full warp mask).  NARROW: the request is short enough that every valid key
 // lies in the head and the first GC body vectors; the remaining body vectors
-// are written as zeros without any arithmetic.
-template <typename T, int VB, int GC, int NVC, bool ALIGNED, bool NARROW>
+// are written as zeros without any arithmetic.  UP: c > 0, so the row max of
+// c*x is c*max(x) (else c*min(x)); a template parameter so that only one of
+// the two reductions is compiled into each path.
+template <typename T, int VB, int GC, int NVC, bool ALIGNED, bool NARROW, bool UP>
 __device__ __forceinline__ void softmax_row_pass(T* __restrict__ p, bool live, int L, int Sk,
                                                  float c, int q) {
     constexpr int VE = VB / (int)sizeof(T);
     constexpr int HI = ALIGNED ? 0 : (VE - 1 + GC - 1) / GC;
     constexpr int HIA = HI > 0 ? HI : 1;
-    const bool up = c > 0.f;  // max of raw x (else min); c != 0 (host)
+    constexpr bool up = UP;  // max of raw x (else min); c != 0 (host)
     const float sent = up ? -INFINITY : INFINITY;
     if (!live) L = 0;
     int hd = 0, nv = Sk / VE;
@@ -38,29 +40,36 @@ __device__ __forceinline__ void softmax_row_pass(T* __restrict__ p, bool live, i
     // the group maps onto the row (uniform within the group)
     const bool masked = (L < Sk) || (nv != GC * NVC);
 
-    // ---- SM-2: load (never predicated off; see above)
-    float v[NVC][VE];
-    if (L > 0) {
-        // fallback address for lanes past the prefix: the first body vector,
-        // or (row shorter than its head) the VB-aligned vector containing p
-        const T* fb = nv > 0 ? p + hd
-                             : reinterpret_cast<const T*>(reinterpret_cast<uintptr_t>(p) &
-                                                          ~(uintptr_t)(VB - 1));
+    // ---- SM-2: load (never predicated off; see above).  Every load of the
+    // row -- body vectors and the scalar head / tail -- is issued before any
+    // of them is consumed, so a row costs one memory round trip.  An empty
+    // row (L = 0, or a dead group) loads too; the mask below turns all of it
+    // into sentinels.
+    // fallback address for lanes past the prefix: the first body vector, or
+    // (row shorter than its head) the VB-aligned vector containing p
+    const T* fb = nv > 0 ? p + hd
+                         : reinterpret_cast<const T*>(reinterpret_cast<uintptr_t>(p) &
+                                                      ~(uintptr_t)(VB - 1));
+    Raw<VB> raw[NVC];
 #pragma unroll
-        for (int k = 0; k < NVC; ++k) {
-            const int vi = q + k * GC;
-            const int j0 = hd + vi * VE;
-            const bool in = vi < nv && j0 < L;
-            Raw<VB> w;
-            ld_stream<VB>(in ? p + j0 : fb, w);
-            Elem<T>::template unpack<VB>(w, v[k]);
-        }
-    } else {
-#pragma unroll
-        for (int k = 0; k < NVC; ++k)
-#pragma unroll
-            for (int e = 0; e < VE; ++e) v[k][e] = sent;
+    for (int k = 0; k < NVC; ++k) {
+        const int vi = q + k * GC;
+        const int j0 = hd + vi * VE;
+        const bool in = vi < nv && j0 < L;
+        ld_stream<VB>(in ? p + j0 : fb, raw[k]);
     }
+    T hraw[HIA], traw[HIA];
+    if constexpr (!ALIGNED) {
+#pragma unroll
+        for (int i = 0; i < HI; ++i) {
+            const int jh = q + i * GC, jt = tl0 + q + i * GC;
+            hraw[i] = p[(jh < hd && jh < L) ? jh : 0];
+            traw[i] = p[(jt < Sk && jt < L) ? jt : 0];
+        }
+    }
+    float v[NVC][VE];
+#pragma unroll
+    for (int k = 0; k < NVC; ++k) Elem<T>::template unpack<VB>(raw[k], v[k]);
     if (masked) {
 #pragma unroll
         for (int k = 0; k < NVC; ++k) {
@@ -76,10 +85,8 @@ __device__ __forceinline__ void softmax_row_pass(T* __restrict__ p, bool live, i
         for (int i = 0; i < HI; ++i) {
             const int jh = q + i * GC, jt = tl0 + q + i * GC;
             const bool ih = jh < hd && jh < L, it = jt < Sk && jt < L;
-            const float a = Elem<T>::to_f(p[ih ? jh : 0]);
-            const float b = Elem<T>::to_f(p[it ? jt : 0]);
-            hv[i] = ih ? a : sent;
-            tv[i] = it ? b : sent;
+            hv[i] = ih ? Elem<T>::to_f(hraw[i]) : sent;
+            tv[i] = it ? Elem<T>::to_f(traw[i]) : sent;
         }
     }
 
@@ -87,7 +94,7 @@ __device__ __forceinline__ void softmax_row_pass(T* __restrict__ p, bool live, i
     float m[1];
     {
         float a = sent;
-        if (up) {
+        if constexpr (up) {
 #pragma unroll
             for (int k = 0; k < NVC; ++k)
 #pragma unroll
