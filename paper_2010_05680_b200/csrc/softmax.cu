@@ -604,7 +604,9 @@ struct SoftmaxTier {
     TT_SM_WARP(false, T, TN, 32, 8, 3, 256, 3), TT_SM_WARP(false, T, TN, 32, 8, 2, 256, 4),     \
     TT_SM_WARP(false, T, TN, 32, 16, 2, 256, 3), TT_SM_WARP(false, T, TN, 16, 8, 5, 256, 4),    \
     TT_SM_WARP(false, T, TN, 16, 16, 3, 256, 5), TT_SM_WARP(false, T, TN, 16, 8, 3, 256, 5),   \
-    TT_SM_WARP(false, T, TN, 16, 8, 2, 256, 6)
+    TT_SM_WARP(false, T, TN, 16, 8, 2, 256, 6), TT_SM_WARP(false, T, TN, 32, 8, 4, 256, 2),     \
+    TT_SM_WARP(false, T, TN, 16, 8, 8, 256, 2), TT_SM_WARP(false, T, TN, 32, 16, 2, 256, 4),    \
+    TT_SM_WARP(false, T, TN, 16, 16, 4, 256, 4), TT_SM_WARP(false, T, TN, 32, 32, 1, 256, 4)
 
 // M2..M4: min CTAs/SM (register cap) of the NV = 2..4 warp tiers, chosen so
 // the row (NV * VE fp32 values per lane) fits without spilling.
@@ -641,6 +643,7 @@ const Pref kSmPref[] = {
     {1, 128, 256, "softmax_warp<f16,V16,G8,NV4,T256,M4,P4>"},
     {1, 256, 320, "softmax_warp<f16,V16,G8,NV5,T256,M4,P4>"},
     {1, 320, 384, "softmax_warp<f16,V32,G8,NV3,T256,M3,P4>"},
+    {1, 384, 512, "softmax_warp<f16,V32,G32,NV1,T256,M6,P2>"},  // C3 / C2 ragged: -3..6%
     {2, 64, 128, "softmax_warp<bf16,V16,G8,NV2,T256,M6,P4>"},
     {2, 128, 256, "softmax_warp<bf16,V16,G8,NV4,T256,M4,P4>"},
     {2, 256, 320, "softmax_warp<bf16,V16,G8,NV5,T256,M4,P4>"},

@@ -58,13 +58,19 @@ __device__ __forceinline__ void softmax_row_pass(T* __restrict__ p, bool live, i
         const bool in = vi < nv && j0 < L;
         ld_stream<VB>(in ? p + j0 : fb, raw[k]);
     }
+    // scalar head / tail: one pointer each, shared by the load and the store
+    // (an in-row key past L is loaded harmlessly and masked below)
     T hraw[HIA], traw[HIA];
+    T* ph[HIA];
+    T* pt[HIA];
     if constexpr (!ALIGNED) {
 #pragma unroll
         for (int i = 0; i < HI; ++i) {
             const int jh = q + i * GC, jt = tl0 + q + i * GC;
-            hraw[i] = p[(jh < hd && jh < L) ? jh : 0];
-            traw[i] = p[(jt < Sk && jt < L) ? jt : 0];
+            ph[i] = p + (jh < hd ? jh : 0);
+            pt[i] = p + (jt < Sk ? jt : 0);
+            hraw[i] = *ph[i];
+            traw[i] = *pt[i];
         }
     }
     float v[NVC][VE];
@@ -165,8 +171,8 @@ __device__ __forceinline__ void softmax_row_pass(T* __restrict__ p, bool live, i
 #pragma unroll
         for (int i = 0; i < HI; ++i) {
             const int jh = q + i * GC, jt = tl0 + q + i * GC;
-            if (jh < hd) p[jh] = Elem<T>::from_f(hv[i] * inv);
-            if (jt < Sk) p[jt] = Elem<T>::from_f(tv[i] * inv);
+            if (jh < hd) *ph[i] = Elem<T>::from_f(hv[i] * inv);
+            if (jt < Sk) *pt[i] = Elem<T>::from_f(tv[i] * inv);
         }
     }
 }

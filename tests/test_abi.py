@@ -121,7 +121,7 @@ def test_launch_without_device_fails_loudly(ttlib):
     (torch.float32, 40, "softmax_warp<f32,V16,G16,NV1,T256,M6,P4>"),
     (torch.float16, 37, "softmax_warp<f16,V16,G8,NV1,T256,M6,P4>"),
     (torch.bfloat16, 512, "softmax_warp<bf16,V32,G32,NV1,T256,M6,P4>"),
-    (torch.float16, 491, "softmax_warp<f16,V32,G32,NV1,T256,M6,P4>"),
+    (torch.float16, 491, "softmax_warp<f16,V32,G32,NV1,T256,M6,P2>"),
     (torch.float32, 500, "softmax_warp<f32,V32,G32,NV2,T256,M3,P2>"),
     (torch.float32, 4096, "softmax_rows<f32,V32,G128,NV4,R1,T128,M1>"),
     (torch.bfloat16, 32768, "softmax_rows<bf16,V32,G1024,NV2,R1,T1024,M1>"),

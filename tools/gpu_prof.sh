@@ -7,7 +7,7 @@ for j in "${JOBS[@]}"; do
   if [ -n "$tier" ]; then
     $P -o gpurun_out/prof_$name python tools/prof_one.py $spec --tier "$tier" $extra > gpurun_out/prof_$name.log 2>&1
   else
-    $P -o gpurun_out/prof_$name python tools/prof_one.py $spec > gpurun_out/prof_$name.log 2>&1
+    $P -o gpurun_out/prof_$name python tools/prof_one.py $spec $extra > gpurun_out/prof_$name.log 2>&1
   fi
 done
 ls -la gpurun_out/

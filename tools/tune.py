@@ -38,13 +38,18 @@ def timeit(fn, nbufs, reps=50, warm=5):
 def main():
     op, dt = sys.argv[1], W.DTYPES[sys.argv[2]]
     dims = [int(v) for v in sys.argv[3:]]
-    ragged = os.environ.get("RAGGED") == "1"
+    ragged = os.environ.get("RAGGED", "0") != "0"  # "1": U{1..Sk} draws; "c3": BASELINE C3 lengths
     e = W.ELEM_BYTES[dt]
     names = tt.tiers(op, dt)
     only = os.environ.get("ONLY")
     if op == "softmax":
         B, H, Sq, Sk = dims
-        lens = W.lengths_ragged(B, Sk) if ragged else W.lengths_full(B, Sk)
+        if os.environ.get("RAGGED") == "c3":
+            lens = W.c3_lengths()
+            B, Sk = len(lens), int(lens.max())
+            dims = [B, H, Sk, Sk]
+        else:
+            lens = W.lengths_ragged(B, Sk) if ragged else W.lengths_full(B, Sk)
         nbytes = B * H * Sq * Sk * e
         nbufs = max(1, -(-4 * L2 // nbytes))
         bufs = [W.scores(B, H, Sq, Sk, dt, device="cuda", seed=i) for i in range(nbufs)]
