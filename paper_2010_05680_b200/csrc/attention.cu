@@ -7,8 +7,13 @@
 // One CTA = 128 query rows of one (b, h); 4 warps, thread t owns query row t
 // (TMEM lane t).  Per 128-key tile:
 //   1. K / V tiles arrive in shared memory by cp.async (16-byte chunks written
-//      in the SWIZZLE_128B layout UMMA reads), double-buffered; keys >= L_b are
-//      zero-filled, never read (masked keys cannot inject NaN into the MMA).
+//      in the SWIZZLE_128B layout UMMA reads); keys >= L_b are zero-filled,
+//      never read (masked keys cannot inject NaN into the MMA).  NBUF = 1
+//      (default): one K and one V buffer, K(t+1) is fetched while P(t) is
+//      computed and V(t+1) while the next S MMA runs -- 80 KB of shared
+//      memory, so 2 CTAs share an SM and overlap each other's serial phases;
+//      NBUF = 2 double-buffers both (112 KB, 1 CTA / SM), kept as a variant
+//      (ttx_attention_variant) -- 1.6x slower on C4.
 //   2. one thread issues S = Q K^T: 4 x tcgen05.mma M128 N128 K16 (bf16/f16 in,
 //      fp32 out) into TMEM columns [0, 128); tcgen05.commit -> mbarrier.
 //   3. every thread tcgen05.ld's its row of S, masks keys >= L_b, runs the online
