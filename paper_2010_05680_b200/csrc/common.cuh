@@ -203,6 +203,36 @@ __device__ __forceinline__ float ex2_approx(float x) {
     return y;
 }
 
+// Packed fp32 pairs (sm_100a FFMA2 / FADD2 / FMUL2): one issue slot does two
+// IEEE round-to-nearest fp32 operations, which halves the issue cost of the
+// per-element arithmetic of the issue-bound 16-bit softmax rows.
+struct F2 {
+    unsigned long long r;
+};
+__device__ __forceinline__ F2 f2_make(float a, float b) {
+    F2 o;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(o.r) : "f"(a), "f"(b));
+    return o;
+}
+__device__ __forceinline__ void f2_split(F2 v, float& a, float& b) {
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v.r));
+}
+__device__ __forceinline__ F2 f2_fma(F2 a, F2 b, F2 c) {
+    F2 o;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(o.r) : "l"(a.r), "l"(b.r), "l"(c.r));
+    return o;
+}
+__device__ __forceinline__ F2 f2_add(F2 a, F2 b) {
+    F2 o;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(o.r) : "l"(a.r), "l"(b.r));
+    return o;
+}
+__device__ __forceinline__ F2 f2_mul(F2 a, F2 b) {
+    F2 o;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(o.r) : "l"(a.r), "l"(b.r));
+    return o;
+}
+
 // Warp-wide f32 max in one instruction (CREDUX.MAX.F32.NAN, sm_100a only).
 __device__ __forceinline__ float warp_max_redux(float v) {
     float m;

@@ -756,7 +756,11 @@ struct LnTier {
     TT_LN_WARP_P(false, T, TN, 32, 32, 1, 256, 4, 1), TT_LN_WARP_P(false, T, TN, 32, 32, 4, 256, 2, 1), \
     TT_LN_EARLY(false, T, TN, 16, 32, 3, 256), TT_LN_EARLY(false, T, TN, 32, 32, 2, 256),        \
     TT_LN_EARLY(false, T, TN, 32, 32, 3, 256), TT_LN_EARLY(false, T, TN, 32, 32, 4, 256),        \
-    TT_LN_EARLY(false, T, TN, 16, 32, 3, 128), TT_LN_EARLY(false, T, TN, 32, 32, 2, 128)
+    TT_LN_EARLY(false, T, TN, 16, 32, 3, 128), TT_LN_EARLY(false, T, TN, 32, 32, 2, 128),        \
+    TT_LN_WARP(false, T, TN, 16, 16, 6, 256, 3), TT_LN_WARP(false, T, TN, 16, 8, 12, 256, 2),   \
+    TT_LN_WARP(false, T, TN, 32, 16, 3, 256, 3), TT_LN_WARP(false, T, TN, 32, 16, 6, 256, 3),   \
+    TT_LN_WARP(false, T, TN, 32, 8, 6, 256, 2), TT_LN_WARP(false, T, TN, 32, 8, 12, 256, 2),    \
+    TT_LN_WARP(false, T, TN, 16, 16, 6, 256, 4), TT_LN_WARP(false, T, TN, 32, 16, 3, 256, 4)
 
 // MA / MB / MC: min CTAs/SM (register cap) for warp tiers holding about
 // 16 / 24-32 / 48-64 fp32 row values per lane.

@@ -126,14 +126,27 @@ __device__ __forceinline__ void softmax_row_pass(T* __restrict__ p, bool live, i
     if (!(fabsf(nm) <= 3.0e38f)) nm = 0.f;  // empty row (L = 0)
 
     // ---- SM-4: e_j = 2^(c x_j - m), once (sentinel -> +0.0); s = sum e_j
+    // (pairs of keys through FFMA2 / FADD2: two running sums, one per lane of
+    // the pair, added at the end)
     float s[1] = {0.f};
+    {
+        const F2 c2 = f2_make(c, c), nm2 = f2_make(nm, nm);
+        F2 s2 = f2_make(0.f, 0.f);
 #pragma unroll
-    for (int k = 0; k < NVC; ++k)
+        for (int k = 0; k < NVC; ++k)
 #pragma unroll
-        for (int e = 0; e < VE; ++e) {
-            v[k][e] = ex2_approx(fmaf(v[k][e], c, nm));
-            s[0] += v[k][e];
-        }
+            for (int e = 0; e < VE; e += 2) {
+                const F2 t = f2_fma(f2_make(v[k][e], v[k][e + 1]), c2, nm2);
+                float t0, t1;
+                f2_split(t, t0, t1);
+                v[k][e] = ex2_approx(t0);
+                v[k][e + 1] = ex2_approx(t1);
+                s2 = f2_add(s2, f2_make(v[k][e], v[k][e + 1]));
+            }
+        float s0, s1;
+        f2_split(s2, s0, s1);
+        s[0] = s0 + s1;
+    }
     if constexpr (!ALIGNED) {
 #pragma unroll
         for (int i = 0; i < HI; ++i) {
@@ -154,8 +167,10 @@ __device__ __forceinline__ void softmax_row_pass(T* __restrict__ p, bool live, i
         const int vi = q + k * GC;
         if (vi < nv) {
             float y[VE];
+            const F2 inv2 = f2_make(inv, inv);
 #pragma unroll
-            for (int e = 0; e < VE; ++e) y[e] = v[k][e] * inv;
+            for (int e = 0; e < VE; e += 2)
+                f2_split(f2_mul(f2_make(v[k][e], v[k][e + 1]), inv2), y[e], y[e + 1]);
             Raw<VB> w;
             Elem<T>::template pack<VB>(y, w);
             st_stream<VB>(p + hd + vi * VE, w);

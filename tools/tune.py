@@ -22,15 +22,26 @@ L2 = 126 * 1024 * 1024
 
 
 def timeit(fn, nbufs, reps=50, warm=5):
-    st = torch.cuda.current_stream()
-    for i in range(warm):
-        fn(i % nbufs)
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    """ms per call: the calls are captured once into a CUDA graph and replayed,
+    so host launch overhead (Python + ctypes) does not inflate small shapes;
+    CUDA events on the replay stream."""
+    st = torch.cuda.Stream()
+    with torch.cuda.stream(st):
+        for i in range(warm):
+            fn(i % nbufs)
     torch.cuda.synchronize()
-    a.record(st)
-    for i in range(reps):
-        fn(i % nbufs)
-    b.record(st)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=st):
+        for i in range(reps):
+            fn(i % nbufs)
+    with torch.cuda.stream(st):
+        g.replay()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(st):
+        a.record(st)
+        g.replay()
+        b.record(st)
     torch.cuda.synchronize()
     return a.elapsed_time(b) / reps
 
