@@ -87,6 +87,37 @@ __device__ __forceinline__ void tc_ld32(uint32_t taddr, float (&v)[32]) {
     for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// the same without the wait (several loads in flight, then tc_wait_ld)
+__device__ __forceinline__ void tc_ld32_nowait(uint32_t taddr, uint32_t (&r)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+        "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+          "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]),
+          "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+          "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),
+          "=r"(r[31])
+        : "r"(taddr));
+}
+__device__ __forceinline__ void tc_wait_ld() {
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+// 32 consecutive TMEM columns of this thread's lane <- registers
+__device__ __forceinline__ void tc_st32(uint32_t taddr, const float (&v)[32]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"
+        "%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(
+            taddr),
+        "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]),
+        "f"(v[8]), "f"(v[9]), "f"(v[10]), "f"(v[11]), "f"(v[12]), "f"(v[13]), "f"(v[14]),
+        "f"(v[15]), "f"(v[16]), "f"(v[17]), "f"(v[18]), "f"(v[19]), "f"(v[20]), "f"(v[21]),
+        "f"(v[22]), "f"(v[23]), "f"(v[24]), "f"(v[25]), "f"(v[26]), "f"(v[27]), "f"(v[28]),
+        "f"(v[29]), "f"(v[30]), "f"(v[31])
+        : "memory");
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+
 // bounded wait: a fault in the async units traps instead of hanging the GPU
 __device__ __forceinline__ void mbar_wait_bounded(uint64_t* bar, uint32_t parity) {
     uint32_t done = 0, spins = 0;
@@ -145,7 +176,7 @@ constexpr size_t attn_smem() {
     return (size_t)(3 + 2 * NBUF) * kTile + 64 + 1024;
 }
 
-template <typename T, int NBUF>
+template <typename T, int NBUF, bool UP>
 __global__ void __launch_bounds__(kNT, 3 - NBUF)
     attention_tc_kernel(T* __restrict__ out, const T* __restrict__ q, const T* __restrict__ k,
                         const T* __restrict__ v, const int32_t* __restrict__ lengths, int H,
@@ -175,7 +206,7 @@ __global__ void __launch_bounds__(kNT, 3 - NBUF)
         return;
     }
 
-    if (warp == 0) {  // TMEM: S in columns [0,128), O tile in [128,192)
+    if (warp == 0) {  // TMEM: S in columns [0,128), O in [128,192)
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(
                          smem_u32(tmem_slot))
                      : "memory");
@@ -200,18 +231,20 @@ __global__ void __launch_bounds__(kNT, 3 - NBUF)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
-    const uint32_t t_s = tmem, t_o = tmem + 128;
     const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
+    const uint32_t t_s = tmem + lane_off, t_o = tmem + 128 + lane_off;
 
     constexpr int kFmt = sizeof(T) == 2 && std::is_same<T, __nv_bfloat16>::value ? 1 : 0;
     constexpr uint32_t idesc_s = f16_idesc(kFmt, 0, kBM, kBN);
     constexpr uint32_t idesc_o = f16_idesc(kFmt, 1, kBM, kD);
-
-    float o[kD];
-#pragma unroll
-    for (int i = 0; i < kD; ++i) o[i] = 0.f;
-    float m_run = -INFINITY, l_run = 0.f;
+    // O and l are kept relative to a reference max m_ref (log2 units, scaled);
+    // m_ref only moves -- and O is rescaled in TMEM -- when a tile's max
+    // exceeds it by more than kRescale, so p = 2^(s c - m_ref) <= 2^kRescale.
+    constexpr float kRescale = 8.f;
+    const float sent = UP ? -INFINITY : INFINITY;
+    float m_ref = -INFINITY, l_run = 0.f;
     uint32_t ph_s = 0, ph_o = 0;
+    unsigned char* prow = sbase + (sP - base);
 
     for (int kt = 0; kt < nkt; ++kt) {
         const int st = NBUF == 2 ? (kt & 1) : 0;
@@ -229,7 +262,7 @@ __global__ void __launch_bounds__(kNT, 3 - NBUF)
             const uint32_t kbase = sK + st * kTile;
 #pragma unroll
             for (int ks = 0; ks < kD / 16; ++ks)
-                tc_mma(t_s, sw128_desc(sQ + ks * 32, 16, 1024),
+                tc_mma(tmem, sw128_desc(sQ + ks * 32, 16, 1024),
                        sw128_desc(kbase + ks * 32, 16, 1024), idesc_s, ks > 0);
             tc_commit(&bars[0]);
         }
@@ -241,68 +274,91 @@ __global__ void __launch_bounds__(kNT, 3 - NBUF)
             cp_async_commit();
         }
 
-        // ---- online softmax on this thread's row of S
+        // ---- this thread's row of S: 4 TMEM loads in flight, one wait
+        float sv[kBN];
+        {
+            uint32_t r[4][32];
+#pragma unroll
+            for (int ch = 0; ch < 4; ++ch) tc_ld32_nowait(t_s + ch * 32, r[ch]);
+            tc_wait_ld();
+#pragma unroll
+            for (int ch = 0; ch < 4; ++ch)
+#pragma unroll
+                for (int e = 0; e < 32; ++e) sv[ch * 32 + e] = __uint_as_float(r[ch][e]);
+        }
         const int key0 = kt * kBN;
-        float tmax = -INFINITY;
+        if (key0 + kBN > L) {  // the partial tile only: keys >= L -> sentinel
 #pragma unroll
-        for (int ch = 0; ch < 4; ++ch) {
-            float sv[32];
-            tc_ld32(t_s + lane_off + ch * 32, sv);
+            for (int e = 0; e < kBN; ++e) sv[e] = key0 + e < L ? sv[e] : sent;
+        }
+        // max (UP) or min of the raw scores, then the scaled max
+        float mx = sent;
 #pragma unroll
-            for (int e = 0; e < 32; ++e) {
-                const float t = (key0 + ch * 32 + e < L) ? sv[e] * c : -INFINITY;
-                tmax = fmaxf(tmax, t);
+        for (int e = 0; e < kBN; ++e) mx = UP ? fmaxf(mx, sv[e]) : fminf(mx, sv[e]);
+        const float m_tile = mx * c;
+        if (kt == 0) {
+            m_ref = m_tile;  // nothing accumulated yet
+        } else if (__any_sync(0xffffffffu, m_tile > m_ref + kRescale)) {
+            // rescale this warp's O rows (the previous P.V has completed)
+            const float m_new = fmaxf(m_ref, m_tile);
+            const float alpha = ex2_approx(m_ref - m_new);
+            l_run *= alpha;
+            m_ref = m_new;
+#pragma unroll
+            for (int ch = 0; ch < kD / 32; ++ch) {
+                float ov[32];
+                tc_ld32(t_o + ch * 32, ov);
+#pragma unroll
+                for (int e = 0; e < 32; ++e) ov[e] *= alpha;
+                tc_st32(t_o + ch * 32, ov);
             }
         }
-        const float m_new = fmaxf(m_run, tmax);
-        const float alpha = ex2_approx(m_run - m_new);  // m_run = -inf -> 0
-        float psum = 0.f;
-        unsigned char* prow = sbase + (sP - base);
+
+        // ---- p = 2^(s c - m_ref) (masked keys: sentinel -> +0), row sum, P -> smem
+        const F2 c2 = f2_make(c, c), nm2 = f2_make(-m_ref, -m_ref);
+        F2 ps2 = f2_make(0.f, 0.f);
 #pragma unroll
         for (int ch = 0; ch < 4; ++ch) {
-            float sv[32];
-            tc_ld32(t_s + lane_off + ch * 32, sv);
-            float p[32];
+            float pv[32];
 #pragma unroll
-            for (int e = 0; e < 32; ++e) {
-                p[e] = (key0 + ch * 32 + e < L) ? ex2_approx(sv[e] * c - m_new) : 0.f;
-                psum += p[e];
+            for (int e = 0; e < 32; e += 2) {
+                float t0, t1;
+                f2_split(f2_fma(f2_make(sv[ch * 32 + e], sv[ch * 32 + e + 1]), c2, nm2), t0, t1);
+                pv[e] = ex2_approx(t0);
+                pv[e + 1] = ex2_approx(t1);
+                ps2 = f2_add(ps2, f2_make(pv[e], pv[e + 1]));
             }
             // keys ch*32 .. ch*32+31 -> P half (ch / 2), 16-byte chunks (ch % 2) * 4 + j
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
                 Raw<16> w;
-                Elem<T>::template pack<16>(p + 8 * j, w);
+                Elem<T>::template pack<16>(pv + 8 * j, w);
                 const uint32_t off = (uint32_t)(ch >> 1) * kTile + sw_off(tid, (ch & 1) * 4 + j);
                 *reinterpret_cast<uint4*>(prow + off) = make_uint4(w.w[0], w.w[1], w.w[2], w.w[3]);
             }
         }
-        l_run = l_run * alpha + psum;
-        m_run = m_new;
+        {
+            float a0, a1;
+            f2_split(ps2, a0, a1);
+            l_run += a0 + a1;
+        }
         fence_proxy_async_smem();  // P (generic stores) -> tensor core
         tc_fence_before();
         __syncthreads();
         tc_fence_after();
 
-        // ---- O_tile = P V (P K-major; V MN-major: 16 keys = 2048 B per K-step)
+        // ---- O += P V in TMEM (P K-major; V MN-major: 16 keys = 2048 B per K-step)
         if (tid == 0) {
             const uint32_t vbase = sV + st * kTile;
 #pragma unroll
             for (int ks = 0; ks < kBN / 16; ++ks)
-                tc_mma(t_o, sw128_desc(sP + (ks >> 2) * kTile + (ks & 3) * 32, 16, 1024),
-                       sw128_desc(vbase + ks * 2048, 16384, 1024), idesc_o, ks > 0);
+                tc_mma(tmem + 128, sw128_desc(sP + (ks >> 2) * kTile + (ks & 3) * 32, 16, 1024),
+                       sw128_desc(vbase + ks * 2048, 16384, 1024), idesc_o, (kt > 0 || ks > 0));
             tc_commit(&bars[1]);
         }
         mbar_wait_bounded(&bars[1], ph_o);
         ph_o ^= 1;
         tc_fence_after();
-#pragma unroll
-        for (int ch = 0; ch < 2; ++ch) {
-            float ov[32];
-            tc_ld32(t_o + lane_off + ch * 32, ov);
-#pragma unroll
-            for (int e = 0; e < 32; ++e) o[ch * 32 + e] = fmaf(o[ch * 32 + e], alpha, ov[e]);
-        }
         if constexpr (NBUF == 2) {
             // stage st is free again: prefetch tile kt + 2 into it
             if (kt + 2 < nkt) {
@@ -317,17 +373,23 @@ __global__ void __launch_bounds__(kNT, 3 - NBUF)
     }
 
     // ---- o = O / l, narrowed, one 128-byte row per thread
-    if (row < S) {
-        const float inv = 1.0f / l_run;
-        T* orow = out + head + (size_t)row * kD;
+    {
+        uint32_t r[2][32];
+        tc_ld32_nowait(t_o, r[0]);
+        tc_ld32_nowait(t_o + 32, r[1]);
+        tc_wait_ld();
+        if (row < S) {
+            const float inv = 1.0f / l_run;
+            T* orow = out + head + (size_t)row * kD;
 #pragma unroll
-        for (int j = 0; j < kD / 8; ++j) {
-            float y[8];
+            for (int j = 0; j < kD / 8; ++j) {
+                float y[8];
 #pragma unroll
-            for (int e = 0; e < 8; ++e) y[e] = o[8 * j + e] * inv;
-            Raw<16> w;
-            Elem<T>::template pack<16>(y, w);
-            reinterpret_cast<uint4*>(orow)[j] = make_uint4(w.w[0], w.w[1], w.w[2], w.w[3]);
+                for (int e = 0; e < 8; ++e) y[e] = __uint_as_float(r[j >> 2][(j & 3) * 8 + e]) * inv;
+                Raw<16> w;
+                Elem<T>::template pack<16>(y, w);
+                reinterpret_cast<uint4*>(orow)[j] = make_uint4(w.w[0], w.w[1], w.w[2], w.w[3]);
+            }
         }
     }
     tc_fence_before();
@@ -349,16 +411,22 @@ cudaError_t launch_attn(void* out, const void* q, const void* k, const void* v,
     constexpr size_t smem = attn_smem<NBUF>();
     static std::atomic<int> attr{0};
     if (!attr.load()) {
-        cudaError_t e = cudaFuncSetAttribute(attention_tc_kernel<T, NBUF>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)smem);
-        if (e != cudaSuccess) return e;
+        for (auto kern : {attention_tc_kernel<T, NBUF, true>, attention_tc_kernel<T, NBUF, false>}) {
+            cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)smem);
+            if (e != cudaSuccess) return e;
+        }
         attr.store(1);
     }
     dim3 grid((unsigned)((S + kBM - 1) / kBM), (unsigned)H, (unsigned)B);
-    attention_tc_kernel<T, NBUF><<<grid, kNT, smem, st>>>(
-        static_cast<T*>(out), static_cast<const T*>(q), static_cast<const T*>(k),
-        static_cast<const T*>(v), lengths, (int)H, (int)S, scale * 1.4426950408889634f);
+    // c = scale * log2(e); scale 0 -> a tiny positive c (uniform weights, as the
+    // softmax kernels do), so the masked-key sentinel still maps to p = +0
+    float c = scale * 1.4426950408889634f;
+    if (c == 0.f) c = 1e-30f;
+    auto kern = c > 0.f ? attention_tc_kernel<T, NBUF, true> : attention_tc_kernel<T, NBUF, false>;
+    kern<<<grid, kNT, smem, st>>>(static_cast<T*>(out), static_cast<const T*>(q),
+                                  static_cast<const T*>(k), static_cast<const T*>(v), lengths,
+                                  (int)H, (int)S, c);
     return cudaGetLastError();
 }
 

@@ -1,6 +1,6 @@
 # ncu --set full of selected tiers: PROF="name|op dtype dims|tier;..." (one launch after 2 warm-ups)
 set -x
-P="ncu --set full --import-source on --clock-control none -k regex:softmax_|ln_ -s 2 -c 1"
+P="ncu --set full --import-source on --clock-control none -k regex:${KREGEX:-softmax_|ln_} -s 2 -c 1"
 IFS=';' read -ra JOBS <<< "$PROF"
 for j in "${JOBS[@]}"; do
   IFS='|' read -r name spec tier extra <<< "$j"

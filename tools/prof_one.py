@@ -3,6 +3,7 @@
 
   python tools/prof_one.py softmax bf16 64 16 512 512 [--tier NAME] [--reps 5]
   python tools/prof_one.py layernorm bf16 32768 1024 [--tier NAME]
+  python tools/prof_one.py attention bf16 64 16 512 [--tier 1|2]   (B H S; tier = K/V buffering)
 """
 import argparse
 import os
@@ -26,10 +27,22 @@ def main():
     ap.add_argument("--ragged", action="store_true")
     a = ap.parse_args()
     dt = W.DTYPES[a.dtype]
-    if a.tier:
+    if a.tier and a.op != "attention":
         names = tt.tiers(a.op, dt)
         tt.force_tier(a.op, dt, names.index(a.tier))
-    if a.op == "softmax":
+    if a.op == "attention":
+        B, H, S = a.dims
+        g = torch.Generator(device="cuda").manual_seed(0)
+        q, k, v = [torch.randn(B, H, S, 64, device="cuda", dtype=dt, generator=g)
+                   for _ in range(3)]
+        o = torch.empty_like(q)
+        lens = W.lengths_ragged(B, S) if a.ragged else W.lengths_full(B, S)
+        L = torch.as_tensor(lens).cuda()
+        if a.tier:
+            tt.attention_variant(int(a.tier))
+        for _ in range(a.reps):
+            tt.tt_attention_fwd(o, q, k, v, L, 0.125)
+    elif a.op == "softmax":
         B, H, Sq, Sk = a.dims
         lens = W.lengths_ragged(B, Sk) if a.ragged else W.lengths_full(B, Sk)
         x = W.scores(B, H, Sq, Sk, dt, device="cuda")
