@@ -27,8 +27,11 @@ TT_API const char* ttx_tier_name(int op, int dtype, int i);
 /* Force tier i for (op, dtype); i = -1 restores automatic selection.
  * Returns TT_ERROR_INVALID_VALUE for a bad op, dtype or index. */
 TT_API tt_status ttx_force_tier(int op, int dtype, int i);
-/* Fused attention (tt_attention_fwd) K/V buffering: 0 = automatic,
- * 1 = single-buffered (2 CTAs per SM), 2 = double-buffered (1 CTA per SM). */
+/* Fused attention (tt_attention_fwd) variant: 0 = automatic, 1 = 128-key tiles
+ * single-buffered (2 CTAs per SM), 2 = 128-key tiles double-buffered (1 CTA per
+ * SM), 3 = 64-key tiles single-buffered (4 CTAs per SM), 4 = 64-key tiles
+ * double-buffered and software-pipelined (3 CTAs per SM).  Returns
+ * TT_ERROR_INVALID_VALUE outside 0..4. */
 TT_API tt_status ttx_attention_variant(int v);
 
 #ifdef __cplusplus

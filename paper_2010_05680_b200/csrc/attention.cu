@@ -5,24 +5,28 @@
 // all the kernels between two GEMM kernels").
 //
 // One CTA = 128 query rows of one (b, h); 4 warps, thread t owns query row t
-// (TMEM lane t).  Per 128-key tile:
+// (TMEM lane t).  Per tile of BN keys (64 by default):
 //   1. K / V tiles arrive in shared memory by cp.async (16-byte chunks written
 //      in the SWIZZLE_128B layout UMMA reads); keys >= L_b are zero-filled,
-//      never read (masked keys cannot inject NaN into the MMA).  NBUF = 1
-//      (default): one K and one V buffer, K(t+1) is fetched while P(t) is
-//      computed and V(t+1) while the next S MMA runs -- 80 KB of shared
-//      memory, so 2 CTAs share an SM and overlap each other's serial phases;
-//      NBUF = 2 double-buffers both (112 KB, 1 CTA / SM), kept as a variant
-//      (ttx_attention_variant) -- 1.6x slower on C4.
-//   2. one thread issues S = Q K^T: 4 x tcgen05.mma M128 N128 K16 (bf16/f16 in,
-//      fp32 out) into TMEM columns [0, 128); tcgen05.commit -> mbarrier.
-//   3. every thread tcgen05.ld's its row of S, masks keys >= L_b, runs the online
-//      max / exp2 / sum in registers (no shuffles: a row is one thread) and
-//      writes P (16-bit) into shared memory, again in the UMMA layout.
-//   4. one thread issues O_tile = P V: 8 x tcgen05.mma M128 N64 K16 (V as an
-//      MN-major operand) into TMEM columns [128, 192); each thread then folds
-//      O_tile into its register accumulator O = O * alpha + O_tile.
+//      never read (masked keys cannot inject NaN into the MMA).
+//   2. one thread issues S = Q K^T: 4 x tcgen05.mma M128 N=BN K16 (bf16/f16 in,
+//      fp32 out) into TMEM columns [0, BN); tcgen05.commit -> mbarrier.
+//   3. every thread tcgen05.ld's its row of S (one wait for all columns), masks
+//      keys >= L_b (partial tile only), takes the row max and writes
+//      p = 2^(s c - m_ref) (16-bit) into shared memory in the UMMA layout; the
+//      row sum l is kept in a register (a row is one thread: no shuffles).
+//   4. one thread issues O += P V: BN/16 x tcgen05.mma M128 N64 K16 (V as an
+//      MN-major operand) into TMEM columns [BN, BN + 64) -- O never leaves
+//      TMEM.  m_ref only moves when a tile's max exceeds it by more than 2^8;
+//      then the warp rescales its O rows in TMEM (tcgen05.ld / st), which
+//      after the first tiles is rare.
 // Finally o = O / l, narrowed, stored row-per-thread.  Head dim D = 64.
+// Schedules (ttx_attention_variant): NBUF = 2 (default, with BN = 64: 64 KB of
+// shared memory, 3 CTAs per SM) double-buffers K and V and software-pipelines
+// the tile loop -- S(t+1) is issued as soon as S(t) has been read out of TMEM,
+// so the QK^T MMA runs under softmax(t), and P.V(t) is only waited for when P,
+// O or its V buffer is reused.  NBUF = 1 keeps one K and one V buffer and runs
+// the steps in order (2 CTAs per SM at BN = 128, 4 at BN = 64).
 #include <atomic>
 #include <type_traits>
 
@@ -33,7 +37,7 @@ namespace tt {
 
 namespace {
 
-constexpr int kBM = 128, kBN = 128, kD = 64, kNT = 128;
+constexpr int kBM = 128, kD = 64, kNT = 128;
 constexpr int kTile = kBM * kD * 2;  // 16 KB: 128 rows x 128 B
 
 // ---- PTX wrappers (tcgen05 / cp.async) -------------------------------------
@@ -152,12 +156,12 @@ __device__ __forceinline__ uint32_t sw_off(int r, int c) {
     return (uint32_t)((r >> 3) * 1024 + (r & 7) * 128 + ((c ^ (r & 7)) << 4));
 }
 
-// rows [row0, row0 + 128) of a [S, 64] 16-bit matrix into a swizzled tile;
+// rows [row0, row0 + ROWS) of a [S, 64] 16-bit matrix into a swizzled tile;
 // rows >= valid are zero-filled without reading global memory
-template <typename T>
+template <typename T, int ROWS = kBM>
 __device__ __forceinline__ void load_tile(uint32_t tile, const T* g, int row0, int valid) {
 #pragma unroll
-    for (int i = 0; i < (kBM * 8) / kNT; ++i) {
+    for (int i = 0; i < (ROWS * 8) / kNT; ++i) {
         const int idx = threadIdx.x + i * kNT;
         const int r = idx >> 3, c = idx & 7;
         const bool in = row0 + r < valid;
@@ -168,27 +172,41 @@ __device__ __forceinline__ void load_tile(uint32_t tile, const T* g, int row0, i
 
 }  // namespace
 
-// NBUF = 2: K / V double-buffered (112 KB smem, 1 CTA per SM);
-// NBUF = 1: single-buffered (80 KB, 2 CTAs per SM, so one CTA's softmax runs
-// while the other's MMAs and loads are in flight).
-template <int NBUF>
+// BN keys per tile (128 or 64).  A K or V tile is BN rows of 128 B; P is
+// 128 x BN 16-bit (BN / 64 SW128 tiles of 16 KB).
+//   NBUF = 2, BN = 128: K / V double-buffered, 112 KB smem, 1 CTA per SM;
+//   NBUF = 1, BN = 128: 80 KB, 2 CTAs per SM (one CTA's softmax runs while the
+//                       other's MMAs and loads are in flight);
+//   NBUF = 1, BN = 64:  48 KB and 128 TMEM columns, 4 CTAs per SM;
+//   NBUF = 2, BN = 64:  64 KB, 3 CTAs per SM.
+// NBUF = 2 runs the software-pipelined schedule (see the loop).
+template <int NBUF, int BN>
 constexpr size_t attn_smem() {
-    return (size_t)(3 + 2 * NBUF) * kTile + 64 + 1024;
+    return (size_t)kTile + (size_t)2 * NBUF * BN * 128 + (size_t)BN * 256 + 64 + 1024;
+}
+template <int NBUF, int BN>
+constexpr int attn_minb() {
+    return BN == 64 ? (NBUF == 1 ? 4 : 3) : (NBUF == 1 ? 2 : 1);
+}
+template <int BN>
+constexpr int attn_tmem_cols() {
+    return BN + kD <= 128 ? 128 : 256;
 }
 
-template <typename T, int NBUF, bool UP>
-__global__ void __launch_bounds__(kNT, 3 - NBUF)
+template <typename T, int NBUF, int BN, bool UP>
+__global__ void __launch_bounds__(kNT, attn_minb<NBUF, BN>())
     attention_tc_kernel(T* __restrict__ out, const T* __restrict__ q, const T* __restrict__ k,
                         const T* __restrict__ v, const int32_t* __restrict__ lengths, int H,
                         int S, float c) {
+    constexpr int kKV = BN * 128;  // bytes of one K or V tile
     extern __shared__ __align__(1024) unsigned char smem_raw[];
-    // 1024-aligned carve-up: Q | K[NBUF] | V[NBUF] | P0 P1 | barriers + TMEM slot
+    // 1024-aligned carve-up: Q | K[NBUF] | V[NBUF] | P | barriers + TMEM slot
     const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;
     unsigned char* sbase = smem_raw + (base - smem_u32(smem_raw));
-    const uint32_t sQ = base, sK = base + kTile, sV = base + (1 + NBUF) * kTile,
-                   sP = base + (1 + 2 * NBUF) * kTile;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sbase + (3 + 2 * NBUF) * kTile);
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sbase + (3 + 2 * NBUF) * kTile + 16);
+    const uint32_t sQ = base, sK = base + kTile, sV = base + kTile + NBUF * kKV,
+                   sP = base + kTile + 2 * NBUF * kKV;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sbase + kTile + 2 * NBUF * kKV + BN * 256);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sbase + kTile + 2 * NBUF * kKV + BN * 256 + 16);
 
     const int qt = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
     const int tid = threadIdx.x, warp = tid >> 5;
@@ -206,9 +224,10 @@ __global__ void __launch_bounds__(kNT, 3 - NBUF)
         return;
     }
 
-    if (warp == 0) {  // TMEM: S in columns [0,128), O in [128,192)
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(
-                         smem_u32(tmem_slot))
+    if (warp == 0) {  // TMEM: S in columns [0,BN), O in [BN,BN+64)
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         smem_u32(tmem_slot)),
+                     "n"(attn_tmem_cols<BN>())
                      : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
@@ -217,89 +236,80 @@ __global__ void __launch_bounds__(kNT, 3 - NBUF)
         mbar_init(&bars[1], 1);
         fence_mbar_init();
     }
-    const int nkt = (L + kBN - 1) / kBN;
+    const int nkt = (L + BN - 1) / BN;
     load_tile<T>(sQ, q + head, qt * kBM, S);
-    load_tile<T>(sK, k + head, 0, L);
-    load_tile<T>(sV, v + head, 0, L);
+    load_tile<T, BN>(sK, k + head, 0, L);
+    load_tile<T, BN>(sV, v + head, 0, L);
     cp_async_commit();
-    if (NBUF == 2 && nkt > 1) {
-        load_tile<T>(sK + kTile, k + head, kBN, L);
-        load_tile<T>(sV + kTile, v + head, kBN, L);
-    }
+    if (NBUF == 2 && nkt > 1) load_tile<T, BN>(sK + kKV, k + head, BN, L);  // K(1)
     cp_async_commit();
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
     const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
-    const uint32_t t_s = tmem + lane_off, t_o = tmem + 128 + lane_off;
+    const uint32_t t_s = tmem + lane_off, t_o = tmem + BN + lane_off;
 
     constexpr int kFmt = sizeof(T) == 2 && std::is_same<T, __nv_bfloat16>::value ? 1 : 0;
-    constexpr uint32_t idesc_s = f16_idesc(kFmt, 0, kBM, kBN);
+    constexpr uint32_t idesc_s = f16_idesc(kFmt, 0, kBM, BN);
     constexpr uint32_t idesc_o = f16_idesc(kFmt, 1, kBM, kD);
     // O and l are kept relative to a reference max m_ref (log2 units, scaled);
     // m_ref only moves -- and O is rescaled in TMEM -- when a tile's max
     // exceeds it by more than kRescale, so p = 2^(s c - m_ref) <= 2^kRescale.
     constexpr float kRescale = 8.f;
+    constexpr int NCH = BN / 32;
     const float sent = UP ? -INFINITY : INFINITY;
     float m_ref = -INFINITY, l_run = 0.f;
     uint32_t ph_s = 0, ph_o = 0;
     unsigned char* prow = sbase + (sP - base);
 
-    for (int kt = 0; kt < nkt; ++kt) {
-        const int st = NBUF == 2 ? (kt & 1) : 0;
-        if (NBUF == 2 && kt + 1 < nkt)
-            cp_async_wait<1>();
-        else
-            cp_async_wait<0>();
-        fence_proxy_async_smem();  // cp.async writes -> visible to the tensor core (async proxy)
-        tc_fence_before();
-        __syncthreads();
-        tc_fence_after();
-
-        // ---- S = Q K^T (K-major A and B, 4 K-steps of 16)
+    auto issue_s = [&](int kt) {  // S = Q K(kt)^T (K-major A and B, 4 K-steps of 16)
         if (tid == 0) {
-            const uint32_t kbase = sK + st * kTile;
+            const uint32_t kbase = sK + (NBUF == 2 ? (kt & 1) : 0) * kKV;
 #pragma unroll
             for (int ks = 0; ks < kD / 16; ++ks)
                 tc_mma(tmem, sw128_desc(sQ + ks * 32, 16, 1024),
                        sw128_desc(kbase + ks * 32, 16, 1024), idesc_s, ks > 0);
             tc_commit(&bars[0]);
         }
-        mbar_wait_bounded(&bars[0], ph_s);
-        ph_s ^= 1;
-        tc_fence_after();
-        if (NBUF == 1 && kt + 1 < nkt) {  // K consumed: stream the next K tile in now
-            load_tile<T>(sK, k + head, (kt + 1) * kBN, L);
-            cp_async_commit();
+    };
+    auto issue_pv = [&](int kt) {  // O += P V(kt) (P K-major; V MN-major, 2048 B per K-step)
+        if (tid == 0) {
+            const uint32_t vbase = sV + (NBUF == 2 ? (kt & 1) : 0) * kKV;
+#pragma unroll
+            for (int ks = 0; ks < BN / 16; ++ks)
+                tc_mma(tmem + BN, sw128_desc(sP + (ks >> 2) * kTile + (ks & 3) * 32, 16, 1024),
+                       sw128_desc(vbase + ks * 2048, 16384, 1024), idesc_o, (kt > 0 || ks > 0));
+            tc_commit(&bars[1]);
         }
-
-        // ---- this thread's row of S: 4 TMEM loads in flight, one wait
-        float sv[kBN];
-        {
-            uint32_t r[4][32];
+    };
+    // this thread's row of S: BN / 32 TMEM loads in flight, one wait
+    auto load_s = [&](float (&sv)[BN]) {
+        uint32_t r[NCH][32];
 #pragma unroll
-            for (int ch = 0; ch < 4; ++ch) tc_ld32_nowait(t_s + ch * 32, r[ch]);
-            tc_wait_ld();
+        for (int ch = 0; ch < NCH; ++ch) tc_ld32_nowait(t_s + ch * 32, r[ch]);
+        tc_wait_ld();
 #pragma unroll
-            for (int ch = 0; ch < 4; ++ch)
+        for (int ch = 0; ch < NCH; ++ch)
 #pragma unroll
-                for (int e = 0; e < 32; ++e) sv[ch * 32 + e] = __uint_as_float(r[ch][e]);
+            for (int e = 0; e < 32; ++e) sv[ch * 32 + e] = __uint_as_float(r[ch][e]);
+    };
+    // online softmax of tile kt from registers: mask (partial tile only), max,
+    // conditional O rescale (the previous P.V must have completed), then
+    // p = 2^(s c - m_ref) -> P in shared memory, row sum -> l
+    auto softmax_tile = [&](float (&sv)[BN], int kt) {
+        const int key0 = kt * BN;
+        if (key0 + BN > L) {
+#pragma unroll
+            for (int e = 0; e < BN; ++e) sv[e] = key0 + e < L ? sv[e] : sent;
         }
-        const int key0 = kt * kBN;
-        if (key0 + kBN > L) {  // the partial tile only: keys >= L -> sentinel
-#pragma unroll
-            for (int e = 0; e < kBN; ++e) sv[e] = key0 + e < L ? sv[e] : sent;
-        }
-        // max (UP) or min of the raw scores, then the scaled max
         float mx = sent;
 #pragma unroll
-        for (int e = 0; e < kBN; ++e) mx = UP ? fmaxf(mx, sv[e]) : fminf(mx, sv[e]);
+        for (int e = 0; e < BN; ++e) mx = UP ? fmaxf(mx, sv[e]) : fminf(mx, sv[e]);
         const float m_tile = mx * c;
         if (kt == 0) {
             m_ref = m_tile;  // nothing accumulated yet
         } else if (__any_sync(0xffffffffu, m_tile > m_ref + kRescale)) {
-            // rescale this warp's O rows (the previous P.V has completed)
             const float m_new = fmaxf(m_ref, m_tile);
             const float alpha = ex2_approx(m_ref - m_new);
             l_run *= alpha;
@@ -313,12 +323,10 @@ __global__ void __launch_bounds__(kNT, 3 - NBUF)
                 tc_st32(t_o + ch * 32, ov);
             }
         }
-
-        // ---- p = 2^(s c - m_ref) (masked keys: sentinel -> +0), row sum, P -> smem
         const F2 c2 = f2_make(c, c), nm2 = f2_make(-m_ref, -m_ref);
         F2 ps2 = f2_make(0.f, 0.f);
 #pragma unroll
-        for (int ch = 0; ch < 4; ++ch) {
+        for (int ch = 0; ch < NCH; ++ch) {
             float pv[32];
 #pragma unroll
             for (int e = 0; e < 32; e += 2) {
@@ -337,39 +345,91 @@ __global__ void __launch_bounds__(kNT, 3 - NBUF)
                 *reinterpret_cast<uint4*>(prow + off) = make_uint4(w.w[0], w.w[1], w.w[2], w.w[3]);
             }
         }
-        {
-            float a0, a1;
-            f2_split(ps2, a0, a1);
-            l_run += a0 + a1;
-        }
-        fence_proxy_async_smem();  // P (generic stores) -> tensor core
+        float a0, a1;
+        f2_split(ps2, a0, a1);
+        l_run += a0 + a1;
+    };
+    auto sync_for_mma = [&]() {  // generic-proxy smem writes (cp.async, P) -> tensor core
+        fence_proxy_async_smem();
         tc_fence_before();
         __syncthreads();
         tc_fence_after();
+    };
 
-        // ---- O += P V in TMEM (P K-major; V MN-major: 16 keys = 2048 B per K-step)
-        if (tid == 0) {
-            const uint32_t vbase = sV + st * kTile;
-#pragma unroll
-            for (int ks = 0; ks < kBN / 16; ++ks)
-                tc_mma(tmem + 128, sw128_desc(sP + (ks >> 2) * kTile + (ks & 3) * 32, 16, 1024),
-                       sw128_desc(vbase + ks * 2048, 16384, 1024), idesc_o, (kt > 0 || ks > 0));
-            tc_commit(&bars[1]);
+    if constexpr (NBUF == 1) {
+        // One K and one V buffer: K(kt+1) streams in during softmax(kt), V(kt+1)
+        // during the next S MMA.  cp.async groups in flight at the top of an
+        // iteration: K(kt), V(kt) -- wait for K only.
+        for (int kt = 0; kt < nkt; ++kt) {
+            cp_async_wait<1>();
+            sync_for_mma();
+            issue_s(kt);
+            mbar_wait_bounded(&bars[0], ph_s);
+            ph_s ^= 1;
+            tc_fence_after();
+            if (kt + 1 < nkt) {  // K consumed: stream the next K tile in now
+                load_tile<T, BN>(sK, k + head, (kt + 1) * BN, L);
+                cp_async_commit();
+            }
+            float sv[BN];
+            load_s(sv);
+            softmax_tile(sv, kt);
+            if (kt + 1 < nkt)  // V(kt) (K(kt + 1) may still be in flight)
+                cp_async_wait<1>();
+            else
+                cp_async_wait<0>();
+            sync_for_mma();
+            issue_pv(kt);
+            mbar_wait_bounded(&bars[1], ph_o);
+            ph_o ^= 1;
+            tc_fence_after();
+            if (kt + 1 < nkt) {  // V consumed by the P.V MMA
+                load_tile<T, BN>(sV, v + head, (kt + 1) * BN, L);
+                cp_async_commit();
+            }
         }
-        mbar_wait_bounded(&bars[1], ph_o);
+    } else {
+        // Software-pipelined, K and V double-buffered: S(kt+1) is issued as soon
+        // as S(kt) has been read out of TMEM, so it runs under softmax(kt); P.V(kt)
+        // runs under the next iteration's S wait and is only waited for when its
+        // buffers (P, V, O) are reused.  cp.async commit order: prologue {Q, K0,
+        // V0}, {K1}; then per iteration E: {K(kt+2)}, F: {V(kt+1)}.
+        cp_async_wait<1>();  // Q, K0, V0
+        sync_for_mma();
+        issue_s(0);
+        for (int kt = 0; kt < nkt; ++kt) {
+            mbar_wait_bounded(&bars[0], ph_s);  // A: S(kt)
+            ph_s ^= 1;
+            tc_fence_after();
+            float sv[BN];
+            load_s(sv);  // B
+            if (kt + 1 < nkt) {  // C, D: K(kt+1) ready and S read by every warp -> S(kt+1)
+                if (kt == 0)
+                    cp_async_wait<0>();
+                else
+                    cp_async_wait<1>();
+                sync_for_mma();
+                issue_s(kt + 1);
+            }
+            // E: K(kt) buffer is free (S(kt) completed)
+            if (kt + 2 < nkt) load_tile<T, BN>(sK + (kt & 1) * kKV, k + head, (kt + 2) * BN, L);
+            cp_async_commit();
+            // F: P.V(kt-1) done -> P, O and V((kt+1) & 1) are free
+            if (kt > 0) {
+                mbar_wait_bounded(&bars[1], ph_o);
+                ph_o ^= 1;
+                tc_fence_after();
+            }
+            if (kt + 1 < nkt) load_tile<T, BN>(sV + ((kt + 1) & 1) * kKV, v + head, (kt + 1) * BN, L);
+            cp_async_commit();
+            softmax_tile(sv, kt);
+            cp_async_wait<2>();  // G: V(kt) (K(kt+2), V(kt+1) may still be in flight)
+            sync_for_mma();
+            issue_pv(kt);
+        }
+        mbar_wait_bounded(&bars[1], ph_o);  // the last P.V
         ph_o ^= 1;
         tc_fence_after();
-        if constexpr (NBUF == 2) {
-            // stage st is free again: prefetch tile kt + 2 into it
-            if (kt + 2 < nkt) {
-                load_tile<T>(sK + st * kTile, k + head, (kt + 2) * kBN, L);
-                load_tile<T>(sV + st * kTile, v + head, (kt + 2) * kBN, L);
-            }
-            cp_async_commit();
-        } else if (kt + 1 < nkt) {  // V consumed by the P.V MMA
-            load_tile<T>(sV, v + head, (kt + 1) * kBN, L);
-            cp_async_commit();
-        }
     }
 
     // ---- o = O / l, narrowed, one 128-byte row per thread
@@ -396,22 +456,24 @@ __global__ void __launch_bounds__(kNT, 3 - NBUF)
     __syncthreads();
     if (warp == 0) {
         tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                     "n"(attn_tmem_cols<BN>())
                      : "memory");
     }
 }
 
 namespace {
-std::atomic<int> g_attn_nbuf{0};  // 0 = automatic (single-buffered, 2 CTAs / SM)
+std::atomic<int> g_attn_nbuf{0};  // 0 = automatic (variant 4)
 
-template <typename T, int NBUF>
+template <typename T, int NBUF, int BN>
 cudaError_t launch_attn(void* out, const void* q, const void* k, const void* v,
                         const int32_t* lengths, int64_t B, int64_t H, int64_t S, float scale,
                         cudaStream_t st) {
-    constexpr size_t smem = attn_smem<NBUF>();
+    constexpr size_t smem = attn_smem<NBUF, BN>();
     static std::atomic<int> attr{0};
     if (!attr.load()) {
-        for (auto kern : {attention_tc_kernel<T, NBUF, true>, attention_tc_kernel<T, NBUF, false>}) {
+        for (auto kern : {attention_tc_kernel<T, NBUF, BN, true>,
+                          attention_tc_kernel<T, NBUF, BN, false>}) {
             cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                  (int)smem);
             if (e != cudaSuccess) return e;
@@ -423,7 +485,8 @@ cudaError_t launch_attn(void* out, const void* q, const void* k, const void* v,
     // softmax kernels do), so the masked-key sentinel still maps to p = +0
     float c = scale * 1.4426950408889634f;
     if (c == 0.f) c = 1e-30f;
-    auto kern = c > 0.f ? attention_tc_kernel<T, NBUF, true> : attention_tc_kernel<T, NBUF, false>;
+    auto kern = c > 0.f ? attention_tc_kernel<T, NBUF, BN, true>
+                        : attention_tc_kernel<T, NBUF, BN, false>;
     kern<<<grid, kNT, smem, st>>>(static_cast<T*>(out), static_cast<const T*>(q),
                                   static_cast<const T*>(k), static_cast<const T*>(v), lengths,
                                   (int)H, (int)S, c);
@@ -434,14 +497,19 @@ template <typename T>
 cudaError_t launch_attn_any(void* out, const void* q, const void* k, const void* v,
                             const int32_t* lengths, int64_t B, int64_t H, int64_t S, float scale,
                             cudaStream_t st) {
-    if (g_attn_nbuf.load(std::memory_order_relaxed) == 2)
-        return launch_attn<T, 2>(out, q, k, v, lengths, B, H, S, scale, st);
-    return launch_attn<T, 1>(out, q, k, v, lengths, B, H, S, scale, st);
+    // automatic: 64-key tiles, pipelined (fastest on every BERT shape measured,
+    // profiles/r01_attn_bench.jsonl)
+    switch (g_attn_nbuf.load(std::memory_order_relaxed)) {
+        case 1: return launch_attn<T, 1, 128>(out, q, k, v, lengths, B, H, S, scale, st);
+        case 2: return launch_attn<T, 2, 128>(out, q, k, v, lengths, B, H, S, scale, st);
+        case 3: return launch_attn<T, 1, 64>(out, q, k, v, lengths, B, H, S, scale, st);
+        default: return launch_attn<T, 2, 64>(out, q, k, v, lengths, B, H, S, scale, st);
+    }
 }
 }  // namespace
 
 bool attention_force_variant(int v) {
-    if (v < 0 || v > 2) return false;
+    if (v < 0 || v > 4) return false;
     g_attn_nbuf.store(v);
     return true;
 }

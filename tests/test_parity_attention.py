@@ -15,9 +15,9 @@ DT = [torch.float16, torch.bfloat16]
 TOL = {torch.float16: 4e-3, torch.bfloat16: 8e-3}
 
 
-@pytest.fixture(params=[1, 2], ids=["nbuf1", "nbuf2"])
+@pytest.fixture(params=[1, 2, 3, 4], ids=["bn128", "bn128x2", "bn64", "bn64x2"])
 def variant(ttlib, request):
-    """Both K/V buffering variants of the kernel (ttx_attention_variant)."""
+    """Every kernel variant (ttx_attention_variant: tile width and K/V buffering)."""
     ttlib.attention_variant(request.param)
     yield request.param
     ttlib.attention_variant(0)
