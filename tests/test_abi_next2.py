@@ -39,3 +39,30 @@ def test_split_merge_validation(ttlib, dt):
     assert m(dt, P[0], P[0] + 8, 1, 2, 3, 8, 0) == INV                     # overlap
     assert m(dt, P[0] + 1, P[1], 1, 2, 3, 8, 0) == NS
     assert m(dt, 0, 0, 1, 0, 3, 8, 0) == OK
+
+
+@pytest.mark.parametrize("dt", [1, 2])
+def test_attention_validation(ttlib, dt):
+    """tt_attention_fwd (NEXT-3) host checks: every case returns before a CUDA call."""
+    f = ttlib.lib().tt_attention_fwd
+    far = 1 << 24
+    o, q, k, v, L = (FAKE + i * far for i in range(5))
+    assert f(dt, o, q, k, v, L, 2, 2, 8, 64, float("nan"), 0) == INV       # scale
+    assert f(dt, o, q, k, v, L, -1, 2, 8, 64, 0.125, 0) == INV             # negative dim
+    assert f(3, o, q, k, v, L, 2, 2, 8, 64, 0.125, 0) == INV               # dtype
+    assert f(dt, 0, q, k, v, L, 2, 2, 8, 64, 0.125, 0) == INV              # null out
+    assert f(dt, o, q, k, v, 0, 2, 2, 8, 64, 0.125, 0) == INV              # null lengths
+    assert f(dt, o, o + 64, k, v, L, 2, 2, 8, 64, 0.125, 0) == INV         # out overlaps q
+    assert f(dt, o, q, k, v, L, 2, 2, 8, 32, 0.125, 0) == NS               # head dim 32
+    assert f(0, o, q, k, v, L, 2, 2, 8, 64, 0.125, 0) == NS                # fp32
+    assert f(dt, o + 2, q, k, v, L, 2, 2, 8, 64, 0.125, 0) == NS           # misaligned out
+    assert f(dt, o, q, k, v, L + 2, 2, 2, 8, 64, 0.125, 0) == NS           # misaligned lengths
+    assert f(dt, 0, 0, 0, 0, 0, 0, 2, 8, 64, 0.125, 0) == OK               # empty: no-op
+
+
+def test_attention_variant_hook(ttlib):
+    h = ttlib.lib().ttx_attention_variant
+    for v in range(5):
+        assert h(v) == OK
+    assert h(-1) == INV and h(5) == INV
+    assert h(0) == OK
