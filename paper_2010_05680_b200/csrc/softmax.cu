@@ -191,7 +191,11 @@ __global__ void __launch_bounds__(NT, MINB) softmax_rows_kernel(T* __restrict__ 
 // ----------------------------------------------------------------------------
 // Rows [first, row_end) of this CTA, GC lanes per row, walked in warp-uniform
 // slabs (every lane of a warp runs the same number of passes).
-template <typename T, int VB, int GC, int NVC, int NT, bool ALIGNED, bool NARROW, bool UP>
+// PF: cross-row prefetch -- the loads of a group's next row are issued
+// before the current row is computed, so each warp keeps two rows in flight
+// (for rows under ~1 KB one row per warp is too few bytes in flight per SM).
+template <typename T, int VB, int GC, int NVC, int NT, bool ALIGNED, bool NARROW, bool UP,
+          bool PF = false>
 __device__ __forceinline__ void softmax_cta_rows(T* __restrict__ scores,
                                                  const int32_t* __restrict__ lengths,
                                                  uint32_t first, uint32_t row_end, FastDivU32 rpb,
@@ -202,6 +206,31 @@ __device__ __forceinline__ void softmax_cta_rows(T* __restrict__ scores,
     const uint32_t step = (NT / 32) * GPW;
     auto len_of = [&](uint32_t r) { return min(max(__ldg(lengths + rpb.div(r)), 0), Sk); };
     uint32_t row = first + (threadIdx.x >> 5) * GPW + lane / GC;
+    if constexpr (PF) {
+        using RR = RowRaw<T, VB, GC, NVC, ALIGNED>;
+        uint32_t base = first + (threadIdx.x >> 5) * GPW;
+        if (base >= row_end) return;  // warp-uniform
+        bool live = row < row_end;
+        int L = live ? (one_req ? Lcta : len_of(row)) : 0;
+        T* pc = scores + (size_t)(live ? row : first) * (size_t)Sk;
+        RR cur;
+        row_load<T, VB, GC, NVC, ALIGNED>(pc, L, Sk, q, cur);
+        for (; base < row_end; base += step, row += step) {
+            const uint32_t rn = row + step;
+            const bool ln = rn < row_end;
+            const int Ln = ln ? (one_req ? Lcta : len_of(rn)) : 0;
+            T* pn = scores + (size_t)(ln ? rn : first) * (size_t)Sk;
+            RR nxt;
+            if (base + step < row_end)  // warp-uniform: another pass follows
+                row_load<T, VB, GC, NVC, ALIGNED>(pn, Ln, Sk, q, nxt);
+            row_finish<T, VB, GC, NVC, ALIGNED, NARROW, UP>(pc, live, L, Sk, c, q, cur);
+            cur = nxt;
+            pc = pn;
+            L = Ln;
+            live = ln;
+        }
+        return;
+    }
     int Lnext = one_req ? Lcta : (row < row_end ? len_of(row) : 0);
     for (uint32_t base = first + (threadIdx.x >> 5) * GPW; base < row_end; base += step, row += step) {
         const bool live = row < row_end;
@@ -212,7 +241,7 @@ __device__ __forceinline__ void softmax_cta_rows(T* __restrict__ scores,
     }
 }
 
-template <typename T, int VB, int G, int NV, int NT, bool ALIGNED, bool UP>
+template <typename T, int VB, int G, int NV, int NT, bool ALIGNED, bool UP, bool PF>
 __device__ __forceinline__ void softmax_warp_body(T* __restrict__ scores,
                                                   const int32_t* __restrict__ lengths,
                                                   uint32_t nrows, FastDivU32 rpb, int Sk, float c,
@@ -233,29 +262,31 @@ __device__ __forceinline__ void softmax_warp_body(T* __restrict__ scores,
         constexpr bool ok4 = ALIGNED || 4 >= VE - 1, ok8 = ALIGNED || 8 >= VE - 1;
         if (one_req && Lcta < Sk) {
             if (ok4 && Lcta <= 4 * VE)
-                return softmax_cta_rows<T, VB, 4, 1, NT, ALIGNED, ok4, UP>(
+                return softmax_cta_rows<T, VB, 4, 1, NT, ALIGNED, ok4, UP, PF>(
                     scores, lengths, first, row_end, rpb, Sk, c, true, Lcta);
             if (ok8 && Lcta <= 8 * VE)
-                return softmax_cta_rows<T, VB, 8, 1, NT, ALIGNED, ok8, UP>(
+                return softmax_cta_rows<T, VB, 8, 1, NT, ALIGNED, ok8, UP, PF>(
                     scores, lengths, first, row_end, rpb, Sk, c, true, Lcta);
             if (Lcta <= 16 * VE)
-                return softmax_cta_rows<T, VB, 16, 1, NT, ALIGNED, true, UP>(
+                return softmax_cta_rows<T, VB, 16, 1, NT, ALIGNED, true, UP, PF>(
                     scores, lengths, first, row_end, rpb, Sk, c, true, Lcta);
         }
     }
-    softmax_cta_rows<T, VB, G, NV, NT, ALIGNED, false, UP>(scores, lengths, first, row_end, rpb, Sk,
-                                                           c, one_req, Lcta);
+    softmax_cta_rows<T, VB, G, NV, NT, ALIGNED, false, UP, PF>(scores, lengths, first, row_end,
+                                                               rpb, Sk, c, one_req, Lcta);
 }
 
-template <typename T, int VB, int G, int NV, int NT, int MINB, bool ALIGNED>
+template <typename T, int VB, int G, int NV, int NT, int MINB, bool ALIGNED, bool PF>
 __global__ void __launch_bounds__(NT, MINB) softmax_warp_kernel(T* __restrict__ scores,
                                                                 const int32_t* __restrict__ lengths,
                                                                 uint32_t nrows, FastDivU32 rpb,
                                                                 int Sk, float c, int rpg) {
     if (c > 0.f)  // uniform: the sign of the scale picks the max or min reduction
-        softmax_warp_body<T, VB, G, NV, NT, ALIGNED, true>(scores, lengths, nrows, rpb, Sk, c, rpg);
+        softmax_warp_body<T, VB, G, NV, NT, ALIGNED, true, PF>(scores, lengths, nrows, rpb, Sk, c,
+                                                               rpg);
     else
-        softmax_warp_body<T, VB, G, NV, NT, ALIGNED, false>(scores, lengths, nrows, rpb, Sk, c, rpg);
+        softmax_warp_body<T, VB, G, NV, NT, ALIGNED, false, PF>(scores, lengths, nrows, rpb, Sk, c,
+                                                                rpg);
 }
 
 // ----------------------------------------------------------------------------
@@ -500,7 +531,7 @@ cudaError_t launch_softmax(void* scores, const int32_t* lengths, int64_t nrows, 
 }
 
 
-template <typename T, int VB, int G, int NV, int NT, int MINB, int RPG>
+template <typename T, int VB, int G, int NV, int NT, int MINB, int RPG, bool PF = false>
 cudaError_t launch_softmax_warp(void* scores, const int32_t* lengths, int64_t nrows, int64_t rpb,
                                 int Sk, float scale, cudaStream_t st) {
     constexpr int GPB = NT / G;
@@ -508,8 +539,8 @@ cudaError_t launch_softmax_warp(void* scores, const int32_t* lengths, int64_t nr
         return launch_softmax<T, VB, G, NV, 1, NT, MINB>(scores, lengths, nrows, rpb, Sk, scale, st);
     const bool aligned = (reinterpret_cast<uintptr_t>(scores) % VB) == 0 &&
                          ((int64_t)Sk * (int64_t)sizeof(T)) % VB == 0;
-    auto kern = aligned ? softmax_warp_kernel<T, VB, G, NV, NT, MINB, true>
-                        : softmax_warp_kernel<T, VB, G, NV, NT, MINB, false>;
+    auto kern = aligned ? softmax_warp_kernel<T, VB, G, NV, NT, MINB, true, PF>
+                        : softmax_warp_kernel<T, VB, G, NV, NT, MINB, false, PF>;
     // RPG > 0: fixed rows per group; RPG = 0: one persistent wave (rows spread
     // evenly over SMs x resident CTAs).
     int rpg = RPG;
@@ -567,6 +598,13 @@ struct SoftmaxTier {
             &launch_softmax_warp<T, VB, G, NV, NT, MINB, RPG>,                             \
             "softmax_warp<" TN ",V" #VB ",G" #G ",NV" #NV ",T" #NT ",M" #MINB ",P" #RPG ">" \
     }
+// cross-row prefetch (two rows in flight per group)
+#define TT_SM_WARP_F(AUTO, T, TN, VB, G, NV, NT, MINB, RPG)                               \
+    SoftmaxTier {                                                                          \
+        (G) * (NV) * ((VB) / (int)sizeof(T)), AUTO,                                        \
+            &launch_softmax_warp<T, VB, G, NV, NT, MINB, RPG, true>,                       \
+            "softmax_warp<" TN ",V" #VB ",G" #G ",NV" #NV ",T" #NT ",M" #MINB ",P" #RPG ",F>" \
+    }
 // default: 4 rows per group per CTA
 #define TT_SM_WARP(AUTO, T, TN, VB, G, NV, NT, MINB) TT_SM_WARP_R(AUTO, T, TN, VB, G, NV, NT, MINB, 4)
 
@@ -606,7 +644,9 @@ struct SoftmaxTier {
     TT_SM_WARP(false, T, TN, 16, 16, 3, 256, 5), TT_SM_WARP(false, T, TN, 16, 8, 3, 256, 5),   \
     TT_SM_WARP(false, T, TN, 16, 8, 2, 256, 6), TT_SM_WARP(false, T, TN, 32, 8, 4, 256, 2),     \
     TT_SM_WARP(false, T, TN, 16, 8, 8, 256, 2), TT_SM_WARP(false, T, TN, 32, 16, 2, 256, 4),    \
-    TT_SM_WARP(false, T, TN, 16, 16, 4, 256, 4), TT_SM_WARP(false, T, TN, 32, 32, 1, 256, 4)
+    TT_SM_WARP(false, T, TN, 16, 16, 4, 256, 4), TT_SM_WARP(false, T, TN, 32, 32, 1, 256, 4),   \
+    TT_SM_WARP_F(false, T, TN, 32, 32, 1, 256, 6, 2), TT_SM_WARP_F(false, T, TN, 32, 32, 1, 256, 6, 4), \
+    TT_SM_WARP_F(false, T, TN, 32, 32, 1, 256, 5, 4), TT_SM_WARP_F(false, T, TN, 16, 8, 4, 256, 3, 4)
 
 // M2..M4: min CTAs/SM (register cap) of the NV = 2..4 warp tiers, chosen so
 // the row (NV * VE fp32 values per lane) fits without spilling.

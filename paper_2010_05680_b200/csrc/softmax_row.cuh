@@ -13,69 +13,93 @@ __device__ __forceinline__ float rcp_approx(float x) {
     return y;
 }
 
-// One row on a group of GC lanes (GC <= 32), NVC vectors per lane.  `live`
-// false: the group has no row this step (it still joins the shuffles, which use
-// the full warp mask).  NARROW: the request is short enough that every valid key
-// lies in the head and the first GC body vectors; the remaining body vectors
-// are written as zeros without any arithmetic.  UP: c > 0, so the row max of
-// c*x is c*max(x) (else c*min(x)); a template parameter so that only one of
-// the two reductions is compiled into each path.
-template <typename T, int VB, int GC, int NVC, bool ALIGNED, bool NARROW, bool UP>
-__device__ __forceinline__ void softmax_row_pass(T* __restrict__ p, bool live, int L, int Sk,
-                                                 float c, int q) {
+// Raw bytes of one row as loaded by one lane: NVC body vectors plus the
+// scalar head / tail elements (unaligned rows only).  Kept in registers
+// between row_load and row_finish, so a group can issue the loads of its next
+// row before it computes the current one (cross-row prefetch, PF tiers).
+template <typename T, int VB, int GC, int NVC, bool ALIGNED>
+struct RowRaw {
+    static constexpr int VE = VB / (int)sizeof(T);
+    static constexpr int HI = ALIGNED ? 0 : (VE - 1 + GC - 1) / GC;
+    static constexpr int HIA = HI > 0 ? HI : 1;
+    Raw<VB> raw[NVC];
+    T h[HIA], t[HIA];
+};
+
+// Head length and body vector count of a row starting at p.
+template <typename T, int VB, bool ALIGNED>
+__device__ __forceinline__ void row_split(const T* p, int Sk, int& hd, int& nv) {
     constexpr int VE = VB / (int)sizeof(T);
-    constexpr int HI = ALIGNED ? 0 : (VE - 1 + GC - 1) / GC;
-    constexpr int HIA = HI > 0 ? HI : 1;
-    constexpr bool up = UP;  // max of raw x (else min); c != 0 (host)
-    const float sent = up ? -INFINITY : INFINITY;
-    if (!live) L = 0;
-    int hd = 0, nv = Sk / VE;
+    hd = 0;
+    nv = Sk / VE;
     if constexpr (!ALIGNED) {
         const int mis = (int)((reinterpret_cast<uintptr_t>(p) & (VB - 1)) / sizeof(T));
         hd = mis ? min(VE - mis, Sk) : 0;
         nv = (Sk - hd) / VE;
     }
-    const int tl0 = hd + nv * VE;
-    // masking is needed unless every key is valid and every vector slot of
-    // the group maps onto the row (uniform within the group)
-    const bool masked = (L < Sk) || (nv != GC * NVC);
+}
 
-    // ---- SM-2: load (never predicated off; see above).  Every load of the
-    // row -- body vectors and the scalar head / tail -- is issued before any
-    // of them is consumed, so a row costs one memory round trip.  An empty
-    // row (L = 0, or a dead group) loads too; the mask below turns all of it
-    // into sentinels.
-    // fallback address for lanes past the prefix: the first body vector, or
-    // (row shorter than its head) the VB-aligned vector containing p
+// ---- SM-2 (issue half): every load of the row -- body vectors and the scalar
+// head / tail -- is issued before any of them is consumed, so a row costs one
+// memory round trip.  Loads are never predicated off: a lane past the valid
+// prefix (or every lane of an empty / dead row, L = 0) re-reads the first body
+// vector, or (row shorter than its head) the VB-aligned vector containing p;
+// the mask in row_finish turns those into sentinels.
+template <typename T, int VB, int GC, int NVC, bool ALIGNED>
+__device__ __forceinline__ void row_load(const T* __restrict__ p, int L, int Sk, int q,
+                                         RowRaw<T, VB, GC, NVC, ALIGNED>& r) {
+    using RR = RowRaw<T, VB, GC, NVC, ALIGNED>;
+    constexpr int VE = RR::VE;
+    int hd, nv;
+    row_split<T, VB, ALIGNED>(p, Sk, hd, nv);
     const T* fb = nv > 0 ? p + hd
                          : reinterpret_cast<const T*>(reinterpret_cast<uintptr_t>(p) &
                                                       ~(uintptr_t)(VB - 1));
-    Raw<VB> raw[NVC];
 #pragma unroll
     for (int k = 0; k < NVC; ++k) {
         const int vi = q + k * GC;
         const int j0 = hd + vi * VE;
         const bool in = vi < nv && j0 < L;
-        ld_stream<VB>(in ? p + j0 : fb, raw[k]);
+        ld_stream<VB>(in ? p + j0 : fb, r.raw[k]);
     }
-    // scalar head / tail: one pointer each, shared by the load and the store
-    // (an in-row key past L is loaded harmlessly and masked below)
-    T hraw[HIA], traw[HIA];
-    T* ph[HIA];
-    T* pt[HIA];
     if constexpr (!ALIGNED) {
+        // an in-row key past L is loaded harmlessly and masked in row_finish
+        const int tl0 = hd + nv * VE;
 #pragma unroll
-        for (int i = 0; i < HI; ++i) {
+        for (int i = 0; i < RR::HI; ++i) {
             const int jh = q + i * GC, jt = tl0 + q + i * GC;
-            ph[i] = p + (jh < hd ? jh : 0);
-            pt[i] = p + (jt < Sk ? jt : 0);
-            hraw[i] = *ph[i];
-            traw[i] = *pt[i];
+            r.h[i] = p[jh < hd ? jh : 0];
+            r.t[i] = p[jt < Sk ? jt : 0];
         }
     }
+}
+
+// SM-2 (mask half) .. SM-5 for one row whose raw bytes are in r.  `live`
+// false: the group has no row this step (it still joins the shuffles, which
+// use the full warp mask; L must be 0).  NARROW: the request is short enough
+// that every valid key lies in the head and the first GC body vectors; the
+// remaining body vectors are written as zeros without any arithmetic.  UP:
+// c > 0, so the row max of c*x is c*max(x) (else c*min(x)); a template
+// parameter so that only one of the two reductions is compiled into each path.
+template <typename T, int VB, int GC, int NVC, bool ALIGNED, bool NARROW, bool UP>
+__device__ __forceinline__ void row_finish(T* __restrict__ p, bool live, int L, int Sk, float c,
+                                           int q, const RowRaw<T, VB, GC, NVC, ALIGNED>& r) {
+    using RR = RowRaw<T, VB, GC, NVC, ALIGNED>;
+    constexpr int VE = RR::VE;
+    constexpr int HI = RR::HI;
+    constexpr int HIA = RR::HIA;
+    constexpr bool up = UP;  // max of raw x (else min); c != 0 (host)
+    const float sent = up ? -INFINITY : INFINITY;
+    int hd, nv;
+    row_split<T, VB, ALIGNED>(p, Sk, hd, nv);
+    const int tl0 = hd + nv * VE;
+    // masking is needed unless every key is valid and every vector slot of
+    // the group maps onto the row (uniform within the group)
+    const bool masked = (L < Sk) || (nv != GC * NVC);
+
     float v[NVC][VE];
 #pragma unroll
-    for (int k = 0; k < NVC; ++k) Elem<T>::template unpack<VB>(raw[k], v[k]);
+    for (int k = 0; k < NVC; ++k) Elem<T>::template unpack<VB>(r.raw[k], v[k]);
     if (masked) {
 #pragma unroll
         for (int k = 0; k < NVC; ++k) {
@@ -91,8 +115,8 @@ __device__ __forceinline__ void softmax_row_pass(T* __restrict__ p, bool live, i
         for (int i = 0; i < HI; ++i) {
             const int jh = q + i * GC, jt = tl0 + q + i * GC;
             const bool ih = jh < hd && jh < L, it = jt < Sk && jt < L;
-            hv[i] = ih ? Elem<T>::to_f(hraw[i]) : sent;
-            tv[i] = it ? Elem<T>::to_f(traw[i]) : sent;
+            hv[i] = ih ? Elem<T>::to_f(r.h[i]) : sent;
+            tv[i] = it ? Elem<T>::to_f(r.t[i]) : sent;
         }
     }
 
@@ -186,10 +210,20 @@ __device__ __forceinline__ void softmax_row_pass(T* __restrict__ p, bool live, i
 #pragma unroll
         for (int i = 0; i < HI; ++i) {
             const int jh = q + i * GC, jt = tl0 + q + i * GC;
-            if (jh < hd) *ph[i] = Elem<T>::from_f(hv[i] * inv);
-            if (jt < Sk) *pt[i] = Elem<T>::from_f(tv[i] * inv);
+            if (jh < hd) p[jh] = Elem<T>::from_f(hv[i] * inv);
+            if (jt < Sk) p[jt] = Elem<T>::from_f(tv[i] * inv);
         }
     }
+}
+
+// One row, load then finish (no prefetch).
+template <typename T, int VB, int GC, int NVC, bool ALIGNED, bool NARROW, bool UP>
+__device__ __forceinline__ void softmax_row_pass(T* __restrict__ p, bool live, int L, int Sk,
+                                                 float c, int q) {
+    if (!live) L = 0;
+    RowRaw<T, VB, GC, NVC, ALIGNED> r;
+    row_load<T, VB, GC, NVC, ALIGNED>(p, L, Sk, q, r);
+    row_finish<T, VB, GC, NVC, ALIGNED, NARROW, UP>(p, live, L, Sk, c, q, r);
 }
 
 }  // namespace tt
