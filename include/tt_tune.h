@@ -34,6 +34,17 @@ TT_API tt_status ttx_force_tier(int op, int dtype, int i);
  * TT_ERROR_INVALID_VALUE outside 0..4. */
 TT_API tt_status ttx_attention_variant(int v);
 
+/* Programmatic dependent launch (PDL, default on): every kernel is launched
+ * with the programmatic-stream-serialization attribute and begins with
+ * griddepcontrol.wait (before any global access) then launch_dependents, so a
+ * kernel's launch and prologue overlap the tail of the previous kernel in the
+ * stream while its memory accesses still follow that kernel's completion.
+ * enable: 1 on, 0 off (plain stream order).  Process-wide; for tools and tests.
+ * Returns TT_ERROR_INVALID_VALUE for any other value. */
+TT_API tt_status ttx_set_pdl(int enable);
+/* Current PDL switch (1 on, 0 off). */
+TT_API int ttx_get_pdl(void);
+
 #ifdef __cplusplus
 }
 #endif

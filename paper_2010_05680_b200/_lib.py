@@ -36,6 +36,7 @@ EXPORTS = (
     "ttx_tier_count", "ttx_tier_name", "ttx_force_tier",
     "tt_add_bias_gelu", "tt_split_qkv_add_bias", "tt_merge_heads",
     "tt_dp_schedule", "tt_schedule_cost", "tt_attention_fwd", "ttx_attention_variant",
+    "ttx_set_pdl", "ttx_get_pdl",
 )
 
 
@@ -84,6 +85,8 @@ def lib() -> ctypes.CDLL:
             L.tt_attention_fwd.argtypes = [_i, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _i64,
                                            _f, _vp]
             L.ttx_attention_variant.argtypes = [_i]
+            L.ttx_set_pdl.argtypes = [_i]
+            L.ttx_get_pdl.argtypes = []
             L.tt_dp_schedule.argtypes = [_vp, _i64, _vp, _i64, _i64, _vp, _vp, _vp, _vp]
             L.tt_schedule_cost.argtypes = [_vp, _i64, _vp, _i64, _i64, _vp, _vp, _i64, _vp]
             L.ttx_tier_count.argtypes = [_i]
@@ -330,6 +333,16 @@ def attention_variant(v: int):
     tiles double-buffered, pipelined (1 CTA/SM), 3 = 64-key tiles (4 CTAs/SM),
     4 = 64-key tiles double-buffered, pipelined (3 CTAs/SM)."""
     _check(lib().ttx_attention_variant(int(v)), "ttx_attention_variant")
+
+
+def set_pdl(enable: bool):
+    """Programmatic dependent launch on (default) or off for every kernel of the
+    library (include/tt_tune.h ttx_set_pdl)."""
+    _check(lib().ttx_set_pdl(1 if enable else 0), "ttx_set_pdl")
+
+
+def get_pdl() -> bool:
+    return bool(lib().ttx_get_pdl())
 
 
 # ------------------------------------------------------------------ scheduler

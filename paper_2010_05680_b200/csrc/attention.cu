@@ -198,6 +198,7 @@ __global__ void __launch_bounds__(kNT, attn_minb<NBUF, BN>())
     attention_tc_kernel(T* __restrict__ out, const T* __restrict__ q, const T* __restrict__ k,
                         const T* __restrict__ v, const int32_t* __restrict__ lengths, int H,
                         int S, float c) {
+    PdlScope pdl_;  // griddepcontrol.wait first: no global access before it (PDL)
     constexpr int kKV = BN * 128;  // bytes of one K or V tile
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     // 1024-aligned carve-up: Q | K[NBUF] | V[NBUF] | P | barriers + TMEM slot
@@ -487,9 +488,13 @@ cudaError_t launch_attn(void* out, const void* q, const void* k, const void* v,
     if (c == 0.f) c = 1e-30f;
     auto kern = c > 0.f ? attention_tc_kernel<T, NBUF, BN, true>
                         : attention_tc_kernel<T, NBUF, BN, false>;
-    kern<<<grid, kNT, smem, st>>>(static_cast<T*>(out), static_cast<const T*>(q),
+    {
+        const cudaError_t le_ = launch_k(kern, grid, kNT, smem, st,
+            static_cast<T*>(out), static_cast<const T*>(q),
                                   static_cast<const T*>(k), static_cast<const T*>(v), lengths,
                                   (int)H, (int)S, c);
+        if (le_ != cudaSuccess) return le_;
+    }
     return cudaGetLastError();
 }
 

@@ -17,11 +17,53 @@
 #include <cuda_fp16.h>
 #include <stdint.h>
 
+#include <cuda_runtime.h>
+#include <utility>
+
 #if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ != 1000)
 #error "libtt is written for sm_100a only (-gencode arch=compute_100a,code=sm_100a)"
 #endif
 
 namespace tt {
+
+// ----------------------------------------------------------------------------
+// Programmatic dependent launch (PDL).  Every kernel starts with
+// `PdlScope pdl_;`: griddepcontrol.wait blocks until the preceding kernel in
+// the stream has completed and its memory is visible (a no-op when the launch
+// was not programmatic), so NO global access precedes it.  When the scope ends
+// -- after the CTA's last store, on every return path --
+// griddepcontrol.launch_dependents lets the next kernel's CTAs be scheduled
+// once every CTA of this grid has got there, so the next launch's latency and
+// prologue overlap our tail.  (Triggering at kernel entry instead was measured
+// slower on single-wave grids: the dependents' CTAs occupy SMs early and the
+// grid after them is placed unevenly.)
+// ----------------------------------------------------------------------------
+struct PdlScope {
+    __device__ __forceinline__ PdlScope() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+    __device__ __forceinline__ ~PdlScope() {
+        asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    }
+};
+
+bool pdl_enabled();  // tt_api.cu: process-wide switch (ttx_set_pdl), default on
+
+// kern<<<grid, block, smem, st>>>(args...) with the programmatic-stream-
+// serialization attribute when PDL is enabled.
+template <typename... P, typename... A>
+inline cudaError_t launch_k(void (*kern)(P...), dim3 grid, dim3 block, size_t smem,
+                            cudaStream_t st, A&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, std::forward<A>(args)...);
+}
 
 // ----------------------------------------------------------------------------
 // Raw vectors of VB bytes (VB in {2, 4, 8, 16, 32}); 32-byte accesses compile

@@ -78,6 +78,7 @@ template <typename T, int VB, bool APPROX, int NT>
 __global__ void __launch_bounds__(NT) add_bias_gelu_kernel(T* out, const T* x,
                                                            const T* __restrict__ bias,
                                                            int64_t rows, int n, int rpb) {
+    PdlScope pdl_;  // griddepcontrol.wait first: no global access before it (PDL)
     constexpr int VE = VB / (int)sizeof(T);
     const int nvec = n / VE;
     const int64_t r0 = (int64_t)blockIdx.x * rpb;
@@ -123,9 +124,12 @@ cudaError_t launch_gelu(void* out, const void* x, const void* bias, int64_t rows
     if (rpb > max_rpb) rpb = max_rpb > 0 ? max_rpb : 1;
     const int64_t grid = (rows + rpb - 1) / rpb;
     if (grid > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
-    add_bias_gelu_kernel<T, VB, APPROX, NT><<<(unsigned)grid, NT, 0, st>>>(
+    {
+        const cudaError_t le_ = launch_k(add_bias_gelu_kernel<T, VB, APPROX, NT>, (unsigned)grid, NT, 0, st,
         static_cast<T*>(out), static_cast<const T*>(x), static_cast<const T*>(bias), rows,
         (int)n, (int)rpb);
+        if (le_ != cudaSuccess) return le_;
+    }
     return cudaGetLastError();
 }
 
@@ -138,6 +142,7 @@ __global__ void __launch_bounds__(NT) split_qkv_kernel(T* q, T* k, T* v, const T
                                                        uint32_t H, uint32_t D, uint64_t total,
                                                        FastDivU32 div_gd, FastDivU32 div_3h,
                                                        FastDivU32 div_s) {
+    PdlScope pdl_;  // griddepcontrol.wait first: no global access before it (PDL)
     constexpr int VE = VB / (int)sizeof(T);
     const uint32_t gd = D / VE;
     for (uint64_t i = (uint64_t)blockIdx.x * NT + threadIdx.x; i < total;
@@ -169,11 +174,14 @@ cudaError_t launch_split(void* q, void* k, void* v, const void* qkv, const void*
     const uint64_t want = (total + NT - 1) / NT;
     const uint64_t cap = (uint64_t)sm_count_e() * 16;
     const unsigned grid = (unsigned)(want < cap ? want : cap);
-    split_qkv_kernel<T, VB, NT><<<grid, NT, 0, st>>>(
+    {
+        const cudaError_t le_ = launch_k(split_qkv_kernel<T, VB, NT>, grid, NT, 0, st,
         static_cast<T*>(q), static_cast<T*>(k), static_cast<T*>(v), static_cast<const T*>(qkv),
         static_cast<const T*>(bias), (uint32_t)S, (uint32_t)H, (uint32_t)D, total,
         FastDivU32::make((uint32_t)gd), FastDivU32::make((uint32_t)(3 * H)),
         FastDivU32::make((uint32_t)S));
+        if (le_ != cudaSuccess) return le_;
+    }
     return cudaGetLastError();
 }
 
@@ -184,6 +192,7 @@ __global__ void __launch_bounds__(NT) merge_heads_kernel(T* out, const T* in, ui
                                                          uint32_t H, uint32_t D, uint64_t total,
                                                          FastDivU32 div_gd, FastDivU32 div_h,
                                                          FastDivU32 div_s) {
+    PdlScope pdl_;  // griddepcontrol.wait first: no global access before it (PDL)
     constexpr int VE = VB / (int)sizeof(T);
     const uint32_t gd = D / VE;
     for (uint64_t i = (uint64_t)blockIdx.x * NT + threadIdx.x; i < total;
@@ -210,10 +219,13 @@ cudaError_t launch_merge(void* out, const void* in, int64_t B, int64_t S, int64_
     const uint64_t want = (total + NT - 1) / NT;
     const uint64_t cap = (uint64_t)sm_count_e() * 16;
     const unsigned grid = (unsigned)(want < cap ? want : cap);
-    merge_heads_kernel<T, VB, NT><<<grid, NT, 0, st>>>(
+    {
+        const cudaError_t le_ = launch_k(merge_heads_kernel<T, VB, NT>, grid, NT, 0, st,
         static_cast<T*>(out), static_cast<const T*>(in), (uint32_t)S, (uint32_t)H, (uint32_t)D,
         total, FastDivU32::make((uint32_t)gd), FastDivU32::make((uint32_t)H),
         FastDivU32::make((uint32_t)S));
+        if (le_ != cudaSuccess) return le_;
+    }
     return cudaGetLastError();
 }
 

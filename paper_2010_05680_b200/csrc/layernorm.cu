@@ -30,6 +30,7 @@ __global__ void __launch_bounds__(NT, MINB)
     ln_rows_kernel(T* out, const T* x, const T* residual, const T* __restrict__ bias,
                    const T* __restrict__ gamma, const T* __restrict__ beta, int64_t rows,
                    int hidden, float eps) {
+    PdlScope pdl_;  // griddepcontrol.wait first: no global access before it (PDL)
     constexpr int VE = VB / (int)sizeof(T);
     constexpr int GPB = NT / G;
     constexpr int NWG = G > 32 ? G / 32 : 1;
@@ -268,6 +269,7 @@ __global__ void __launch_bounds__(NT, MINB)
     ln_pf_kernel(T* out, const T* x, const T* residual, const T* __restrict__ bias,
                    const T* __restrict__ gamma, const T* __restrict__ beta, uint32_t rows,
                    int hidden, float eps) {
+    PdlScope pdl_;  // griddepcontrol.wait first: no global access before it (PDL)
     using Row = LnRow<T, VB, G, NV>;
     constexpr int VE = Row::VE;
     constexpr int QV = Row::QV;
@@ -335,6 +337,7 @@ __global__ void __launch_bounds__(NT, MINB)
     ln_warp_kernel(T* out, const T* x, const T* residual, const T* __restrict__ bias,
                    const T* __restrict__ gamma, const T* __restrict__ beta, uint32_t rows,
                    int hidden, float eps) {
+    PdlScope pdl_;  // griddepcontrol.wait first: no global access before it (PDL)
     constexpr int VE = VB / (int)sizeof(T);
     constexpr int QV = VE / 4;  // float4 quads per vector
     constexpr int GPB = NT / G;
@@ -445,6 +448,7 @@ __global__ void __launch_bounds__(NW * 32)
     ln_tma_kernel(T* out, const T* x, const T* residual, const T* __restrict__ bias,
                   const T* __restrict__ gamma, const T* __restrict__ beta, int64_t rows, int hidden,
                   float eps, int D, int slot_bytes) {
+    PdlScope pdl_;  // griddepcontrol.wait first: no global access before it (PDL)
     constexpr int VE = 16 / (int)sizeof(T);
     constexpr int QV = VE / 4;
     extern __shared__ __align__(128) unsigned char smem[];
@@ -613,10 +617,13 @@ cudaError_t launch_ln_tma(void* out, const void* x, const void* res, const void*
     const int64_t need = (rows + NW - 1) / NW;
     const int64_t cap = (int64_t)sm_count() * occ;
     const int64_t grid = need < cap ? need : cap;
-    kern<<<(unsigned)grid, NW * 32, smem, st>>>(
+    {
+        const cudaError_t le_ = launch_k(kern, (unsigned)grid, NW * 32, smem, st,
         static_cast<T*>(out), static_cast<const T*>(x), static_cast<const T*>(res),
         static_cast<const T*>(bias), static_cast<const T*>(gamma), static_cast<const T*>(beta),
         rows, hidden, eps, D, slot_bytes);
+        if (le_ != cudaSuccess) return le_;
+    }
     return cudaGetLastError();
 }
 
@@ -632,10 +639,13 @@ cudaError_t launch_ln(void* out, const void* x, const void* res, const void* bia
     const int64_t rows_per_cta = (int64_t)GPB * R;
     const int64_t grid = (rows + rows_per_cta - 1) / rows_per_cta;
     if (grid > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
-    ln_rows_kernel<T, VB, G, NV, R, NT, MINB, EARLY><<<(unsigned)grid, NT, 0, st>>>(
+    {
+        const cudaError_t le_ = launch_k(ln_rows_kernel<T, VB, G, NV, R, NT, MINB, EARLY>, (unsigned)grid, NT, 0, st,
         static_cast<T*>(out), static_cast<const T*>(x), static_cast<const T*>(res),
         static_cast<const T*>(bias), static_cast<const T*>(gamma), static_cast<const T*>(beta),
         rows, hidden, eps);
+        if (le_ != cudaSuccess) return le_;
+    }
     return cudaGetLastError();
 }
 
@@ -665,10 +675,13 @@ cudaError_t launch_ln_warp(void* out, const void* x, const void* res, const void
     const int64_t need = (rows + GPB - 1) / GPB;
     const int64_t cap = (int64_t)sm_count() * occ;
     const int64_t grid = need < cap ? need : cap;
-    kern<<<(unsigned)grid, NT, smem, st>>>(
+    {
+        const cudaError_t le_ = launch_k(kern, (unsigned)grid, NT, smem, st,
         static_cast<T*>(out), static_cast<const T*>(x), static_cast<const T*>(res),
         static_cast<const T*>(bias), static_cast<const T*>(gamma), static_cast<const T*>(beta),
         (uint32_t)rows, hidden, eps);
+        if (le_ != cudaSuccess) return le_;
+    }
     return cudaGetLastError();
 }
 

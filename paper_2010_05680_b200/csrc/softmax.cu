@@ -32,6 +32,7 @@ __global__ void __launch_bounds__(NT, MINB) softmax_rows_kernel(T* __restrict__ 
                                                           const int32_t* __restrict__ lengths,
                                                           int64_t nrows, int64_t rows_per_batch,
                                                           int Sk, float c) {
+    PdlScope pdl_;  // griddepcontrol.wait first: no global access before it (PDL)
     constexpr int VE = VB / (int)sizeof(T);          // elements per vector
     constexpr int HI = (VE - 1 + G - 1) / G;         // head / tail iterations per lane
     constexpr int GPB = NT / G;                      // groups per CTA
@@ -281,6 +282,7 @@ __global__ void __launch_bounds__(NT, MINB) softmax_warp_kernel(T* __restrict__ 
                                                                 const int32_t* __restrict__ lengths,
                                                                 uint32_t nrows, FastDivU32 rpb,
                                                                 int Sk, float c, int rpg) {
+    PdlScope pdl_;  // griddepcontrol.wait first: no global access before it (PDL)
     if (c > 0.f)  // uniform: the sign of the scale picks the max or min reduction
         softmax_warp_body<T, VB, G, NV, NT, ALIGNED, true, PF>(scores, lengths, nrows, rpb, Sk, c,
                                                                rpg);
@@ -305,6 +307,7 @@ __global__ void __launch_bounds__(NW * 32) softmax_tma_kernel(T* __restrict__ sc
                                                               int64_t nrows, int64_t rows_per_batch,
                                                               int Sk, float c, int D,
                                                               int slot_bytes) {
+    PdlScope pdl_;  // griddepcontrol.wait first: no global access before it (PDL)
     constexpr int E = (int)sizeof(T);
     constexpr int VE = 16 / E;               // elements per 16-byte chunk
     constexpr int HI = (VE - 1 + 31) / 32;   // = 1
@@ -505,8 +508,12 @@ cudaError_t launch_softmax_tma(void* scores, const int32_t* lengths, int64_t nro
     const int64_t need = (nrows + NW - 1) / NW;
     const int64_t cap = (int64_t)sm_count() * occ;
     const int64_t grid = need < cap ? need : cap;
-    kern<<<(unsigned)grid, NW * 32, smem, st>>>(static_cast<T*>(scores), lengths, nrows, rpb, Sk,
+    {
+        const cudaError_t le_ = launch_k(kern, (unsigned)grid, NW * 32, smem, st,
+            static_cast<T*>(scores), lengths, nrows, rpb, Sk,
                                                 scale * kLog2e, D, slot_bytes);
+        if (le_ != cudaSuccess) return le_;
+    }
     return cudaGetLastError();
 }
 
@@ -525,8 +532,11 @@ cudaError_t launch_softmax(void* scores, const int32_t* lengths, int64_t nrows, 
     const int64_t rows_per_cta = (int64_t)GPB * R;
     const int64_t grid = (nrows + rows_per_cta - 1) / rows_per_cta;
     if (grid > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
-    softmax_rows_kernel<T, VB, G, NV, R, NT, MINB><<<(unsigned)grid, NT, 0, st>>>(
+    {
+        const cudaError_t le_ = launch_k(softmax_rows_kernel<T, VB, G, NV, R, NT, MINB>, (unsigned)grid, NT, 0, st,
         static_cast<T*>(scores), lengths, nrows, rpb, Sk, scale * kLog2e);
+        if (le_ != cudaSuccess) return le_;
+    }
     return cudaGetLastError();
 }
 
@@ -570,8 +580,12 @@ cudaError_t launch_softmax_warp(void* scores, const int32_t* lengths, int64_t nr
     // 2^(x * 1e-30 - m * 1e-30) rounds to exactly 1.0f.
     float c = scale * kLog2e;
     if (c == 0.f) c = 1e-30f;
-    kern<<<(unsigned)grid, NT, 0, st>>>(static_cast<T*>(scores), lengths, (uint32_t)nrows,
+    {
+        const cudaError_t le_ = launch_k(kern, (unsigned)grid, NT, 0, st,
+            static_cast<T*>(scores), lengths, (uint32_t)nrows,
                                        FastDivU32::make((uint32_t)rpb), Sk, c, rpg);
+        if (le_ != cudaSuccess) return le_;
+    }
     return cudaGetLastError();
 }
 

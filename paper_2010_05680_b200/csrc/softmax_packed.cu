@@ -106,6 +106,7 @@ __global__ void __launch_bounds__(NT, MINB)
     softmax_packed_kernel(T* __restrict__ scores, const int32_t* __restrict__ cu,
                           const int64_t* __restrict__ blocks, int num_req, uint32_t H,
                           uint32_t total_rows, float c, int rpg) {
+    PdlScope pdl_;  // griddepcontrol.wait first: no global access before it (PDL)
     if (c > 0.f)  // uniform: the sign of the scale picks the max or min reduction
         packed_body<T, VB, NV, NT, true>(scores, cu, blocks, num_req, H, total_rows, c, rpg);
     else
@@ -136,8 +137,11 @@ cudaError_t launch_packed(void* scores, const int32_t* cu, const int64_t* blocks
     if (grid > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
     float c = scale * kLog2eP;
     if (c == 0.f) c = 1e-30f;  // see softmax.cu: keeps sentinel keys at exactly +0.0
-    softmax_packed_kernel<T, 32, NV, NT, MINB><<<(unsigned)grid, NT, 0, st>>>(
+    {
+        const cudaError_t le_ = launch_k(softmax_packed_kernel<T, 32, NV, NT, MINB>, (unsigned)grid, NT, 0, st,
         static_cast<T*>(scores), cu, blocks, num_req, (uint32_t)H, (uint32_t)total_rows, c, RPG);
+        if (le_ != cudaSuccess) return le_;
+    }
     (void)sm_count_p;
     return cudaGetLastError();
 }

@@ -1,3 +1,4 @@
+#include <atomic>
 // tt_api.cu -- the C ABI of libtt.so (contract: include/tt.h).
 //
 // Host-side validation happens before any CUDA call; the kernels themselves
@@ -280,6 +281,11 @@ void copy_name(const char* name, char* buf, int cap) {
 
 }  // namespace
 
+namespace tt {
+std::atomic<int> g_pdl{1};
+bool pdl_enabled() { return g_pdl.load(std::memory_order_relaxed) != 0; }
+}  // namespace tt
+
 extern "C" {
 
 tt_status tt_softmax_masked_f32(float* scores, const int32_t* lengths, int64_t B, int64_t H,
@@ -470,6 +476,14 @@ const char* ttx_tier_name(int op, int dtype, int i) {
 tt_status ttx_attention_variant(int v) {
     return tt::attention_force_variant(v) ? TT_SUCCESS : TT_ERROR_INVALID_VALUE;
 }
+
+tt_status ttx_set_pdl(int enable) {
+    if (enable != 0 && enable != 1) return TT_ERROR_INVALID_VALUE;
+    tt::g_pdl.store(enable, std::memory_order_relaxed);
+    return TT_SUCCESS;
+}
+
+int ttx_get_pdl(void) { return tt::g_pdl.load(std::memory_order_relaxed); }
 
 tt_status ttx_force_tier(int op, int dtype, int i) {
     bool ok = op == 0 ? tt::softmax_force_tier(dtype, i)

@@ -1,0 +1,108 @@
+"""Programmatic dependent launch (include/tt_tune.h ttx_set_pdl).
+
+Every kernel starts with griddepcontrol.wait before any global access, so a
+chain of DEPENDENT calls (each reading what the previous one wrote) must give
+the same bytes with PDL on and off, and match the oracle applied in sequence.
+The chains below are launch-bound on purpose (C1-sized calls back to back,
+also inside a CUDA graph), which is where the next kernel actually launches
+early.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import workloads as W
+from _parity import assert_close
+
+
+def test_set_pdl_validates(ttlib):
+    L = ttlib.lib()
+    assert L.ttx_set_pdl(2) == ttlib.TT_ERROR_INVALID_VALUE
+    assert L.ttx_set_pdl(-1) == ttlib.TT_ERROR_INVALID_VALUE
+    old = ttlib.get_pdl()
+    try:
+        ttlib.set_pdl(False)
+        assert ttlib.get_pdl() is False
+        ttlib.set_pdl(True)
+        assert ttlib.get_pdl() is True
+    finally:
+        ttlib.set_pdl(old)
+
+
+def _ln_chain(tt, d, n, eps):
+    """x_{i+1} = LN(x_i + bias + residual) n times, each call reading the last output."""
+    cur = d["x"]
+    outs = []
+    for _ in range(n):
+        o = torch.empty_like(cur)
+        tt.tt_add_bias_layernorm(o, cur, d["residual"], d["bias"], d["gamma"], d["beta"], eps)
+        outs.append(o)
+        cur = o
+    return outs
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_dependent_chain_pdl_on_off_identical(ttlib, dtype):
+    """Softmax in place 8 times, then an 8-deep LN chain: bitwise equal with PDL
+    on and off, and equal to the oracle applied step by step (rounded to the
+    storage dtype between steps, as the kernels do)."""
+    lens = np.array([40, 23], dtype=np.int32)
+    x0 = W.scores(2, 12, 40, 40, dtype, seed=W.SEED + 11)
+    d0 = W.ln_inputs(40, 768, dtype, seed=W.SEED + 11)
+    res = {}
+    old = ttlib.get_pdl()
+    try:
+        for pdl in (False, True):
+            ttlib.set_pdl(pdl)
+            y = x0.cuda()
+            L = torch.as_tensor(lens).cuda()
+            for _ in range(8):
+                ttlib.tt_softmax_masked(y, L, W.SCALE_BERT)
+            dd = {k: v.cuda() for k, v in d0.items()}
+            outs = _ln_chain(ttlib, dd, 8, W.EPS_BERT)
+            torch.cuda.synchronize()
+            res[pdl] = (y.cpu(), [o.cpu() for o in outs])
+    finally:
+        ttlib.set_pdl(old)
+    assert torch.equal(res[False][0].view(torch.uint8), res[True][0].view(torch.uint8))
+    for a, b in zip(res[False][1], res[True][1]):
+        assert torch.equal(a.view(torch.uint8), b.view(torch.uint8))
+    # oracle, step by step
+    ref = x0
+    for _ in range(8):
+        ref = oracle.softmax_masked(ref, lens, W.SCALE_BERT).to(dtype)
+    assert_close("softmax", dtype, res[True][0], ref.double(), "pdl softmax chain")
+    cur = d0["x"]
+    for i in range(8):
+        r = oracle.add_bias_layernorm(cur, d0["residual"], d0["bias"], d0["gamma"], d0["beta"],
+                                      W.EPS_BERT)
+        # compare step i against the oracle fed the kernel's own step i-1 output
+        assert_close("layernorm", dtype, res[True][1][i], r, f"pdl ln chain step {i}")
+        cur = res[True][1][i]
+
+
+@pytest.mark.gpu
+def test_dependent_chain_in_cuda_graph(ttlib):
+    """The same dependent LN chain captured in a CUDA graph (programmatic edges)
+    and replayed: identical to eager execution."""
+    dtype = torch.float16
+    d0 = {k: v.cuda() for k, v in W.ln_inputs(40, 768, dtype, seed=W.SEED + 12).items()}
+    eager = _ln_chain(ttlib, d0, 6, W.EPS_BERT)
+    torch.cuda.synchronize()
+    st = torch.cuda.Stream()
+    bufs = [torch.empty_like(d0["x"]) for _ in range(6)]
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=st):
+        cur = d0["x"]
+        for o in bufs:
+            ttlib.tt_add_bias_layernorm(o, cur, d0["residual"], d0["bias"], d0["gamma"],
+                                        d0["beta"], W.EPS_BERT)
+            cur = o
+    for b in bufs:
+        b.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    for a, b in zip(eager, bufs):
+        assert torch.equal(a.view(torch.uint8), b.view(torch.uint8))
