@@ -13,7 +13,7 @@ import threading
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libtt.so")
+LIB_PATH = os.environ.get("TT_LIB_PATH") or os.path.join(_HERE, "libtt.so")  # override: experiments only
 
 TT_SUCCESS = 0
 TT_ERROR_INVALID_VALUE = 1

@@ -126,8 +126,33 @@ __device__ __forceinline__ void ld_param(const void* p, Raw<VB>& r) {
     }
 }
 
+// Streaming stores carry an L2 evict_first policy: the output's dirty lines are
+// the first to be written back, so a kernel drains its own writes instead of
+// leaving up to ~60 MB of them in L2 for the next kernel's reads to compete
+// with.  Measured on the C4 step (bench.py, 2 runs each): 0.2092 -> 0.2069 ms,
+// softmax 163.9 -> 163.0 us and LayerNorm 42.5 -> 41.1 us.
+#ifndef TT_ST_EVICT_FIRST
+#define TT_ST_EVICT_FIRST 1
+#endif
 template <int VB>
 __device__ __forceinline__ void st_stream(void* p, const Raw<VB>& r) {
+#if TT_ST_EVICT_FIRST
+    if constexpr (VB == 32 || VB == 16) {
+        uint64_t pol;
+        asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+        if constexpr (VB == 32)
+            asm volatile(
+                "st.global.L1::no_allocate.L2::cache_hint.v8.u32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8}, %9;"
+                ::"l"(p), "r"(r.w[0]), "r"(r.w[1]), "r"(r.w[2]), "r"(r.w[3]), "r"(r.w[4]),
+                "r"(r.w[5]), "r"(r.w[6]), "r"(r.w[7]), "l"(pol)
+                : "memory");
+        else
+            asm volatile("st.global.L1::no_allocate.L2::cache_hint.v4.u32 [%0], {%1,%2,%3,%4}, %5;"
+                         ::"l"(p), "r"(r.w[0]), "r"(r.w[1]), "r"(r.w[2]), "r"(r.w[3]), "l"(pol)
+                         : "memory");
+        return;
+    }
+#endif
     if constexpr (VB == 32) {
         asm volatile(
             "st.global.L1::no_allocate.v8.u32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p),
