@@ -30,8 +30,9 @@ TT_API tt_status ttx_force_tier(int op, int dtype, int i);
 /* Fused attention (tt_attention_fwd) variant: 0 = automatic, 1 = 128-key tiles
  * single-buffered (2 CTAs per SM), 2 = 128-key tiles double-buffered (1 CTA per
  * SM), 3 = 64-key tiles single-buffered (4 CTAs per SM), 4 = 64-key tiles
- * double-buffered and software-pipelined (3 CTAs per SM).  Returns
- * TT_ERROR_INVALID_VALUE outside 0..4. */
+ * double-buffered and software-pipelined (3 CTAs per SM), 5 = warp-specialised
+ * (producer warp, MMA warp, 4 softmax warps; mbarrier hand-offs, no CTA barrier
+ * in the tile loop; 2 CTAs per SM).  Returns TT_ERROR_INVALID_VALUE outside 0..5. */
 TT_API tt_status ttx_attention_variant(int v);
 
 /* Programmatic dependent launch (PDL, default on): every kernel is launched

@@ -331,7 +331,8 @@ def tt_attention_fwd(out, q, k, v, lengths, scale: float, stream=None):
 def attention_variant(v: int):
     """0 = automatic, 1 = 128-key tiles single-buffered (2 CTAs/SM), 2 = 128-key
     tiles double-buffered, pipelined (1 CTA/SM), 3 = 64-key tiles (4 CTAs/SM),
-    4 = 64-key tiles double-buffered, pipelined (3 CTAs/SM)."""
+    4 = 64-key tiles double-buffered, pipelined (3 CTAs/SM), 5 = warp-specialised
+    (producer / MMA / softmax warps, mbarrier hand-offs, 2 CTAs/SM)."""
     _check(lib().ttx_attention_variant(int(v)), "ttx_attention_variant")
 
 

@@ -463,6 +463,269 @@ __global__ void __launch_bounds__(kNT, attn_minb<NBUF, BN>())
     }
 }
 
+
+// ----------------------------------------------------------------------------
+// Warp-specialised variant (ttx_attention_variant 5): no CTA-wide barrier in
+// the tile loop.  6 warps, 128 query rows, 64-key tiles:
+//   warps 0-3  softmax: thread t owns query row t (TMEM lane t);
+//   warp  4    producer: cp.async of Q, K(t), V(t) into 2-stage rings;
+//   warp  5    MMA issuer (one lane) and TMEM owner.
+// TMEM: S double-buffered in columns [0, 64) and [64, 128), O in [128, 192).
+// Shared: Q 16 KB | K 2 x 8 KB | V 2 x 8 KB | P 2 x 16 KB | mbarriers.
+// Hand-offs are mbarriers, slot i = tile & 1, phase = (tile >> 1) & 1:
+//   kfull/vfull  producer -> MMA (cp.async complete + proxy fence)
+//   sfull        MMA commit after S(t): S ready, and K slot free for the producer
+//   sfree        4 softmax warps -> MMA: S(t) read out of TMEM
+//   pfull        4 softmax warps -> MMA: P(t) in shared memory (and any O rescale done)
+//   pvdone       MMA commit after P.V(t): P and V slots free, O updated
+// The MMA lane issues S(t+1) before waiting for P(t), so QK^T of the next tile
+// runs under the softmax of this one; softmax(t) waits for P.V(t-1) only when
+// it must rescale O (rare) and for P.V(t-2) before reusing its P buffer.
+// ----------------------------------------------------------------------------
+constexpr int kWsThreads = 192;
+constexpr size_t kWsSmem = (size_t)kTile + 4 * 8192 + 2 * kTile + 16 * 8 + 16 + 1024;
+
+// rows [row0, row0 + ROWS) of a [S, 64] 16-bit matrix by one warp
+template <typename T, int ROWS>
+__device__ __forceinline__ void load_tile_warp(uint32_t tile, const T* g, int row0, int valid,
+                                               int lane) {
+#pragma unroll
+    for (int i = 0; i < (ROWS * 8) / 32; ++i) {
+        const int idx = lane + i * 32;
+        const int r = idx >> 3, c = idx & 7;
+        const bool in = row0 + r < valid;
+        const T* src = g + (size_t)(in ? row0 + r : 0) * kD + c * 8;
+        cp_async16(tile + sw_off(r, c), src, in ? 16u : 0u);
+    }
+}
+
+template <typename T, bool UP>
+__global__ void __launch_bounds__(kWsThreads, 2)
+    attention_ws_kernel(T* __restrict__ out, const T* __restrict__ q, const T* __restrict__ k,
+                        const T* __restrict__ v, const int32_t* __restrict__ lengths, int H, int S,
+                        float c) {
+    PdlScope pdl_;  // griddepcontrol.wait first: no global access before it (PDL)
+    constexpr int BN = 64;
+    constexpr int kKV = BN * 128;  // 8 KB
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;
+    unsigned char* sbase = smem_raw + (base - smem_u32(smem_raw));
+    const uint32_t sQ = base, sK = base + kTile, sV = sK + 2 * kKV, sP = sV + 2 * kKV;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sbase + kTile + 4 * kKV + 2 * kTile);
+    uint64_t* kfull = bars;       // [2]
+    uint64_t* vfull = bars + 2;   // [2]
+    uint64_t* sfull = bars + 4;   // [2]
+    uint64_t* sfree = bars + 6;   // [2]
+    uint64_t* pfull = bars + 8;   // [2]
+    uint64_t* pvdone = bars + 10; // [2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
+
+    const int qt = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int L = min(max(__ldg(lengths + b), 0), S);
+    const size_t head = ((size_t)b * H + h) * (size_t)S * kD;
+
+    if (L == 0) {  // no valid key: the output rows are zero
+        const int row = qt * kBM + tid;
+        if (tid < kBM && row < S) {
+            uint4 z = make_uint4(0, 0, 0, 0);
+#pragma unroll
+            for (int i = 0; i < kD * 2 / 16; ++i)
+                reinterpret_cast<uint4*>(out + head + (size_t)row * kD)[i] = z;
+        }
+        return;
+    }
+    if (warp == 5) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(
+                         smem_u32(tmem_slot))
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    if (tid == 0) {
+        for (int i = 0; i < 4; ++i) mbar_init(&bars[i], 1);        // kfull, vfull: producer lane 0
+        for (int i = 4; i < 6; ++i) mbar_init(&bars[i], 1);        // sfull: MMA commit
+        for (int i = 6; i < 10; ++i) mbar_init(&bars[i], 4);       // sfree, pfull: 4 softmax warps
+        for (int i = 10; i < 12; ++i) mbar_init(&bars[i], 1);      // pvdone: MMA commit
+        fence_mbar_init();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    const int nkt = (L + BN - 1) / BN;
+    constexpr int kFmt = sizeof(T) == 2 && std::is_same<T, __nv_bfloat16>::value ? 1 : 0;
+
+    if (warp == 4) {
+        // ---------------- producer
+        for (int t = 0; t < nkt; ++t) {
+            const int s = t & 1;
+            if (t >= 2) mbar_wait_bounded(&sfull[s], ((t - 2) >> 1) & 1);  // S(t-2): K slot free
+            if (t == 0) load_tile_warp<T, kBM>(sQ, q + head, qt * kBM, S, lane);
+            load_tile_warp<T, BN>(sK + s * kKV, k + head, t * BN, L, lane);
+            cp_async_commit();
+            if (t >= 2) mbar_wait_bounded(&pvdone[s], ((t - 2) >> 1) & 1);  // P.V(t-2): V slot free
+            load_tile_warp<T, BN>(sV + s * kKV, v + head, t * BN, L, lane);
+            cp_async_commit();
+            cp_async_wait<1>();  // Q, K(t)
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&kfull[s]);
+            cp_async_wait<0>();  // V(t)
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&vfull[s]);
+        }
+    } else if (warp == 5) {
+        // ---------------- MMA issuer
+        if (lane == 0) {
+            constexpr uint32_t idesc_s = f16_idesc(kFmt, 0, kBM, BN);
+            constexpr uint32_t idesc_o = f16_idesc(kFmt, 1, kBM, kD);
+            auto issue_pv = [&](int j) {
+                const int s = j & 1;
+                mbar_wait_bounded(&pfull[s], (j >> 1) & 1);
+                mbar_wait_bounded(&vfull[s], (j >> 1) & 1);
+                tc_fence_after();
+                const uint32_t pb = sP + s * kTile, vb = sV + s * kKV;
+#pragma unroll
+                for (int ks = 0; ks < BN / 16; ++ks)
+                    tc_mma(tmem + 128, sw128_desc(pb + ks * 32, 16, 1024),
+                           sw128_desc(vb + ks * 2048, 16384, 1024), idesc_o, (j > 0 || ks > 0));
+                tc_commit(&pvdone[s]);
+            };
+            for (int t = 0; t < nkt; ++t) {
+                const int s = t & 1;
+                mbar_wait_bounded(&kfull[s], (t >> 1) & 1);
+                if (t >= 2) mbar_wait_bounded(&sfree[s], ((t - 2) >> 1) & 1);
+                tc_fence_after();
+                const uint32_t kb = sK + s * kKV;
+#pragma unroll
+                for (int ks = 0; ks < kD / 16; ++ks)
+                    tc_mma(tmem + s * BN, sw128_desc(sQ + ks * 32, 16, 1024),
+                           sw128_desc(kb + ks * 32, 16, 1024), idesc_s, ks > 0);
+                tc_commit(&sfull[s]);
+                if (t >= 1) issue_pv(t - 1);
+            }
+            issue_pv(nkt - 1);
+        }
+        __syncwarp();
+    } else {
+        // ---------------- softmax warps: thread tid = query row tid
+        const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
+        const uint32_t t_o = tmem + 128 + lane_off;
+        constexpr float kRescale = 8.f;
+        const float sent = UP ? -INFINITY : INFINITY;
+        float m_ref = -INFINITY, l_run = 0.f;
+        unsigned char* pbase = sbase + (sP - base);
+        for (int t = 0; t < nkt; ++t) {
+            const int s = t & 1;
+            mbar_wait_bounded(&sfull[s], (t >> 1) & 1);
+            tc_fence_after();
+            float sv[BN];
+            {
+                uint32_t r[2][32];
+                tc_ld32_nowait(tmem + s * BN + lane_off, r[0]);
+                tc_ld32_nowait(tmem + s * BN + 32 + lane_off, r[1]);
+                tc_wait_ld();
+#pragma unroll
+                for (int ch = 0; ch < 2; ++ch)
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) sv[ch * 32 + e] = __uint_as_float(r[ch][e]);
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&sfree[s]);
+            const int key0 = t * BN;
+            if (key0 + BN > L) {
+#pragma unroll
+                for (int e = 0; e < BN; ++e) sv[e] = key0 + e < L ? sv[e] : sent;
+            }
+            float mx = sent;
+#pragma unroll
+            for (int e = 0; e < BN; ++e) mx = UP ? fmaxf(mx, sv[e]) : fminf(mx, sv[e]);
+            const float m_tile = mx * c;
+            if (t == 0) {
+                m_ref = m_tile;
+            } else if (__any_sync(0xffffffffu, m_tile > m_ref + kRescale)) {
+                // O must hold P.V(t-1) before it is rescaled
+                mbar_wait_bounded(&pvdone[(t - 1) & 1], ((t - 1) >> 1) & 1);
+                tc_fence_after();
+                const float m_new = fmaxf(m_ref, m_tile);
+                const float alpha = ex2_approx(m_ref - m_new);
+                l_run *= alpha;
+                m_ref = m_new;
+#pragma unroll
+                for (int ch = 0; ch < kD / 32; ++ch) {
+                    float ov[32];
+                    tc_ld32(t_o + ch * 32, ov);
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) ov[e] *= alpha;
+                    tc_st32(t_o + ch * 32, ov);
+                }
+            }
+            // P buffer s is free once P.V(t-2) has completed
+            if (t >= 2) mbar_wait_bounded(&pvdone[s], ((t - 2) >> 1) & 1);
+            const F2 c2 = f2_make(c, c), nm2 = f2_make(-m_ref, -m_ref);
+            F2 ps2 = f2_make(0.f, 0.f);
+            unsigned char* prow = pbase + s * kTile;
+#pragma unroll
+            for (int ch = 0; ch < 2; ++ch) {
+                float pv[32];
+#pragma unroll
+                for (int e = 0; e < 32; e += 2) {
+                    float t0, t1;
+                    f2_split(f2_fma(f2_make(sv[ch * 32 + e], sv[ch * 32 + e + 1]), c2, nm2), t0,
+                             t1);
+                    pv[e] = ex2_approx(t0);
+                    pv[e + 1] = ex2_approx(t1);
+                    ps2 = f2_add(ps2, f2_make(pv[e], pv[e + 1]));
+                }
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    Raw<16> w;
+                    Elem<T>::template pack<16>(pv + 8 * j, w);
+                    *reinterpret_cast<uint4*>(prow + sw_off(tid, ch * 4 + j)) =
+                        make_uint4(w.w[0], w.w[1], w.w[2], w.w[3]);
+                }
+            }
+            float a0, a1;
+            f2_split(ps2, a0, a1);
+            l_run += a0 + a1;
+            fence_proxy_async_smem();  // P (generic proxy) -> tensor core (async proxy)
+            tc_fence_before();         // and any O rescale (tcgen05.st)
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&pfull[s]);
+        }
+        // ---- o = O / l after the last P.V
+        mbar_wait_bounded(&pvdone[(nkt - 1) & 1], ((nkt - 1) >> 1) & 1);
+        tc_fence_after();
+        uint32_t r[2][32];
+        tc_ld32_nowait(t_o, r[0]);
+        tc_ld32_nowait(t_o + 32, r[1]);
+        tc_wait_ld();
+        const int row = qt * kBM + tid;
+        if (row < S) {
+            const float inv = 1.0f / l_run;
+            T* orow = out + head + (size_t)row * kD;
+#pragma unroll
+            for (int j = 0; j < kD / 8; ++j) {
+                float y[8];
+#pragma unroll
+                for (int e = 0; e < 8; ++e) y[e] = __uint_as_float(r[j >> 2][(j & 3) * 8 + e]) * inv;
+                Raw<16> w;
+                Elem<T>::template pack<16>(y, w);
+                reinterpret_cast<uint4*>(orow)[j] = make_uint4(w.w[0], w.w[1], w.w[2], w.w[3]);
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 5) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem)
+                     : "memory");
+    }
+}
+
 namespace {
 std::atomic<int> g_attn_nbuf{0};  // 0 = automatic (variant 4)
 
@@ -499,6 +762,30 @@ cudaError_t launch_attn(void* out, const void* q, const void* k, const void* v,
 }
 
 template <typename T>
+cudaError_t launch_attn_ws(void* out, const void* q, const void* k, const void* v,
+                           const int32_t* lengths, int64_t B, int64_t H, int64_t S, float scale,
+                           cudaStream_t st) {
+    static std::atomic<int> attr{0};
+    if (!attr.load()) {
+        for (auto kern : {attention_ws_kernel<T, true>, attention_ws_kernel<T, false>}) {
+            cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)kWsSmem);
+            if (e != cudaSuccess) return e;
+        }
+        attr.store(1);
+    }
+    dim3 grid((unsigned)((S + kBM - 1) / kBM), (unsigned)H, (unsigned)B);
+    float c = scale * 1.4426950408889634f;
+    if (c == 0.f) c = 1e-30f;
+    auto kern = c > 0.f ? attention_ws_kernel<T, true> : attention_ws_kernel<T, false>;
+    const cudaError_t le_ = launch_k(kern, grid, kWsThreads, kWsSmem, st, static_cast<T*>(out),
+                                     static_cast<const T*>(q), static_cast<const T*>(k),
+                                     static_cast<const T*>(v), lengths, (int)H, (int)S, c);
+    if (le_ != cudaSuccess) return le_;
+    return cudaGetLastError();
+}
+
+template <typename T>
 cudaError_t launch_attn_any(void* out, const void* q, const void* k, const void* v,
                             const int32_t* lengths, int64_t B, int64_t H, int64_t S, float scale,
                             cudaStream_t st) {
@@ -508,13 +795,14 @@ cudaError_t launch_attn_any(void* out, const void* q, const void* k, const void*
         case 1: return launch_attn<T, 1, 128>(out, q, k, v, lengths, B, H, S, scale, st);
         case 2: return launch_attn<T, 2, 128>(out, q, k, v, lengths, B, H, S, scale, st);
         case 3: return launch_attn<T, 1, 64>(out, q, k, v, lengths, B, H, S, scale, st);
+        case 5: return launch_attn_ws<T>(out, q, k, v, lengths, B, H, S, scale, st);
         default: return launch_attn<T, 2, 64>(out, q, k, v, lengths, B, H, S, scale, st);
     }
 }
 }  // namespace
 
 bool attention_force_variant(int v) {
-    if (v < 0 || v > 4) return false;
+    if (v < 0 || v > 5) return false;
     g_attn_nbuf.store(v);
     return true;
 }
