@@ -126,18 +126,17 @@ __device__ __forceinline__ void ld_param(const void* p, Raw<VB>& r) {
     }
 }
 
-// Streaming stores carry an L2 evict_first policy: the output's dirty lines are
-// the first to be written back, so a kernel drains its own writes instead of
-// leaving up to ~60 MB of them in L2 for the next kernel's reads to compete
-// with.  Measured on the C4 step (bench.py, 2 runs each): 0.2092 -> 0.2069 ms,
-// softmax 163.9 -> 163.0 us and LayerNorm 42.5 -> 41.1 us.
-#ifndef TT_ST_EVICT_FIRST
-#define TT_ST_EVICT_FIRST 1
-#endif
-template <int VB>
+// Streaming store.  EF: with an L2 evict_first cache policy, so the output's
+// dirty lines are the first the L2 writes back and a kernel drains its own
+// writes instead of leaving up to ~60 MB of them for the next kernel's reads to
+// compete with.  Used by the softmax warp tiers on rows made of whole 128-byte
+// lines (C4 step, bench.py, 2 runs each: 0.2091 -> 0.2066 ms).  Measured slower
+// elsewhere (fp16 hidden-768 LayerNorm -11 %, softmax rows sharing a line with
+// the next row -4.5..-6 %: the line is evicted half-written), so every other
+// store is plain.
+template <int VB, bool EF = false>
 __device__ __forceinline__ void st_stream(void* p, const Raw<VB>& r) {
-#if TT_ST_EVICT_FIRST
-    if constexpr (VB == 32 || VB == 16) {
+    if constexpr (EF && (VB == 32 || VB == 16)) {
         uint64_t pol;
         asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
         if constexpr (VB == 32)
@@ -152,7 +151,6 @@ __device__ __forceinline__ void st_stream(void* p, const Raw<VB>& r) {
                          : "memory");
         return;
     }
-#endif
     if constexpr (VB == 32) {
         asm volatile(
             "st.global.L1::no_allocate.v8.u32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p),

@@ -196,7 +196,7 @@ __global__ void __launch_bounds__(NT, MINB) softmax_rows_kernel(T* __restrict__ 
 // before the current row is computed, so each warp keeps two rows in flight
 // (for rows under ~1 KB one row per warp is too few bytes in flight per SM).
 template <typename T, int VB, int GC, int NVC, int NT, bool ALIGNED, bool NARROW, bool UP,
-          bool PF = false>
+          bool PF = false, bool EF = false>
 __device__ __forceinline__ void softmax_cta_rows(T* __restrict__ scores,
                                                  const int32_t* __restrict__ lengths,
                                                  uint32_t first, uint32_t row_end, FastDivU32 rpb,
@@ -224,7 +224,7 @@ __device__ __forceinline__ void softmax_cta_rows(T* __restrict__ scores,
             RR nxt;
             if (base + step < row_end)  // warp-uniform: another pass follows
                 row_load<T, VB, GC, NVC, ALIGNED>(pn, Ln, Sk, q, nxt);
-            row_finish<T, VB, GC, NVC, ALIGNED, NARROW, UP>(pc, live, L, Sk, c, q, cur);
+            row_finish<T, VB, GC, NVC, ALIGNED, NARROW, UP, EF>(pc, live, L, Sk, c, q, cur);
             cur = nxt;
             pc = pn;
             L = Ln;
@@ -237,12 +237,15 @@ __device__ __forceinline__ void softmax_cta_rows(T* __restrict__ scores,
         const bool live = row < row_end;
         const int L = Lnext;
         if (!one_req && row + step < row_end) Lnext = len_of(row + step);
-        softmax_row_pass<T, VB, GC, NVC, ALIGNED, NARROW, UP>(
-            scores + (size_t)(live ? row : first) * (size_t)Sk, live, L, Sk, c, q);
+        T* p = scores + (size_t)(live ? row : first) * (size_t)Sk;
+        const int Lr = live ? L : 0;
+        RowRaw<T, VB, GC, NVC, ALIGNED> rr;
+        row_load<T, VB, GC, NVC, ALIGNED>(p, Lr, Sk, q, rr);
+        row_finish<T, VB, GC, NVC, ALIGNED, NARROW, UP, EF>(p, live, Lr, Sk, c, q, rr);
     }
 }
 
-template <typename T, int VB, int G, int NV, int NT, bool ALIGNED, bool UP, bool PF>
+template <typename T, int VB, int G, int NV, int NT, bool ALIGNED, bool UP, bool PF, bool EF>
 __device__ __forceinline__ void softmax_warp_body(T* __restrict__ scores,
                                                   const int32_t* __restrict__ lengths,
                                                   uint32_t nrows, FastDivU32 rpb, int Sk, float c,
@@ -263,31 +266,31 @@ __device__ __forceinline__ void softmax_warp_body(T* __restrict__ scores,
         constexpr bool ok4 = ALIGNED || 4 >= VE - 1, ok8 = ALIGNED || 8 >= VE - 1;
         if (one_req && Lcta < Sk) {
             if (ok4 && Lcta <= 4 * VE)
-                return softmax_cta_rows<T, VB, 4, 1, NT, ALIGNED, ok4, UP, PF>(
+                return softmax_cta_rows<T, VB, 4, 1, NT, ALIGNED, ok4, UP, PF, EF>(
                     scores, lengths, first, row_end, rpb, Sk, c, true, Lcta);
             if (ok8 && Lcta <= 8 * VE)
-                return softmax_cta_rows<T, VB, 8, 1, NT, ALIGNED, ok8, UP, PF>(
+                return softmax_cta_rows<T, VB, 8, 1, NT, ALIGNED, ok8, UP, PF, EF>(
                     scores, lengths, first, row_end, rpb, Sk, c, true, Lcta);
             if (Lcta <= 16 * VE)
-                return softmax_cta_rows<T, VB, 16, 1, NT, ALIGNED, true, UP, PF>(
+                return softmax_cta_rows<T, VB, 16, 1, NT, ALIGNED, true, UP, PF, EF>(
                     scores, lengths, first, row_end, rpb, Sk, c, true, Lcta);
         }
     }
-    softmax_cta_rows<T, VB, G, NV, NT, ALIGNED, false, UP, PF>(scores, lengths, first, row_end,
+    softmax_cta_rows<T, VB, G, NV, NT, ALIGNED, false, UP, PF, EF>(scores, lengths, first, row_end,
                                                                rpb, Sk, c, one_req, Lcta);
 }
 
-template <typename T, int VB, int G, int NV, int NT, int MINB, bool ALIGNED, bool PF>
+template <typename T, int VB, int G, int NV, int NT, int MINB, bool ALIGNED, bool PF, bool EF>
 __global__ void __launch_bounds__(NT, MINB) softmax_warp_kernel(T* __restrict__ scores,
                                                                 const int32_t* __restrict__ lengths,
                                                                 uint32_t nrows, FastDivU32 rpb,
                                                                 int Sk, float c, int rpg) {
     PdlScope pdl_;  // griddepcontrol.wait first: no global access before it (PDL)
     if (c > 0.f)  // uniform: the sign of the scale picks the max or min reduction
-        softmax_warp_body<T, VB, G, NV, NT, ALIGNED, true, PF>(scores, lengths, nrows, rpb, Sk, c,
+        softmax_warp_body<T, VB, G, NV, NT, ALIGNED, true, PF, EF>(scores, lengths, nrows, rpb, Sk, c,
                                                                rpg);
     else
-        softmax_warp_body<T, VB, G, NV, NT, ALIGNED, false, PF>(scores, lengths, nrows, rpb, Sk, c,
+        softmax_warp_body<T, VB, G, NV, NT, ALIGNED, false, PF, EF>(scores, lengths, nrows, rpb, Sk, c,
                                                                 rpg);
 }
 
@@ -549,19 +552,24 @@ cudaError_t launch_softmax_warp(void* scores, const int32_t* lengths, int64_t nr
         return launch_softmax<T, VB, G, NV, 1, NT, MINB>(scores, lengths, nrows, rpb, Sk, scale, st);
     const bool aligned = (reinterpret_cast<uintptr_t>(scores) % VB) == 0 &&
                          ((int64_t)Sk * (int64_t)sizeof(T)) % VB == 0;
-    auto kern = aligned ? softmax_warp_kernel<T, VB, G, NV, NT, MINB, true, PF>
-                        : softmax_warp_kernel<T, VB, G, NV, NT, MINB, false, PF>;
+    // rows made of whole 128-byte L2 lines: evict_first stores (see row_finish)
+    const bool lines = aligned && (reinterpret_cast<uintptr_t>(scores) % 128) == 0 &&
+                       ((int64_t)Sk * (int64_t)sizeof(T)) % 128 == 0;
+    const int kv = lines ? 2 : aligned ? 1 : 0;
+    auto kern = lines     ? softmax_warp_kernel<T, VB, G, NV, NT, MINB, true, PF, true>
+                : aligned ? softmax_warp_kernel<T, VB, G, NV, NT, MINB, true, PF, false>
+                          : softmax_warp_kernel<T, VB, G, NV, NT, MINB, false, PF, false>;
     // RPG > 0: fixed rows per group; RPG = 0: one persistent wave (rows spread
     // evenly over SMs x resident CTAs).
     int rpg = RPG;
     if (RPG == 0) {
-        static std::atomic<int> occ_cache[2] = {{0}, {0}};
-        int occ = occ_cache[aligned].load(std::memory_order_relaxed);
+        static std::atomic<int> occ_cache[3] = {{0}, {0}, {0}};
+        int occ = occ_cache[kv].load(std::memory_order_relaxed);
         if (!occ) {
             cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT, 0);
             if (e != cudaSuccess) return e;
             occ = occ > 0 ? occ : 1;
-            occ_cache[aligned].store(occ);
+            occ_cache[kv].store(occ);
         }
         const int64_t slots = (int64_t)sm_count() * occ * GPB;
         rpg = (int)((nrows + slots - 1) / slots);

@@ -81,7 +81,7 @@ __device__ __forceinline__ void row_load(const T* __restrict__ p, int L, int Sk,
 // remaining body vectors are written as zeros without any arithmetic.  UP:
 // c > 0, so the row max of c*x is c*max(x) (else c*min(x)); a template
 // parameter so that only one of the two reductions is compiled into each path.
-template <typename T, int VB, int GC, int NVC, bool ALIGNED, bool NARROW, bool UP>
+template <typename T, int VB, int GC, int NVC, bool ALIGNED, bool NARROW, bool UP, bool EF = false>
 __device__ __forceinline__ void row_finish(T* __restrict__ p, bool live, int L, int Sk, float c,
                                            int q, const RowRaw<T, VB, GC, NVC, ALIGNED>& r) {
     using RR = RowRaw<T, VB, GC, NVC, ALIGNED>;
@@ -185,7 +185,11 @@ __device__ __forceinline__ void row_finish(T* __restrict__ p, bool live, int L, 
     const float inv = L > 0 ? rcp_approx(s[0]) : 0.f;
     if (!live) return;
 
-    // ---- SM-5: normalise and store every column
+    // ---- SM-5: normalise and store every column.  EF (evict_first stores) is
+    // chosen at launch only when every row covers whole 128-byte L2 lines: a
+    // line shared with the next row (partly written) evicted early costs a
+    // partial write-back; measured 6 % slower on odd-pitch C3 rows and 4.5 % on
+    // 800-byte rows, +1 % on C4.
 #pragma unroll
     for (int k = 0; k < NVC; ++k) {
         const int vi = q + k * GC;
@@ -197,7 +201,7 @@ __device__ __forceinline__ void row_finish(T* __restrict__ p, bool live, int L, 
                 f2_split(f2_mul(f2_make(v[k][e], v[k][e + 1]), inv2), y[e], y[e + 1]);
             Raw<VB> w;
             Elem<T>::template pack<VB>(y, w);
-            st_stream<VB>(p + hd + vi * VE, w);
+            st_stream<VB, EF>(p + hd + vi * VE, w);
         }
     }
     if constexpr (NARROW) {
