@@ -378,13 +378,20 @@ def run_e2e(args, tt, wl, units, stream, dist, dev, world):
     d2h = sum(h["scores"].numel() * h["scores"].element_size()
               + h["out"].numel() * h["out"].element_size() for h in hosts)
 
+    # D2H of chunk i on a second stream under the H2D of chunk i+1 (PCIe is
+    # full duplex); `stream` waits for the last D2H inside each call
+    copy_stream = torch.cuda.Stream(device=dev)
+    chunks = args.e2e_chunks
+
     def step():
         for u, h in zip(units, hosts):
-            tt.tt_softmax_masked_staged(h["scores"], h["L"], u["scores"], u["L"], wl.scale,
-                                        stream=stream)
-            tt.tt_add_bias_layernorm_staged(h["out"], h["x"], h["residual"], u["out"], u["x"],
-                                            u["residual"], u["bias"], u["gamma"], u["beta"],
-                                            wl.eps, stream=stream)
+            tt.tt_softmax_masked_staged_overlap(h["scores"], h["L"], u["scores"], u["L"],
+                                                wl.scale, chunks, stream=stream,
+                                                copy_stream=copy_stream)
+            tt.tt_add_bias_layernorm_staged_overlap(h["out"], h["x"], h["residual"], u["out"],
+                                                    u["x"], u["residual"], u["bias"], u["gamma"],
+                                                    u["beta"], wl.eps, chunks, stream=stream,
+                                                    copy_stream=copy_stream)
 
     for _ in range(2):
         step()
@@ -408,7 +415,9 @@ def run_e2e(args, tt, wl, units, stream, dist, dev, world):
     value = per_step_bytes * mult * E / (ms / 1e3) / 1e9
     return {"value": round(value, 2), "unit": UNIT, "steps": E, "ms_per_step": round(ms / E, 3),
             "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-            "api": "tt_softmax_masked_staged + tt_add_bias_layernorm_staged (pinned host)"}
+            "chunks": chunks,
+            "api": "tt_softmax_masked_staged_overlap + tt_add_bias_layernorm_staged_overlap "
+                   "(pinned host; D2H on a second stream under the next chunk's H2D)"}
 
 
 # ------------------------------------------------------------------ oracle timing
@@ -544,6 +553,8 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", choices=["c4", "c3", "c5", "c3p", "c5p"], default="c4")
     ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--e2e-chunks", type=int, default=8,
+                    help="pieces per staged call (D2H of one under the H2D of the next)")
     ap.add_argument("--kernel-events", type=int, default=1000000,
                     help="per-kernel CUDA events for the first N timed steps")
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -220,6 +220,31 @@ TT_API tt_status tt_add_bias_layernorm_staged(int dtype, void* host_out, const v
                                        const void* beta, int64_t rows, int64_t hidden, float eps,
                                        cudaStream_t stream);
 
+/* Overlapped staging: the same operation and contract, but the batch is cut
+ * into `chunks` pieces (requests for the softmax, rows for LayerNorm; each piece
+ * a multiple of the granule that keeps its device base 16-byte aligned).  Piece
+ * i's H2D copy and kernel run on `stream` while piece i-1's result is copied
+ * D2H on `copy_stream`, so the two PCIe directions overlap.  On return `stream`
+ * has been made to wait for the last D2H: the host result is complete when
+ * `stream` completes, and later work on `stream` may reuse the device buffers.
+ * copy_stream NULL, equal to stream, or chunks <= 1: the single-stream call.
+ * The library creates one CUDA event per call (destroyed before returning;
+ * released by the driver when its last use completes). */
+TT_API tt_status tt_softmax_masked_staged_overlap(int dtype, void* host_scores,
+                                                  const int32_t* host_lengths, void* dev_scores,
+                                                  int32_t* dev_lengths, int64_t B, int64_t H,
+                                                  int64_t Sq, int64_t Sk, float scale,
+                                                  int64_t chunks, cudaStream_t stream,
+                                                  cudaStream_t copy_stream);
+TT_API tt_status tt_add_bias_layernorm_staged_overlap(int dtype, void* host_out, const void* host_x,
+                                                      const void* host_residual, void* dev_out,
+                                                      void* dev_x, void* dev_residual,
+                                                      const void* bias, const void* gamma,
+                                                      const void* beta, int64_t rows,
+                                                      int64_t hidden, float eps, int64_t chunks,
+                                                      cudaStream_t stream,
+                                                      cudaStream_t copy_stream);
+
 /* ------------------------------------------------------------------------
  * Introspection
  * ---------------------------------------------------------------------- */

@@ -31,6 +31,7 @@ EXPORTS = (
     "tt_add_bias_layernorm_f32", "tt_add_bias_layernorm_f16", "tt_add_bias_layernorm_bf16",
     "tt_softmax_packed_f32", "tt_softmax_packed_f16", "tt_softmax_packed_bf16",
     "tt_softmax_masked_staged", "tt_add_bias_layernorm_staged",
+    "tt_softmax_masked_staged_overlap", "tt_add_bias_layernorm_staged_overlap",
     "tt_status_string", "tt_last_cuda_error", "tt_version",
     "tt_softmax_masked_plan", "tt_add_bias_layernorm_plan", "tt_softmax_packed_plan",
     "ttx_tier_count", "ttx_tier_name", "ttx_force_tier",
@@ -76,6 +77,11 @@ def lib() -> ctypes.CDLL:
                                                    _f, _vp]
             L.tt_add_bias_layernorm_staged.argtypes = [_i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
                                                        _vp, _i64, _i64, _f, _vp]
+            L.tt_softmax_masked_staged_overlap.argtypes = [_i, _vp, _vp, _vp, _vp, _i64, _i64,
+                                                           _i64, _i64, _f, _i64, _vp, _vp]
+            L.tt_add_bias_layernorm_staged_overlap.argtypes = [_i, _vp, _vp, _vp, _vp, _vp, _vp,
+                                                               _vp, _vp, _vp, _i64, _i64, _f,
+                                                               _i64, _vp, _vp]
             L.tt_softmax_masked_plan.argtypes = [_i, _i64, _i64, _i64, _i64, ctypes.c_char_p, _i]
             L.tt_add_bias_layernorm_plan.argtypes = [_i, _i64, _i64, ctypes.c_char_p, _i]
             L.tt_add_bias_gelu.argtypes = [_i, _vp, _vp, _vp, _i64, _i64, _i, _vp]
@@ -169,6 +175,26 @@ def tt_softmax_masked_staged(host_scores: torch.Tensor, host_lengths: torch.Tens
     return host_scores
 
 
+def tt_softmax_masked_staged_overlap(host_scores: torch.Tensor, host_lengths: torch.Tensor,
+                                     dev_scores: torch.Tensor, dev_lengths: torch.Tensor,
+                                     scale: float, chunks: int, stream=None, copy_stream=None):
+    """As tt_softmax_masked_staged, cut into `chunks` pieces whose D2H copies run
+    on `copy_stream` under the next piece's H2D copy (include/tt.h)."""
+    _dev(dev_scores, "dev_scores")
+    _dev(dev_lengths, "dev_lengths")
+    if host_scores.is_cuda or host_lengths.is_cuda:
+        raise ValueError("host_* must be host tensors")
+    if host_scores.shape != dev_scores.shape or host_scores.dtype != dev_scores.dtype:
+        raise ValueError("host/device scores mismatch")
+    B, H, Sq, Sk = dev_scores.shape
+    _check(lib().tt_softmax_masked_staged_overlap(
+        DTYPE_CODE[dev_scores.dtype], host_scores.data_ptr(), host_lengths.data_ptr(),
+        dev_scores.data_ptr(), dev_lengths.data_ptr(), B, H, Sq, Sk, float(scale), int(chunks),
+        _stream_ptr(stream), _stream_ptr(copy_stream) if copy_stream is not None else None),
+        "tt_softmax_masked_staged_overlap")
+    return host_scores
+
+
 def softmax_plan(dtype: torch.dtype, B: int, H: int, Sq: int, Sk: int) -> str:
     buf = ctypes.create_string_buffer(128)
     _check(lib().tt_softmax_masked_plan(DTYPE_CODE[dtype], B, H, Sq, Sk, buf, 128),
@@ -257,6 +283,25 @@ def tt_add_bias_layernorm_staged(host_out, host_x, host_residual, dev_out, dev_x
         dev_out.data_ptr(), dev_x.data_ptr(), dev_residual.data_ptr(), bias.data_ptr(),
         gamma.data_ptr(), beta.data_ptr(), rows, hidden, float(eps), _stream_ptr(stream)),
         "tt_add_bias_layernorm_staged")
+    return host_out
+
+
+def tt_add_bias_layernorm_staged_overlap(host_out, host_x, host_residual, dev_out, dev_x,
+                                         dev_residual, bias, gamma, beta, eps: float, chunks: int,
+                                         stream=None, copy_stream=None):
+    """As tt_add_bias_layernorm_staged, cut into `chunks` row ranges whose D2H
+    copies run on `copy_stream` (include/tt.h)."""
+    for t, n in ((dev_out, "dev_out"), (dev_x, "dev_x"), (dev_residual, "dev_residual"),
+                 (bias, "bias"), (gamma, "gamma"), (beta, "beta")):
+        _dev(t, n)
+    hidden = dev_x.shape[-1]
+    rows = dev_x.numel() // hidden if hidden else 0
+    _check(lib().tt_add_bias_layernorm_staged_overlap(
+        DTYPE_CODE[dev_x.dtype], host_out.data_ptr(), host_x.data_ptr(), host_residual.data_ptr(),
+        dev_out.data_ptr(), dev_x.data_ptr(), dev_residual.data_ptr(), bias.data_ptr(),
+        gamma.data_ptr(), beta.data_ptr(), rows, hidden, float(eps), int(chunks),
+        _stream_ptr(stream), _stream_ptr(copy_stream) if copy_stream is not None else None),
+        "tt_add_bias_layernorm_staged_overlap")
     return host_out
 
 

@@ -400,6 +400,128 @@ tt_status tt_add_bias_layernorm_staged(int dtype, void* host_out, const void* ho
     return cuda_status(cudaMemcpyAsync(host_out, dev_out, bytes, cudaMemcpyDeviceToHost, stream));
 }
 
+// ---- overlapped staging: chunks of requests (softmax) or rows (LN) go H2D and
+// through the kernel on `stream` while the previous chunk's result goes D2H on
+// `copy_stream` (the two copy directions run concurrently over PCIe).  `stream`
+// finally waits for the last D2H, so the caller's contract is unchanged: the host
+// result is ready when `stream` completes.
+namespace {
+
+int64_t gcd64(int64_t a, int64_t b) {
+    while (b) {
+        const int64_t t = a % b;
+        a = b;
+        b = t;
+    }
+    return a;
+}
+
+// Units per chunk: a multiple of the granule that keeps every chunk's device
+// base 16-byte aligned (unit_bytes * granule % 16 == 0).
+int64_t chunk_units(int64_t units, int64_t chunks, int64_t unit_bytes) {
+    const int64_t gran = 16 / gcd64(unit_bytes % 16 == 0 ? 16 : unit_bytes % 16, 16);
+    if (chunks < 1) chunks = 1;
+    int64_t per = (units + chunks - 1) / chunks;
+    per = ((per + gran - 1) / gran) * gran;
+    return per > 0 ? per : 1;
+}
+
+struct EventGuard {
+    cudaEvent_t ev = nullptr;
+    ~EventGuard() {
+        if (ev) cudaEventDestroy(ev);  // released once its last record completes
+    }
+};
+
+}  // namespace
+
+tt_status tt_softmax_masked_staged_overlap(int dtype, void* host_scores,
+                                           const int32_t* host_lengths, void* dev_scores,
+                                           int32_t* dev_lengths, int64_t B, int64_t H, int64_t Sq,
+                                           int64_t Sk, float scale, int64_t chunks,
+                                           cudaStream_t stream, cudaStream_t copy_stream) {
+    if (!copy_stream || copy_stream == stream || chunks <= 1)
+        return tt_softmax_masked_staged(dtype, host_scores, host_lengths, dev_scores, dev_lengths,
+                                        B, H, Sq, Sk, scale, stream);
+    int64_t nrows = 0;
+    bool empty = false;
+    tt_status s = softmax_validate(dtype, dev_scores, dev_lengths, B, H, Sq, Sk, scale, true,
+                                   &nrows, &empty);
+    if (s != TT_SUCCESS || empty) return s;
+    if (!host_scores || !host_lengths) return TT_ERROR_INVALID_VALUE;
+    const int64_t req_bytes = H * Sq * Sk * elem_bytes(dtype);
+    const int64_t per = chunk_units(B, chunks, req_bytes);
+    EventGuard g;
+    cudaError_t e = cudaEventCreateWithFlags(&g.ev, cudaEventDisableTiming);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(dev_lengths, host_lengths, (size_t)B * sizeof(int32_t),
+                            cudaMemcpyHostToDevice, stream);
+    if (e != cudaSuccess) return cuda_status(e);
+    for (int64_t b0 = 0; b0 < B; b0 += per) {
+        const int64_t nb = B - b0 < per ? B - b0 : per;
+        const size_t off = (size_t)(b0 * req_bytes), bytes = (size_t)(nb * req_bytes);
+        char* d = static_cast<char*>(dev_scores) + off;
+        char* h = static_cast<char*>(host_scores) + off;
+        e = cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, stream);
+        if (e != cudaSuccess) return cuda_status(e);
+        s = softmax_any(dtype, d, dev_lengths + b0, nb, H, Sq, Sk, scale, stream);
+        if (s != TT_SUCCESS) return s;
+        e = cudaEventRecord(g.ev, stream);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(copy_stream, g.ev, 0);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(h, d, bytes, cudaMemcpyDeviceToHost, copy_stream);
+        if (e != cudaSuccess) return cuda_status(e);
+    }
+    e = cudaEventRecord(g.ev, copy_stream);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(stream, g.ev, 0);
+    return cuda_status(e);
+}
+
+tt_status tt_add_bias_layernorm_staged_overlap(int dtype, void* host_out, const void* host_x,
+                                               const void* host_residual, void* dev_out,
+                                               void* dev_x, void* dev_residual, const void* bias,
+                                               const void* gamma, const void* beta, int64_t rows,
+                                               int64_t hidden, float eps, int64_t chunks,
+                                               cudaStream_t stream, cudaStream_t copy_stream) {
+    if (!copy_stream || copy_stream == stream || chunks <= 1)
+        return tt_add_bias_layernorm_staged(dtype, host_out, host_x, host_residual, dev_out, dev_x,
+                                            dev_residual, bias, gamma, beta, rows, hidden, eps,
+                                            stream);
+    bool empty = false;
+    tt_status s = ln_validate(dtype, dev_out, dev_x, dev_residual, bias, gamma, beta, rows, hidden,
+                              eps, true, &empty);
+    if (s != TT_SUCCESS || empty) return s;
+    if (!host_out || !host_x || !host_residual) return TT_ERROR_INVALID_VALUE;
+    const int64_t row_bytes = hidden * elem_bytes(dtype);
+    const int64_t per = chunk_units(rows, chunks, row_bytes);
+    EventGuard g;
+    cudaError_t e = cudaEventCreateWithFlags(&g.ev, cudaEventDisableTiming);
+    if (e != cudaSuccess) return cuda_status(e);
+    for (int64_t r0 = 0; r0 < rows; r0 += per) {
+        const int64_t nr = rows - r0 < per ? rows - r0 : per;
+        const size_t off = (size_t)(r0 * row_bytes), bytes = (size_t)(nr * row_bytes);
+        char* dx = static_cast<char*>(dev_x) + off;
+        char* dr = static_cast<char*>(dev_residual) + off;
+        char* dout = static_cast<char*>(dev_out) + off;
+        e = cudaMemcpyAsync(dx, static_cast<const char*>(host_x) + off, bytes,
+                            cudaMemcpyHostToDevice, stream);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(dr, static_cast<const char*>(host_residual) + off, bytes,
+                                cudaMemcpyHostToDevice, stream);
+        if (e != cudaSuccess) return cuda_status(e);
+        s = ln_any(dtype, dout, dx, dr, bias, gamma, beta, nr, hidden, eps, stream);
+        if (s != TT_SUCCESS) return s;
+        e = cudaEventRecord(g.ev, stream);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(copy_stream, g.ev, 0);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(static_cast<char*>(host_out) + off, dout, bytes,
+                                cudaMemcpyDeviceToHost, copy_stream);
+        if (e != cudaSuccess) return cuda_status(e);
+    }
+    e = cudaEventRecord(g.ev, copy_stream);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(stream, g.ev, 0);
+    return cuda_status(e);
+}
+
 const char* tt_status_string(tt_status s) {
     switch (s) {
         case TT_SUCCESS: return "TT_SUCCESS";

@@ -128,6 +128,23 @@ def test_staged_host_buffers(ttlib, dtype):
     assert_close("layernorm", dtype, ho, _ref(d, W.EPS_BERT), "staged")
 
 
+@pytest.mark.parametrize("dtype", DT)
+@pytest.mark.parametrize("rows,hidden,chunks", [(1001, 768, 4), (37, 36, 5), (64, 1024, 64)])
+def test_staged_overlap_host_buffers(ttlib, dtype, rows, hidden, chunks):
+    """Row-chunked staging with D2H on a second stream (tt_add_bias_layernorm_
+    staged_overlap); hidden 36 makes the 16-byte granule several rows wide."""
+    d = W.ln_inputs(rows, hidden, dtype, seed=9)
+    hx, hr = d["x"].clone().pin_memory(), d["residual"].clone().pin_memory()
+    ho = torch.empty_like(hx).pin_memory()
+    dx, dr, do = (torch.empty_like(hx, device="cuda") for _ in range(3))
+    p = {k: d[k].cuda() for k in ("bias", "gamma", "beta")}
+    cs = torch.cuda.Stream()
+    ttlib.tt_add_bias_layernorm_staged_overlap(ho, hx, hr, do, dx, dr, p["bias"], p["gamma"],
+                                               p["beta"], W.EPS_BERT, chunks, copy_stream=cs)
+    torch.cuda.current_stream().synchronize()
+    assert_close("layernorm", dtype, ho, _ref(d, W.EPS_BERT), f"staged overlap {rows}x{hidden}")
+
+
 def test_rows_not_multiple_of_cta(ttlib):
     for rows in (1, 7, 15, 17, 1023, 1025):
         _check(ttlib, rows, 768, torch.float16, seed=rows)

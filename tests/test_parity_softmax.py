@@ -211,6 +211,30 @@ def test_staged_host_buffers(ttlib, dtype):
     assert masked_bits_zero(host, lens)
 
 
+@pytest.mark.parametrize("dtype", DT)
+@pytest.mark.parametrize("chunks", [2, 3, 8])
+def test_staged_overlap_host_buffers(ttlib, dtype, chunks):
+    """Chunked H2D / kernel on one stream, D2H on a second (include/tt.h
+    tt_softmax_masked_staged_overlap); an odd Sk and H * Sq make the 16-byte
+    chunk granule several requests wide for 16-bit storage.  Run twice on the
+    same device buffers: the second call must wait for the first's copies."""
+    B, H, S = 7, 3, 37
+    lens = np.array([37, 17, 3, 0, 37, 21, 1], dtype=np.int32)
+    cs = torch.cuda.Stream()
+    dev = torch.empty(B, H, S, S, dtype=dtype, device="cuda")
+    dl = torch.empty(B, dtype=torch.int32, device="cuda")
+    for rep in range(2):
+        x = W.scores(B, H, S, S, dtype, seed=80 + rep)
+        host = x.clone().pin_memory()
+        hl = torch.as_tensor(lens).pin_memory()
+        ttlib.tt_softmax_masked_staged_overlap(host, hl, dev, dl, W.SCALE_BERT, chunks,
+                                               copy_stream=cs)
+        torch.cuda.current_stream().synchronize()  # the contract: `stream` covers the D2H
+        assert_close("softmax", dtype, host, oracle.softmax_masked(x, lens, W.SCALE_BERT),
+                     f"overlap chunks={chunks} rep={rep}")
+        assert masked_bits_zero(host, lens)
+
+
 def test_binding_rejects_bad_tensors(ttlib):
     x = torch.zeros(2, 2, 2, 8, device="cuda")
     with pytest.raises(ValueError):
