@@ -245,6 +245,27 @@ __device__ __forceinline__ void softmax_cta_rows(T* __restrict__ scores,
     }
 }
 
+// Rows of one request with L <= G * K * VE on a tier of NV > K vectors per lane:
+// run them with K vectors per lane (K = 1 .. NV-1, smallest that fits).
+template <typename T, int VB, int G, int K, int NV, int NT, bool ALIGNED, bool UP, bool PF, bool EF>
+__device__ __forceinline__ bool softmax_narrow_nv(T* __restrict__ scores,
+                                                  const int32_t* __restrict__ lengths,
+                                                  uint32_t first, uint32_t row_end, FastDivU32 rpb,
+                                                  int Sk, float c, int Lcta) {
+    if constexpr (K >= NV) {
+        return false;
+    } else {
+        constexpr int VE = VB / (int)sizeof(T);
+        if (Lcta <= G * K * VE) {
+            softmax_cta_rows<T, VB, G, K, NT, ALIGNED, true, UP, PF, EF>(
+                scores, lengths, first, row_end, rpb, Sk, c, true, Lcta);
+            return true;
+        }
+        return softmax_narrow_nv<T, VB, G, K + 1, NV, NT, ALIGNED, UP, PF, EF>(
+            scores, lengths, first, row_end, rpb, Sk, c, Lcta);
+    }
+}
+
 template <typename T, int VB, int G, int NV, int NT, bool ALIGNED, bool UP, bool PF, bool EF>
 __device__ __forceinline__ void softmax_warp_body(T* __restrict__ scores,
                                                   const int32_t* __restrict__ lengths,
@@ -274,6 +295,18 @@ __device__ __forceinline__ void softmax_warp_body(T* __restrict__ scores,
             if (Lcta <= 16 * VE)
                 return softmax_cta_rows<T, VB, 16, 1, NT, ALIGNED, true, UP, PF, EF>(
                     scores, lengths, first, row_end, rpb, Sk, c, true, Lcta);
+        }
+    }
+    // (not compiled into the G8 x NV5 tier: there the extra paths made ptxas
+    // spill the main path, -2.5 % on full fp16 S = 300 rows)
+    if constexpr (NV > 1 && !(G == 8 && NV == 5)) {
+        // short request on a multi-vector tier: the fewest vectors per lane that
+        // hold its valid keys; the padding vectors are zero-filled without
+        // arithmetic (NARROW), so a row's cost follows L_b instead of Sk
+        if (one_req && Lcta < Sk) {
+            if (softmax_narrow_nv<T, VB, G, 1, NV, NT, ALIGNED, UP, PF, EF>(
+                    scores, lengths, first, row_end, rpb, Sk, c, Lcta))
+                return;
         }
     }
     softmax_cta_rows<T, VB, G, NV, NT, ALIGNED, false, UP, PF, EF>(scores, lengths, first, row_end,
