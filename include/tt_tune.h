@@ -32,7 +32,9 @@ TT_API tt_status ttx_force_tier(int op, int dtype, int i);
  * SM), 3 = 64-key tiles single-buffered (4 CTAs per SM), 4 = 64-key tiles
  * double-buffered and software-pipelined (3 CTAs per SM), 5 = warp-specialised
  * (producer warp, MMA warp, 4 softmax warps; mbarrier hand-offs, no CTA barrier
- * in the tile loop; 2 CTAs per SM).  Returns TT_ERROR_INVALID_VALUE outside 0..5. */
+ * in the tile loop; 2 CTAs per SM), 6 / 7 = variant 4 with two threads per
+ * query row (8 warps; 2 / 3 CTAs per SM).  Returns TT_ERROR_INVALID_VALUE
+ * outside 0..7. */
 TT_API tt_status ttx_attention_variant(int v);
 
 /* Programmatic dependent launch (PDL, default on): every kernel is launched

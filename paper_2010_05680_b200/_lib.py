@@ -377,7 +377,8 @@ def attention_variant(v: int):
     """0 = automatic, 1 = 128-key tiles single-buffered (2 CTAs/SM), 2 = 128-key
     tiles double-buffered, pipelined (1 CTA/SM), 3 = 64-key tiles (4 CTAs/SM),
     4 = 64-key tiles double-buffered, pipelined (3 CTAs/SM), 5 = warp-specialised
-    (producer / MMA / softmax warps, mbarrier hand-offs, 2 CTAs/SM)."""
+    (producer / MMA / softmax warps, mbarrier hand-offs, 2 CTAs/SM), 6 / 7 = variant 4
+    with two threads per query row (2 / 3 CTAs/SM)."""
     _check(lib().ttx_attention_variant(int(v)), "ttx_attention_variant")
 
 

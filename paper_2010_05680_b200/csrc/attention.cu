@@ -726,6 +726,250 @@ __global__ void __launch_bounds__(kWsThreads, 2)
     }
 }
 
+
+// ----------------------------------------------------------------------------
+// Split-row variant (ttx_attention_variant 6): the pipelined 64-key schedule of
+// variant 4 with TWO threads per query row.  8 warps: warp w reads TMEM lanes
+// 32 (w % 4) .. +31 (its rows) and owns key half h = w / 4 of every S tile, O
+// columns [32 h, 32 h + 32) and output columns likewise.  The row max is
+// exchanged between the two halves through shared memory (double-buffered by
+// tile parity) under a 64-thread named barrier per row group; both halves then
+// take identical rescale decisions, and their partial row sums are added once
+// at the end.  Half the registers per thread (32 S values), twice the warps.
+// ----------------------------------------------------------------------------
+constexpr int kSpNT = 256;
+constexpr size_t kSpSmem = attn_smem<2, 64>() + 4 * 128 * sizeof(float);
+
+template <typename T, int ROWS, int NT>
+__device__ __forceinline__ void load_tile_nt(uint32_t tile, const T* g, int row0, int valid) {
+#pragma unroll
+    for (int i = 0; i < (ROWS * 8) / NT; ++i) {
+        const int idx = threadIdx.x + i * NT;
+        const int r = idx >> 3, c = idx & 7;
+        const bool in = row0 + r < valid;
+        const T* src = g + (size_t)(in ? row0 + r : 0) * kD + c * 8;
+        cp_async16(tile + sw_off(r, c), src, in ? 16u : 0u);
+    }
+}
+
+__device__ __forceinline__ void named_bar(int id, int nthreads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+template <typename T, bool UP, int MINB>
+__global__ void __launch_bounds__(kSpNT, MINB)
+    attention_split_kernel(T* __restrict__ out, const T* __restrict__ q, const T* __restrict__ k,
+                           const T* __restrict__ v, const int32_t* __restrict__ lengths, int H,
+                           int S, float c) {
+    PdlScope pdl_;  // griddepcontrol.wait first: no global access before it (PDL)
+    constexpr int NBUF = 2, BN = 64;
+    constexpr int kKV = BN * 128;
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;
+    unsigned char* sbase = smem_raw + (base - smem_u32(smem_raw));
+    const uint32_t sQ = base, sK = base + kTile, sV = base + kTile + NBUF * kKV,
+                   sP = base + kTile + 2 * NBUF * kKV;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sbase + kTile + 2 * NBUF * kKV + BN * 256);
+    uint32_t* tmem_slot =
+        reinterpret_cast<uint32_t*>(sbase + kTile + 2 * NBUF * kKV + BN * 256 + 16);
+    float* xch = reinterpret_cast<float*>(sbase + kTile + 2 * NBUF * kKV + BN * 256 + 64);
+    // xch: [2 parity][2 halves][128 rows] partial maxima; reused at the end for l
+
+    const int qt = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int rg = warp & 3, hf = warp >> 2;
+    const int r = rg * 32 + lane;  // query row in the tile (= TMEM lane)
+    const int L = min(max(__ldg(lengths + b), 0), S);
+    const size_t head = ((size_t)b * H + h) * (size_t)S * kD;
+    const int row = qt * kBM + r;
+
+    if (L == 0) {
+        if (row < S) {
+            uint4 z = make_uint4(0, 0, 0, 0);
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+                reinterpret_cast<uint4*>(out + head + (size_t)row * kD + hf * 32)[i] = z;
+        }
+        return;
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(
+                         smem_u32(tmem_slot))
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    if (tid == 0) {
+        mbar_init(&bars[0], 1);
+        mbar_init(&bars[1], 1);
+        fence_mbar_init();
+    }
+    const int nkt = (L + BN - 1) / BN;
+    load_tile_nt<T, kBM, kSpNT>(sQ, q + head, qt * kBM, S);
+    load_tile_nt<T, BN, kSpNT>(sK, k + head, 0, L);
+    load_tile_nt<T, BN, kSpNT>(sV, v + head, 0, L);
+    cp_async_commit();
+    if (nkt > 1) load_tile_nt<T, BN, kSpNT>(sK + kKV, k + head, BN, L);
+    cp_async_commit();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    const uint32_t lane_off = (uint32_t)(rg * 32) << 16;
+    const uint32_t t_s = tmem + lane_off + hf * 32, t_o = tmem + BN + lane_off + hf * 32;
+
+    constexpr int kFmt = sizeof(T) == 2 && std::is_same<T, __nv_bfloat16>::value ? 1 : 0;
+    constexpr uint32_t idesc_s = f16_idesc(kFmt, 0, kBM, BN);
+    constexpr uint32_t idesc_o = f16_idesc(kFmt, 1, kBM, kD);
+    constexpr float kRescale = 8.f;
+    const float sent = UP ? -INFINITY : INFINITY;
+    float m_ref = -INFINITY, l_run = 0.f;
+    uint32_t ph_s = 0, ph_o = 0;
+    unsigned char* prow = sbase + (sP - base);
+
+    auto issue_s = [&](int kt) {
+        if (tid == 0) {
+            const uint32_t kbase = sK + (kt & 1) * kKV;
+#pragma unroll
+            for (int ks = 0; ks < kD / 16; ++ks)
+                tc_mma(tmem, sw128_desc(sQ + ks * 32, 16, 1024),
+                       sw128_desc(kbase + ks * 32, 16, 1024), idesc_s, ks > 0);
+            tc_commit(&bars[0]);
+        }
+    };
+    auto issue_pv = [&](int kt) {
+        if (tid == 0) {
+            const uint32_t vbase = sV + (kt & 1) * kKV;
+#pragma unroll
+            for (int ks = 0; ks < BN / 16; ++ks)
+                tc_mma(tmem + BN, sw128_desc(sP + ks * 32, 16, 1024),
+                       sw128_desc(vbase + ks * 2048, 16384, 1024), idesc_o, (kt > 0 || ks > 0));
+            tc_commit(&bars[1]);
+        }
+    };
+    auto sync_for_mma = [&]() {
+        fence_proxy_async_smem();
+        tc_fence_before();
+        __syncthreads();
+        tc_fence_after();
+    };
+    auto softmax_half = [&](float (&sv)[32], int kt) {
+        const int key0 = kt * BN + hf * 32;
+        if (key0 + 32 > L) {
+#pragma unroll
+            for (int e = 0; e < 32; ++e) sv[e] = key0 + e < L ? sv[e] : sent;
+        }
+        float mx = sent;
+#pragma unroll
+        for (int e = 0; e < 32; ++e) mx = UP ? fmaxf(mx, sv[e]) : fminf(mx, sv[e]);
+        float* xb = xch + (kt & 1) * 256;
+        xb[hf * 128 + r] = mx;
+        named_bar(1 + rg, 64);  // warps rg and rg + 4: the two halves of these rows
+        const float mo = xb[(hf ^ 1) * 128 + r];
+        mx = UP ? fmaxf(mx, mo) : fminf(mx, mo);
+        const float m_tile = mx * c;
+        if (kt == 0) {
+            m_ref = m_tile;
+        } else if (__any_sync(0xffffffffu, m_tile > m_ref + kRescale)) {
+            const float m_new = fmaxf(m_ref, m_tile);
+            const float alpha = ex2_approx(m_ref - m_new);
+            l_run *= alpha;
+            m_ref = m_new;
+            float ov[32];
+            tc_ld32(t_o, ov);
+#pragma unroll
+            for (int e = 0; e < 32; ++e) ov[e] *= alpha;
+            tc_st32(t_o, ov);
+        }
+        const F2 c2 = f2_make(c, c), nm2 = f2_make(-m_ref, -m_ref);
+        F2 ps2 = f2_make(0.f, 0.f);
+        float pv[32];
+#pragma unroll
+        for (int e = 0; e < 32; e += 2) {
+            float t0, t1;
+            f2_split(f2_fma(f2_make(sv[e], sv[e + 1]), c2, nm2), t0, t1);
+            pv[e] = ex2_approx(t0);
+            pv[e + 1] = ex2_approx(t1);
+            ps2 = f2_add(ps2, f2_make(pv[e], pv[e + 1]));
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            Raw<16> w;
+            Elem<T>::template pack<16>(pv + 8 * j, w);
+            *reinterpret_cast<uint4*>(prow + sw_off(r, hf * 4 + j)) =
+                make_uint4(w.w[0], w.w[1], w.w[2], w.w[3]);
+        }
+        float a0, a1;
+        f2_split(ps2, a0, a1);
+        l_run += a0 + a1;
+    };
+
+    cp_async_wait<1>();
+    sync_for_mma();
+    issue_s(0);
+    for (int kt = 0; kt < nkt; ++kt) {
+        mbar_wait_bounded(&bars[0], ph_s);
+        ph_s ^= 1;
+        tc_fence_after();
+        float sv[32];
+        tc_ld32(t_s, sv);
+        if (kt + 1 < nkt) {
+            if (kt == 0)
+                cp_async_wait<0>();
+            else
+                cp_async_wait<1>();
+            sync_for_mma();
+            issue_s(kt + 1);
+        }
+        if (kt + 2 < nkt)
+            load_tile_nt<T, BN, kSpNT>(sK + (kt & 1) * kKV, k + head, (kt + 2) * BN, L);
+        cp_async_commit();
+        if (kt > 0) {
+            mbar_wait_bounded(&bars[1], ph_o);
+            ph_o ^= 1;
+            tc_fence_after();
+        }
+        if (kt + 1 < nkt)
+            load_tile_nt<T, BN, kSpNT>(sV + ((kt + 1) & 1) * kKV, v + head, (kt + 1) * BN, L);
+        cp_async_commit();
+        softmax_half(sv, kt);
+        cp_async_wait<2>();
+        sync_for_mma();
+        issue_pv(kt);
+    }
+    mbar_wait_bounded(&bars[1], ph_o);
+    ph_o ^= 1;
+    tc_fence_after();
+
+    // ---- o = O / l: the two halves' partial sums meet in shared memory
+    xch[hf * 128 + r] = l_run;  // (the last tile's max exchange has been read: barrier above)
+    {
+        float ov[32];
+        tc_ld32(t_o, ov);
+        __syncthreads();
+        const float l = xch[r] + xch[128 + r];
+        if (row < S) {
+            const float inv = 1.0f / l;
+            T* orow = out + head + (size_t)row * kD + hf * 32;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                float y[8];
+#pragma unroll
+                for (int e = 0; e < 8; ++e) y[e] = ov[j * 8 + e] * inv;
+                Raw<16> w;
+                Elem<T>::template pack<16>(y, w);
+                reinterpret_cast<uint4*>(orow)[j] = make_uint4(w.w[0], w.w[1], w.w[2], w.w[3]);
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tmem)
+                     : "memory");
+    }
+}
+
 namespace {
 std::atomic<int> g_attn_nbuf{0};  // 0 = automatic (variant 4)
 
@@ -785,6 +1029,32 @@ cudaError_t launch_attn_ws(void* out, const void* q, const void* k, const void* 
     return cudaGetLastError();
 }
 
+template <typename T, int MINB>
+cudaError_t launch_attn_split(void* out, const void* q, const void* k, const void* v,
+                              const int32_t* lengths, int64_t B, int64_t H, int64_t S, float scale,
+                              cudaStream_t st) {
+    static std::atomic<int> attr{0};
+    if (!attr.load()) {
+        for (auto kern : {attention_split_kernel<T, true, MINB>,
+                          attention_split_kernel<T, false, MINB>}) {
+            cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)kSpSmem);
+            if (e != cudaSuccess) return e;
+        }
+        attr.store(1);
+    }
+    dim3 grid((unsigned)((S + kBM - 1) / kBM), (unsigned)H, (unsigned)B);
+    float c = scale * 1.4426950408889634f;
+    if (c == 0.f) c = 1e-30f;
+    auto kern = c > 0.f ? attention_split_kernel<T, true, MINB>
+                        : attention_split_kernel<T, false, MINB>;
+    const cudaError_t le_ = launch_k(kern, grid, kSpNT, kSpSmem, st, static_cast<T*>(out),
+                                     static_cast<const T*>(q), static_cast<const T*>(k),
+                                     static_cast<const T*>(v), lengths, (int)H, (int)S, c);
+    if (le_ != cudaSuccess) return le_;
+    return cudaGetLastError();
+}
+
 template <typename T>
 cudaError_t launch_attn_any(void* out, const void* q, const void* k, const void* v,
                             const int32_t* lengths, int64_t B, int64_t H, int64_t S, float scale,
@@ -796,13 +1066,15 @@ cudaError_t launch_attn_any(void* out, const void* q, const void* k, const void*
         case 2: return launch_attn<T, 2, 128>(out, q, k, v, lengths, B, H, S, scale, st);
         case 3: return launch_attn<T, 1, 64>(out, q, k, v, lengths, B, H, S, scale, st);
         case 5: return launch_attn_ws<T>(out, q, k, v, lengths, B, H, S, scale, st);
+        case 6: return launch_attn_split<T, 2>(out, q, k, v, lengths, B, H, S, scale, st);
+        case 7: return launch_attn_split<T, 3>(out, q, k, v, lengths, B, H, S, scale, st);
         default: return launch_attn<T, 2, 64>(out, q, k, v, lengths, B, H, S, scale, st);
     }
 }
 }  // namespace
 
 bool attention_force_variant(int v) {
-    if (v < 0 || v > 5) return false;
+    if (v < 0 || v > 7) return false;
     g_attn_nbuf.store(v);
     return true;
 }
