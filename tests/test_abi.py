@@ -180,3 +180,21 @@ def test_packed_validation(ttlib, dtype):
     for args in ((0, 12, 100, 50), (4, 0, 100, 50), (4, 12, 0, 50), (4, 12, 100, 0)):
         assert f(0, 0, 0, *args, 1.0, 0) == OK
     assert ttlib.softmax_packed_plan(dtype, 512).startswith("softmax_packed<")
+
+
+def test_staged_overlap_validation(ttlib):
+    """Host-side validation of the overlapped staging calls (include/tt.h): bad
+    arguments are rejected before any CUDA call; empty problems are no-ops."""
+    L = ttlib.lib()
+    INV, OK = 1, 0
+    fs = L.tt_softmax_masked_staged_overlap
+    # null host buffers, with a distinct copy stream and several chunks
+    assert fs(1, 0, 0, FAKE, FAKE, 2, 2, 2, 8, 1.0, 4, 0, FAKE) == INV
+    assert fs(1, FAKE, FAKE, 0, FAKE, 2, 2, 2, 8, 1.0, 4, 0, FAKE) == INV       # null device
+    assert fs(1, FAKE, FAKE, FAKE, FAKE, 2, 2, 2, 8, math.nan, 4, 0, FAKE) == INV
+    assert fs(1, 0, 0, 0, 0, 0, 2, 2, 8, 1.0, 4, 0, FAKE) == OK                 # empty
+    fl = L.tt_add_bias_layernorm_staged_overlap
+    assert fl(2, 0, 0, 0, FAKE, FAKE, FAKE, FAKE, FAKE, FAKE, 4, 64, 1e-5, 4, 0, FAKE) == INV
+    assert fl(2, FAKE, FAKE, FAKE, FAKE, FAKE, FAKE, FAKE, FAKE, FAKE, 4, 64, -1.0, 4, 0,
+              FAKE) == INV                                                      # eps < 0
+    assert fl(2, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 64, 1e-5, 4, 0, FAKE) == OK      # empty
