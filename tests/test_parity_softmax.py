@@ -137,6 +137,23 @@ def test_short_requests_narrow_groups(ttlib, dtype, Sk):
 
 
 @pytest.mark.parametrize("dtype", DT)
+@pytest.mark.parametrize("Sk", [100, 200, 250, 256, 300, 500])
+def test_short_requests_fewer_vectors(ttlib, dtype, Sk):
+    """Multi-vector tiers (NV > 1): a CTA whose rows all belong to one short
+    request runs them with the fewest vectors per lane that hold L_b keys
+    (softmax_narrow_nv).  256 rows per request so that whole CTAs belong to one
+    request; lengths at every K * G * VE boundary of the G8 (16-bit) and G32
+    (fp32) tiers, aligned and unaligned pitches, poison in the padding."""
+    lens = [1, 7, 8, 9, 31, 32, 33, 63, 64, 65, 127, 128, 129, 191, 192, 193, 255, 256, 257,
+            Sk - 1, Sk, 0]
+    lens = [min(l, Sk) for l in lens]
+    x = W.scores(len(lens), 4, 64, Sk, dtype, seed=Sk + 1)
+    _full_check(ttlib, x, lens, W.SCALE_BERT, f"fewer-vectors Sk={Sk}")
+    xp = W.poison_masked(x, lens)
+    _full_check(ttlib, xp, lens, -0.25, f"fewer-vectors poison Sk={Sk}")
+
+
+@pytest.mark.parametrize("dtype", DT)
 def test_length_edge_values(ttlib, dtype):
     Sk = 70
     lens = [0, -5, 1, 69, 70, 71, 1 << 30, -(1 << 30)]
