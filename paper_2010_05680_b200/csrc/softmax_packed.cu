@@ -131,7 +131,13 @@ int sm_count_p() {
 template <typename T, int NV, int MINB>
 cudaError_t launch_packed(void* scores, const int32_t* cu, const int64_t* blocks, int num_req,
                           int64_t H, int64_t total_rows, float scale, cudaStream_t st) {
-    constexpr int NT = 256, GPB = NT / 32, RPG = 4;
+// 4 rows per warp per CTA: measured against 8 and 16 (idle warps when short
+// requests use 4-lane groups notwithstanding): C3 packed step 0.0887 / 0.0890 /
+// 0.0962 ms, C5 packed stream 5.17 / 5.20 / 5.66 ms (profiles/r01_packed_rpg/)
+#ifndef TT_PACKED_RPG
+#define TT_PACKED_RPG 4
+#endif
+    constexpr int NT = 256, GPB = NT / 32, RPG = TT_PACKED_RPG;
     const int64_t per_cta = (int64_t)GPB * RPG;
     const int64_t grid = (total_rows + per_cta - 1) / per_cta;
     if (grid > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
