@@ -33,8 +33,8 @@ TT_API tt_status ttx_force_tier(int op, int dtype, int i);
  * double-buffered and software-pipelined (3 CTAs per SM), 5 = warp-specialised
  * (producer warp, MMA warp, 4 softmax warps; mbarrier hand-offs, no CTA barrier
  * in the tile loop; 2 CTAs per SM), 6 / 7 = variant 4 with two threads per
- * query row (8 warps; 2 / 3 CTAs per SM).  Returns TT_ERROR_INVALID_VALUE
- * outside 0..7. */
+ * query row (8 warps; 2 / 3 CTAs per SM), 8 = variant 4 waiting for the previous
+ * P.V only after the exponentials.  Returns TT_ERROR_INVALID_VALUE outside 0..8. */
 TT_API tt_status ttx_attention_variant(int v);
 
 /* Programmatic dependent launch (PDL, default on): every kernel is launched

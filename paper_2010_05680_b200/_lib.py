@@ -378,7 +378,8 @@ def attention_variant(v: int):
     tiles double-buffered, pipelined (1 CTA/SM), 3 = 64-key tiles (4 CTAs/SM),
     4 = 64-key tiles double-buffered, pipelined (3 CTAs/SM), 5 = warp-specialised
     (producer / MMA / softmax warps, mbarrier hand-offs, 2 CTAs/SM), 6 / 7 = variant 4
-    with two threads per query row (2 / 3 CTAs/SM)."""
+    with two threads per query row (2 / 3 CTAs/SM), 8 = variant 4 with the previous
+    P.V waited for after the exponentials."""
     _check(lib().ttx_attention_variant(int(v)), "ttx_attention_variant")
 
 

@@ -193,7 +193,7 @@ constexpr int attn_tmem_cols() {
     return BN + kD <= 128 ? 128 : 256;
 }
 
-template <typename T, int NBUF, int BN, bool UP>
+template <typename T, int NBUF, int BN, bool UP, bool LATE = false>
 __global__ void __launch_bounds__(kNT, attn_minb<NBUF, BN>())
     attention_tc_kernel(T* __restrict__ out, const T* __restrict__ q, const T* __restrict__ k,
                         const T* __restrict__ v, const int32_t* __restrict__ lengths, int H,
@@ -298,7 +298,9 @@ __global__ void __launch_bounds__(kNT, attn_minb<NBUF, BN>())
     // online softmax of tile kt from registers: mask (partial tile only), max,
     // conditional O rescale (the previous P.V must have completed), then
     // p = 2^(s c - m_ref) -> P in shared memory, row sum -> l
-    auto softmax_tile = [&](float (&sv)[BN], int kt) {
+    // wait_pv: called before O or P is touched (LATE: P.V(kt-1) is waited for
+    // here, after the exponentials, instead of before the softmax)
+    auto softmax_tile = [&](float (&sv)[BN], int kt, auto&& wait_pv) {
         const int key0 = kt * BN;
         if (key0 + BN > L) {
 #pragma unroll
@@ -311,6 +313,7 @@ __global__ void __launch_bounds__(kNT, attn_minb<NBUF, BN>())
         if (kt == 0) {
             m_ref = m_tile;  // nothing accumulated yet
         } else if (__any_sync(0xffffffffu, m_tile > m_ref + kRescale)) {
+            wait_pv();
             const float m_new = fmaxf(m_ref, m_tile);
             const float alpha = ex2_approx(m_ref - m_new);
             l_run *= alpha;
@@ -326,6 +329,33 @@ __global__ void __launch_bounds__(kNT, attn_minb<NBUF, BN>())
         }
         const F2 c2 = f2_make(c, c), nm2 = f2_make(-m_ref, -m_ref);
         F2 ps2 = f2_make(0.f, 0.f);
+        if constexpr (LATE) {
+            // every exponential first (in place), then wait for P.V(kt-1), then P
+#pragma unroll
+            for (int e = 0; e < BN; e += 2) {
+                float t0, t1;
+                f2_split(f2_fma(f2_make(sv[e], sv[e + 1]), c2, nm2), t0, t1);
+                sv[e] = ex2_approx(t0);
+                sv[e + 1] = ex2_approx(t1);
+                ps2 = f2_add(ps2, f2_make(sv[e], sv[e + 1]));
+            }
+            wait_pv();
+#pragma unroll
+            for (int ch = 0; ch < NCH; ++ch)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    Raw<16> w;
+                    Elem<T>::template pack<16>(sv + ch * 32 + 8 * j, w);
+                    const uint32_t off =
+                        (uint32_t)(ch >> 1) * kTile + sw_off(tid, (ch & 1) * 4 + j);
+                    *reinterpret_cast<uint4*>(prow + off) =
+                        make_uint4(w.w[0], w.w[1], w.w[2], w.w[3]);
+                }
+            float a0, a1;
+            f2_split(ps2, a0, a1);
+            l_run += a0 + a1;
+            return;
+        }
 #pragma unroll
         for (int ch = 0; ch < NCH; ++ch) {
             float pv[32];
@@ -374,7 +404,7 @@ __global__ void __launch_bounds__(kNT, attn_minb<NBUF, BN>())
             }
             float sv[BN];
             load_s(sv);
-            softmax_tile(sv, kt);
+            softmax_tile(sv, kt, [] {});
             if (kt + 1 < nkt)  // V(kt) (K(kt + 1) may still be in flight)
                 cp_async_wait<1>();
             else
@@ -415,15 +445,30 @@ __global__ void __launch_bounds__(kNT, attn_minb<NBUF, BN>())
             // E: K(kt) buffer is free (S(kt) completed)
             if (kt + 2 < nkt) load_tile<T, BN>(sK + (kt & 1) * kKV, k + head, (kt + 2) * BN, L);
             cp_async_commit();
-            // F: P.V(kt-1) done -> P, O and V((kt+1) & 1) are free
-            if (kt > 0) {
-                mbar_wait_bounded(&bars[1], ph_o);
-                ph_o ^= 1;
-                tc_fence_after();
+            // F: P.V(kt-1) done -> P, O and V((kt+1) & 1) are free (LATE: waited
+            // for inside the softmax, after the exponentials)
+            bool pv_done = kt == 0;
+            auto wait_pv = [&]() {
+                if (!pv_done) {
+                    mbar_wait_bounded(&bars[1], ph_o);
+                    ph_o ^= 1;
+                    tc_fence_after();
+                    pv_done = true;
+                }
+            };
+            if constexpr (!LATE) {
+                wait_pv();
+                if (kt + 1 < nkt)
+                    load_tile<T, BN>(sV + ((kt + 1) & 1) * kKV, v + head, (kt + 1) * BN, L);
+                cp_async_commit();
             }
-            if (kt + 1 < nkt) load_tile<T, BN>(sV + ((kt + 1) & 1) * kKV, v + head, (kt + 1) * BN, L);
-            cp_async_commit();
-            softmax_tile(sv, kt);
+            softmax_tile(sv, kt, wait_pv);
+            if constexpr (LATE) {
+                wait_pv();
+                if (kt + 1 < nkt)
+                    load_tile<T, BN>(sV + ((kt + 1) & 1) * kKV, v + head, (kt + 1) * BN, L);
+                cp_async_commit();
+            }
             cp_async_wait<2>();  // G: V(kt) (K(kt+2), V(kt+1) may still be in flight)
             sync_for_mma();
             issue_pv(kt);
@@ -973,15 +1018,15 @@ __global__ void __launch_bounds__(kSpNT, MINB)
 namespace {
 std::atomic<int> g_attn_nbuf{0};  // 0 = automatic (variant 4)
 
-template <typename T, int NBUF, int BN>
+template <typename T, int NBUF, int BN, bool LATE = false>
 cudaError_t launch_attn(void* out, const void* q, const void* k, const void* v,
                         const int32_t* lengths, int64_t B, int64_t H, int64_t S, float scale,
                         cudaStream_t st) {
     constexpr size_t smem = attn_smem<NBUF, BN>();
     static std::atomic<int> attr{0};
     if (!attr.load()) {
-        for (auto kern : {attention_tc_kernel<T, NBUF, BN, true>,
-                          attention_tc_kernel<T, NBUF, BN, false>}) {
+        for (auto kern : {attention_tc_kernel<T, NBUF, BN, true, LATE>,
+                          attention_tc_kernel<T, NBUF, BN, false, LATE>}) {
             cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                  (int)smem);
             if (e != cudaSuccess) return e;
@@ -993,8 +1038,8 @@ cudaError_t launch_attn(void* out, const void* q, const void* k, const void* v,
     // softmax kernels do), so the masked-key sentinel still maps to p = +0
     float c = scale * 1.4426950408889634f;
     if (c == 0.f) c = 1e-30f;
-    auto kern = c > 0.f ? attention_tc_kernel<T, NBUF, BN, true>
-                        : attention_tc_kernel<T, NBUF, BN, false>;
+    auto kern = c > 0.f ? attention_tc_kernel<T, NBUF, BN, true, LATE>
+                        : attention_tc_kernel<T, NBUF, BN, false, LATE>;
     {
         const cudaError_t le_ = launch_k(kern, grid, kNT, smem, st,
             static_cast<T*>(out), static_cast<const T*>(q),
@@ -1068,13 +1113,14 @@ cudaError_t launch_attn_any(void* out, const void* q, const void* k, const void*
         case 5: return launch_attn_ws<T>(out, q, k, v, lengths, B, H, S, scale, st);
         case 6: return launch_attn_split<T, 2>(out, q, k, v, lengths, B, H, S, scale, st);
         case 7: return launch_attn_split<T, 3>(out, q, k, v, lengths, B, H, S, scale, st);
+        case 8: return launch_attn<T, 2, 64, true>(out, q, k, v, lengths, B, H, S, scale, st);
         default: return launch_attn<T, 2, 64>(out, q, k, v, lengths, B, H, S, scale, st);
     }
 }
 }  // namespace
 
 bool attention_force_variant(int v) {
-    if (v < 0 || v > 7) return false;
+    if (v < 0 || v > 8) return false;
     g_attn_nbuf.store(v);
     return true;
 }

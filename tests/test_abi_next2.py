@@ -62,7 +62,7 @@ def test_attention_validation(ttlib, dt):
 
 def test_attention_variant_hook(ttlib):
     h = ttlib.lib().ttx_attention_variant
-    for v in range(8):
+    for v in range(9):
         assert h(v) == OK
-    assert h(-1) == INV and h(8) == INV
+    assert h(-1) == INV and h(9) == INV
     assert h(0) == OK

@@ -15,7 +15,7 @@ DT = [torch.float16, torch.bfloat16]
 TOL = {torch.float16: 4e-3, torch.bfloat16: 8e-3}
 
 
-@pytest.fixture(params=[1, 2, 3, 4, 5, 6, 7], ids=["bn128", "bn128x2", "bn64", "bn64x2", "ws", "split", "split3"])
+@pytest.fixture(params=[1, 2, 3, 4, 5, 6, 7, 8], ids=["bn128", "bn128x2", "bn64", "bn64x2", "ws", "split", "split3", "late"])
 def variant(ttlib, request):
     """Every kernel variant (ttx_attention_variant: tile width and K/V buffering)."""
     ttlib.attention_variant(request.param)

@@ -53,7 +53,7 @@ def case(name, B, H, S, dtype, lens):
     outs = [torch.empty(B, H, S, D, device="cuda", dtype=dtype) for _ in range(nb)]
     L = torch.as_tensor(np.asarray(lens, dtype=np.int32)).cuda()
     var_us = {}
-    for v in (1, 2, 3, 4, 5, 6, 7):
+    for v in (1, 2, 3, 4, 5, 6, 7, 8):
         tt.attention_variant(v)
         var_us[v] = timeit(lambda i: tt.tt_attention_fwd(outs[i], *qkv[i], L, 0.125), nb)
     tt.attention_variant(0)
@@ -66,7 +66,7 @@ def case(name, B, H, S, dtype, lens):
                bn128_us=round(var_us[1], 2), bn128x2_us=round(var_us[2], 2),
                bn64_us=round(var_us[3], 2), bn64x2_us=round(var_us[4], 2),
                ws_us=round(var_us[5], 2), split_us=round(var_us[6], 2),
-               split3_us=round(var_us[7], 2))
+               split3_us=round(var_us[7], 2), late_us=round(var_us[8], 2))
     # unfused: QK^T (cuBLAS), masked softmax (ours, in place), PV (cuBLAS)
     sc = torch.empty(B, H, S, S, device="cuda", dtype=dtype)
 
