@@ -16,7 +16,15 @@
  *             frees or synchronises, needs no workspace and keeps no handles.
  * Devices     Device pointers must be on the current CUDA device.
  * Execution   Asynchronous on `stream` (0 = legacy default stream); results
- *             are visible after the caller synchronises the stream.
+ *             are visible after the caller synchronises the stream.  Kernels
+ *             are launched with programmatic dependent launch (PDL): a kernel
+ *             may be scheduled while the previous kernel in the stream drains,
+ *             but executes griddepcontrol.wait before its first global access,
+ *             so stream order is kept for every memory effect; it signals its
+ *             own dependents only after its last store.  A caller kernel that
+ *             is itself launched programmatically after a libtt call must
+ *             execute griddepcontrol.wait before reading libtt's output (as
+ *             with any PDL producer).  ttx_set_pdl(0) (tt_tune.h) turns it off.
  * Alignment   Every tensor base pointer must be 16-byte aligned (any
  *             cudaMalloc / PyTorch allocation is); rows may have any length.
  * Errors      Arguments are validated on the host BEFORE any CUDA call:
