@@ -106,3 +106,24 @@ def test_dependent_chain_in_cuda_graph(ttlib):
     torch.cuda.synchronize()
     for a, b in zip(eager, bufs):
         assert torch.equal(a.view(torch.uint8), b.view(torch.uint8))
+
+
+def test_every_kernel_opens_with_pdl_scope():
+    """Static check of the PDL invariant (include/tt.h Execution): every
+    __global__ function in csrc/ starts with `PdlScope pdl_;` (griddepcontrol.wait
+    before any global access), and every launch goes through launch_k."""
+    import glob
+    import os
+    import re
+    root = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                        "paper_2010_05680_b200", "csrc")
+    n = 0
+    for f in glob.glob(os.path.join(root, "*.cu")):
+        src = open(f).read()
+        assert "<<<" not in src, f"{f}: raw <<<>>> launch bypasses launch_k (PDL attribute)"
+        for m in re.finditer(r"__global__", src):
+            body = src.index(") {\n", m.start()) + 4
+            first = src[body:src.index("\n", body)].strip()
+            assert first.startswith("PdlScope pdl_;"), (f, first)
+            n += 1
+    assert n >= 12
