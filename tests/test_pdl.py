@@ -127,3 +127,46 @@ def test_every_kernel_opens_with_pdl_scope():
             assert first.startswith("PdlScope pdl_;"), (f, first)
             n += 1
     assert n >= 12
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("variant", [0, 5, 6])
+def test_attention_block_chain_pdl_on_off_identical(ttlib, variant):
+    """A whole dependent BERT attention block through the library, every kernel
+    reading what the previous one wrote: QKV split + bias -> fused attention
+    (tcgen05) -> head merge -> add-bias LayerNorm (residual) -> add-bias GELU.
+    Bitwise identical with PDL on and off, for the default, warp-specialised
+    and split-row attention schedules."""
+    dtype = torch.bfloat16
+    B, S, H, D = 3, 200, 4, 64
+    g = torch.Generator(device="cuda").manual_seed(7)
+    qkv = torch.randn(B * S, 3 * H * D, device="cuda", dtype=dtype, generator=g)
+    bqkv = torch.randn(3 * H * D, device="cuda", dtype=dtype, generator=g) * 0.1
+    res = torch.randn(B * S, H * D, device="cuda", dtype=dtype, generator=g)
+    bo, gam, bet = (torch.randn(H * D, device="cuda", dtype=dtype, generator=g) * 0.1
+                    for _ in range(3))
+    gam = gam + 1
+    lens = torch.tensor([200, 77, 1], dtype=torch.int32, device="cuda")
+    outs = {}
+    old = ttlib.get_pdl()
+    try:
+        ttlib.attention_variant(variant)
+        for pdl in (False, True):
+            ttlib.set_pdl(pdl)
+            q, k, v = (torch.empty(B, H, S, D, device="cuda", dtype=dtype) for _ in range(3))
+            ttlib.tt_split_qkv_add_bias(q, k, v, qkv, bqkv, B, S, H, D)
+            o = torch.empty_like(q)
+            ttlib.tt_attention_fwd(o, q, k, v, lens, 0.125)
+            m = torch.empty(B * S, H * D, device="cuda", dtype=dtype)
+            ttlib.tt_merge_heads(m, o, B, S, H, D)
+            ln = torch.empty_like(m)
+            ttlib.tt_add_bias_layernorm(ln, m, res, bo, gam, bet, 1e-12)
+            y = torch.empty_like(ln)
+            ttlib.tt_add_bias_gelu(y, ln, bo)
+            torch.cuda.synchronize()
+            outs[pdl] = y.cpu()
+    finally:
+        ttlib.set_pdl(old)
+        ttlib.attention_variant(0)
+    assert torch.isfinite(outs[True].float()).all()
+    assert torch.equal(outs[False].view(torch.int16), outs[True].view(torch.int16))
