@@ -810,10 +810,12 @@ struct Pref {
 // (ln_rows EARLY tiers), so no dependent load follows the reductions
 // (EARLY costs registers, so only for the tiniest problems)
 constexpr int64_t kTinyRows = 2048, kSmallRows = 8192;
+// (f16 / f32 at hidden 768 re-tuned on C2's S = 128 .. 400 LayerNorm shapes,
+// profiles/r01_tune_lnmid/: 128-thread CTAs, +1..7 % over the 256-thread tiers)
 const Pref kLnPrefSmall[] = {
-    {0, 512, 768, "ln_rows<f32,V32,G32,NV3,R1,T256,M1>"},
+    {0, 512, 768, "ln_rows<f32,V32,G32,NV4,R1,T128,M1>"},
     {0, 768, 1024, "ln_rows<f32,V32,G32,NV4,R1,T256,M1>"},
-    {1, 512, 768, "ln_rows<f16,V16,G32,NV3,R1,T256,M1>"},
+    {1, 512, 768, "ln_rows<f16,V16,G32,NV3,R1,T128,M1,E>"},
     {1, 768, 1024, "ln_rows<f16,V32,G32,NV2,R1,T256,M1>"},
     {2, 512, 768, "ln_rows<bf16,V16,G32,NV3,R1,T256,M1>"},
     {2, 768, 1024, "ln_rows<bf16,V32,G32,NV2,R1,T256,M1>"},
