@@ -820,10 +820,23 @@ const Pref kLnPrefSmall[] = {
     {2, 512, 768, "ln_rows<bf16,V16,G32,NV3,R1,T256,M1>"},
     {2, 768, 1024, "ln_rows<bf16,V32,G32,NV2,R1,T256,M1>"},
 };
+// Very few rows: one CTA (four warps) per row, so the rows spread over as many
+// SMs as there are rows and every thread issues only a few loads (re-tuned on
+// C1 / C2 S = 10 .. 40, profiles/r01_tune_lntiny/: fp16 40 rows 2.67 -> 1.84 us,
+// 200 rows 3.35 -> 1.98 us; fp32 40 rows 2.43 -> 1.90 us, 400 rows 3.90 -> 2.96 us).
+constexpr int64_t kMicroRows = 256, kMiniRows = 1024;
+const Pref kLnPrefMicro[] = {
+    {0, 512, 768, "ln_rows<f32,V32,G128,NV4,R1,T128,M1>"},
+    {1, 512, 768, "ln_rows<f16,V32,G128,NV2,R1,T128,M1>"},
+};
+const Pref kLnPrefMini[] = {
+    {0, 512, 768, "ln_rows<f32,V32,G128,NV4,R1,T128,M1>"},
+    {1, 512, 768, "ln_rows<f16,V16,G128,NV4,R1,T128,M1>"},
+};
 const Pref kLnPrefTiny[] = {
     {0, 512, 768, "ln_rows<f32,V32,G32,NV3,R1,T256,M1,E>"},
     {0, 768, 1024, "ln_rows<f32,V32,G32,NV4,R1,T256,M1,E>"},
-    {1, 512, 768, "ln_rows<f16,V16,G32,NV3,R1,T256,M1,E>"},
+    {1, 512, 768, "ln_rows<f16,V32,G32,NV2,R1,T128,M1,E>"},  // 1280 / 2000 rows: -8 / -4 %
     {1, 768, 1024, "ln_rows<f16,V32,G32,NV2,R1,T256,M1,E>"},
     {2, 512, 768, "ln_rows<bf16,V16,G32,NV3,R1,T256,M1,E>"},
     {2, 768, 1024, "ln_rows<bf16,V32,G32,NV2,R1,T256,M1,E>"},
@@ -869,13 +882,19 @@ const LnTier* pick_dtype(int dtype, int64_t hidden, int vec_bytes, int64_t rows)
     if (f >= 0 && f < kLnN && fits(tab[f], hidden, vec_bytes)) return &tab[f];
     // name -> tier index caches, one per preference table (benign race: every
     // thread stores the same index)
+    static std::atomic<int> idx_micro[sizeof(kLnPrefMicro) / sizeof(Pref)];
+    static std::atomic<int> idx_mini[sizeof(kLnPrefMini) / sizeof(Pref)];
     static std::atomic<int> idx_tiny[sizeof(kLnPrefTiny) / sizeof(Pref)];
     static std::atomic<int> idx_small[sizeof(kLnPrefSmall) / sizeof(Pref)];
     static std::atomic<int> idx_large[sizeof(kLnPref) / sizeof(Pref)];
     const LnTier* pbest =
-        rows <= kTinyRows    ? from_prefs(kLnPrefTiny, idx_tiny, dtype, hidden, vec_bytes)
-        : rows <= kSmallRows ? from_prefs(kLnPrefSmall, idx_small, dtype, hidden, vec_bytes)
-                             : from_prefs(kLnPref, idx_large, dtype, hidden, vec_bytes);
+        rows <= kMicroRows  ? from_prefs(kLnPrefMicro, idx_micro, dtype, hidden, vec_bytes)
+        : rows <= kMiniRows ? from_prefs(kLnPrefMini, idx_mini, dtype, hidden, vec_bytes)
+                            : nullptr;
+    if (!pbest)
+        pbest = rows <= kTinyRows    ? from_prefs(kLnPrefTiny, idx_tiny, dtype, hidden, vec_bytes)
+                : rows <= kSmallRows ? from_prefs(kLnPrefSmall, idx_small, dtype, hidden, vec_bytes)
+                                     : from_prefs(kLnPref, idx_large, dtype, hidden, vec_bytes);
     if (pbest) return pbest;
     const LnTier* best = nullptr;
     for (int i = 0; i < kLnN; ++i) {

@@ -131,9 +131,12 @@ def test_softmax_tier_plan(ttlib, dtype, Sk, tier):
 
 
 @pytest.mark.parametrize("dtype,rows,hidden,tier", [
-    (torch.float32, 10, 768, "ln_rows<f32,V32,G32,NV3,R1,T256,M1,E>"),
+    (torch.float32, 10, 768, "ln_rows<f32,V32,G128,NV4,R1,T128,M1>"),
+    (torch.float32, 2000, 768, "ln_rows<f32,V32,G32,NV3,R1,T256,M1,E>"),
     (torch.float32, 30000, 768, "ln_rows<f32,V32,G32,NV3,R1,T256,M1>"),
-    (torch.float16, 10, 768, "ln_rows<f16,V16,G32,NV3,R1,T256,M1,E>"),
+    (torch.float16, 10, 768, "ln_rows<f16,V32,G128,NV2,R1,T128,M1>"),
+    (torch.float16, 800, 768, "ln_rows<f16,V16,G128,NV4,R1,T128,M1>"),
+    (torch.float16, 2000, 768, "ln_rows<f16,V32,G32,NV2,R1,T128,M1,E>"),
     (torch.float16, 30000, 768, "ln_warp<f16,V16,G32,NV4,T256,M2,PF1>"),
     (torch.bfloat16, 10, 1024, "ln_rows<bf16,V32,G32,NV2,R1,T256,M1,E>"),
     (torch.bfloat16, 32768, 1024, "ln_warp<bf16,V16,G32,NV4,T256,M2,PF1>"),
