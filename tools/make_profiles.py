@@ -55,7 +55,8 @@ def main():
     rnd = sys.argv[1] if len(sys.argv) > 1 else "r01"
     os.makedirs(PROF, exist_ok=True)
     agg = launches(rnd)
-    bench = json.load(open(os.path.join(OUT, "bench.json")))
+    bpath = os.path.join(OUT, "bench.json")
+    bench = json.load(open(bpath)) if os.path.exists(bpath) else {}
     plans = bench.get("kernels", {})
     traffic = {}
     total_ns = sum(sum(m.get("gpu__time_duration.sum", [])) for m in agg.values())
@@ -73,9 +74,12 @@ def main():
         lines.append(f"{k}: launches={len(t)} avg_ns={sum(t)/max(1,len(t)):.0f} "
                      f"share={sum(t)/total_ns:.3f} dram_read={sum(rd)/max(1,len(rd)):.4g} "
                      f"dram_write={sum(wr)/max(1,len(wr)):.4g}")
-    json.dump(traffic, open(os.path.join(PROF, "traffic.json"), "w"), indent=1)
+    if traffic:  # only from a fresh launch list (never overwrite with nothing)
+        json.dump(traffic, open(os.path.join(PROF, "traffic.json"), "w"), indent=1)
     rep = os.path.join(OUT, "prof_c4.ncu-rep")
-    with open(os.path.join(PROF, f"{rnd}_ncu_full.txt"), "w") as f:
+    rep_exists = os.path.exists(os.path.join(OUT, "prof_c4.ncu-rep"))
+    with open(os.path.join(PROF, f"{rnd}_ncu_full.txt"), "w") if (lines or rep_exists) \
+            else open(os.devnull, "w") as f:
         f.write("# ncu --set full --clock-control none, bench.py C4 step (tools/gpu_check.sh NCU=1)\n")
         f.write("# launch-list summary (cold-cache, serialised; compare shares):\n")
         for l in lines:
@@ -93,7 +97,8 @@ def main():
         open(os.path.join(PROF, f"{rnd}_tune.txt"), "w").write(
             "# tools/tune.py sweeps (GB/s algorithmic, CUDA events, inputs > 4x L2); * = automatic tier\n"
             + tune)
-    shutil.copy(os.path.join(OUT, "bench.json"), os.path.join(PROF, f"{rnd}_bench.json"))
+    if bench:
+        shutil.copy(bpath, os.path.join(PROF, f"{rnd}_bench.json"))
     for src, dst, title in (("sweep.jsonl", f"{rnd}_sweep.txt", "tools/sweep.py"),
                             ("sweep_next2.jsonl", f"{rnd}_sweep_next2.txt",
                              "tools/sweep.py --next2 (NEXT-2 kernels)")):
