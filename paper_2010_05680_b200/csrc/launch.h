@@ -12,7 +12,7 @@ namespace tt {
 cudaError_t softmax_launch(int dtype, void* scores, const int32_t* lengths, int64_t nrows,
                            int64_t rows_per_batch, int64_t Sk, float scale, cudaStream_t stream,
                            bool* supported);
-const char* softmax_tier_name(int dtype, int64_t Sk);
+const char* softmax_tier_name(int dtype, int64_t Sk, int64_t nrows);
 
 // Packed (padding-free) softmax: request r is a dense [H, L_r, L_r] block at
 // element offset cu_blocks[r]; L_r = cu_seqlens[r+1] - cu_seqlens[r] <= max_len.

@@ -727,10 +727,15 @@ struct Pref {
     int dtype;
     int min_cols, max_cols;
     const char* name;
+    int64_t min_rows;  // applies only to calls with more rows (0: any)
 };
 // Capacity-fitting sub-warp tiers (G8 with several vectors per lane) win where
 // the warp-per-row tier would leave lanes idle; see profiles/*_tune.txt.
 const Pref kSmPref[] = {
+    // fp32 C2 S = 40 / 64 / 100 (profiles/r01_tune_smtiny/): -31 / -27 / -21 %; not
+    // for C1-sized calls (480 rows: +6 %), hence the row threshold
+    {0, 32, 64, "softmax_warp<f32,V16,G8,NV2,T256,M6,P4>", 2048},
+    {0, 64, 128, "softmax_warp<f32,V16,G8,NV4,T256,M3,P4,F>", 2048},
     {0, 128, 256, "softmax_warp<f32,V32,G32,NV1,T256,M6,P2>"},
     {0, 256, 384, "softmax_warp<f32,V32,G32,NV2,T256,M6,P4>"},
     {0, 384, 512, "softmax_warp<f32,V32,G32,NV2,T256,M3,P2>"},
@@ -745,7 +750,7 @@ const Pref kSmPref[] = {
     {2, 320, 384, "softmax_warp<bf16,V32,G8,NV3,T256,M3,P4>"},
 };
 
-const SoftmaxTier* pick_dtype(int dtype, int64_t Sk) {
+const SoftmaxTier* pick_dtype(int dtype, int64_t Sk, int64_t nrows) {
     const SoftmaxTier* t = table(dtype);
     if (!t) return nullptr;
     const int f = g_force[dtype].load(std::memory_order_relaxed);
@@ -755,7 +760,8 @@ const SoftmaxTier* pick_dtype(int dtype, int64_t Sk) {
     static std::atomic<int> pidx[NP];
     for (int p = 0; p < NP; ++p) {
         const Pref& pr = kSmPref[p];
-        if (pr.dtype != dtype || Sk <= pr.min_cols || Sk > pr.max_cols) continue;
+        if (pr.dtype != dtype || Sk <= pr.min_cols || Sk > pr.max_cols || nrows <= pr.min_rows)
+            continue;
         int k = pidx[p].load(std::memory_order_relaxed);
         if (k == 0) {
             k = -1;
@@ -790,15 +796,15 @@ bool softmax_force_tier(int dtype, int i) {
     return true;
 }
 
-const char* softmax_tier_name(int dtype, int64_t Sk) {
-    const SoftmaxTier* t = pick_dtype(dtype, Sk);
+const char* softmax_tier_name(int dtype, int64_t Sk, int64_t nrows) {
+    const SoftmaxTier* t = pick_dtype(dtype, Sk, nrows);
     return t ? t->name : nullptr;
 }
 
 cudaError_t softmax_launch(int dtype, void* scores, const int32_t* lengths, int64_t nrows,
                            int64_t rows_per_batch, int64_t Sk, float scale, cudaStream_t stream,
                            bool* supported) {
-    const SoftmaxTier* t = pick_dtype(dtype, Sk);
+    const SoftmaxTier* t = pick_dtype(dtype, Sk, nrows);
     *supported = t != nullptr;
     if (!t) return cudaSuccess;
     return t->fn(scores, lengths, nrows, rows_per_batch, (int)Sk, scale, stream);

@@ -546,7 +546,7 @@ tt_status tt_softmax_masked_plan(int dtype, int64_t B, int64_t H, int64_t Sq, in
         copy_name("", buf, cap);
         return s;
     }
-    copy_name(empty ? "none" : tt::softmax_tier_name(dtype, Sk), buf, cap);
+    copy_name(empty ? "none" : tt::softmax_tier_name(dtype, Sk, nrows), buf, cap);
     return TT_SUCCESS;
 }
 
