@@ -201,3 +201,15 @@ def test_staged_overlap_validation(ttlib):
     assert fl(2, FAKE, FAKE, FAKE, FAKE, FAKE, FAKE, FAKE, FAKE, FAKE, 4, 64, -1.0, 4, 0,
               FAKE) == INV                                                      # eps < 0
     assert fl(2, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 64, 1e-5, 4, 0, FAKE) == OK      # empty
+
+
+def test_softmax_preference_row_threshold(ttlib):
+    """Small fp32 rows pick the 8-lane multi-vector tiers only for calls of more
+    than 2048 rows (C2), not for C1-sized calls (DESIGN §5 "Small fp32 rows")."""
+    f32 = torch.float32
+    assert ttlib.softmax_plan(f32, 20, 12, 40, 40) == "softmax_warp<f32,V16,G8,NV2,T256,M6,P4>"
+    assert ttlib.softmax_plan(f32, 1, 12, 40, 40) == "softmax_warp<f32,V16,G16,NV1,T256,M6,P4>"
+    assert ttlib.softmax_plan(f32, 20, 12, 100, 100) == "softmax_warp<f32,V16,G8,NV4,T256,M3,P4,F>"
+    # LayerNorm bands at hidden 768: one CTA per row up to 1024 rows
+    assert ttlib.layernorm_plan(f32, 40, 768) == "ln_rows<f32,V32,G128,NV4,R1,T128,M1>"
+    assert ttlib.layernorm_plan(f32, 5000, 768) == "ln_rows<f32,V32,G32,NV4,R1,T128,M1>"
