@@ -260,3 +260,43 @@ def schedule_bruteforce(lengths, cost, max_batch: int):
         if c < best:
             best, best_plan = c, plan
     return best, best_plan
+
+
+def set_partitions(n: int):
+    """Every partition of {0..n-1} into non-empty blocks, as lists of index
+    lists, by restricted growth strings a[0] = 0, a[i] <= 1 + max(a[:i])
+    (each partition exactly once; there are Bell(n) of them)."""
+    if n == 0:
+        yield []
+        return
+    a = [0] * n
+
+    def rec(i, m):
+        if i == n:
+            blocks = [[] for _ in range(m + 1)]
+            for idx, b in enumerate(a):
+                blocks[b].append(idx)
+            yield blocks
+            return
+        for b in range(m + 2):
+            a[i] = b
+            yield from rec(i + 1, max(m, b))
+
+    yield from rec(1, 0)
+
+
+def schedule_setpartition_bruteforce(lengths, cost, max_batch: int):
+    """Exhaustive minimum of Alg. 2's objective (Eq. 2, l.609-615)
+    over EVERY partition of the requests into batches of at most max_batch --
+    not only the contiguous runs of the length-sorted list that Alg. 2 itself
+    searches (l.619-648).  Bell(n) plans: n <= 10 only.  Returns (min_cost,
+    one optimal plan as lists of request indices)."""
+    n = len(lengths)
+    best, best_plan = float("inf"), None
+    for plan in set_partitions(n):
+        if any(len(b) > max_batch for b in plan):
+            continue
+        c = plan_cost(lengths, cost, plan)
+        if c < best:
+            best, best_plan = c, plan
+    return best, best_plan

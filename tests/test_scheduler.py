@@ -119,3 +119,89 @@ def test_oracle_bruteforce_itself_on_a_hand_case():
     assert oracle.schedule_bruteforce(lens, c1, 2) == (2.0, [[0], [1]])
     assert oracle.schedule_bruteforce(lens, c2, 2) == (0.8, [[0, 1]])
     assert len(list(itertools.product([0, 1], repeat=3))) == 8
+
+
+# ---- set-partition oracle (independent of Alg. 2's contiguity premise) ----
+def test_set_partitions_count_is_bell():
+    """Pin: the enumerator yields each partition of {0..n-1} once; the counts
+    are the Bell numbers 1, 1, 2, 5, 15, 52, 203, 877, 4140 (OEIS A000110)."""
+    bell = [1, 1, 2, 5, 15, 52, 203, 877, 4140]
+    for n, b in enumerate(bell):
+        parts = list(oracle.set_partitions(n))
+        assert len(parts) == b
+        canon = {tuple(sorted(tuple(sorted(blk)) for blk in p)) for p in parts}
+        assert len(canon) == b
+        for p in parts:
+            assert sorted(i for blk in p for i in blk) == list(range(n))
+            assert all(blk for blk in p)
+
+
+def test_setpartition_oracle_hand_cases():
+    """Pins by hand: (i) lengths 1, 9, 1 with a cost linear in the padded
+    length: batching the two 1s together (and 9 alone) is optimal, a plan that
+    is non-contiguous in queue order; (ii) a non-monotone table (padding to 2
+    is cheaper than to 1) makes a non-contiguous batch strictly better than any
+    contiguous run of the sorted list, so the two oracles differ."""
+    lens = [1, 9, 1]
+    c = _table(9, 3, lambda L, k: float(L) + 3.0 / k)
+    best, plan = oracle.schedule_setpartition_bruteforce(lens, c, 3)
+    assert sorted(sorted(b) for b in plan) == [[0, 2], [1]]
+    assert best == 2 * (1 + 1.5) + (9 + 3)
+    # (ii) sorted order 1, 2, 3; cost per request: L=1 -> 5, L=2 -> 1, L=3 -> 4 (any k)
+    lens = [1, 2, 3]
+    c = _table(3, 3, lambda L, k: {1: 5.0, 2: 1.0, 3: 4.0}[L])
+    sp, plan = oracle.schedule_setpartition_bruteforce(lens, c, 2)
+    assert sp == 2 * 1.0 + 4.0 and sorted(sorted(b) for b in plan) == [[0, 1], [2]]
+    ct, _ = oracle.schedule_bruteforce(lens, c, 2)
+    assert ct == sp                                # {1,2} is also a sorted run here
+    lens = [1, 3, 2]                               # same multiset, other queue order
+    assert oracle.schedule_setpartition_bruteforce(lens, c, 2)[0] == 6.0
+    # (iii) a table where padding to 2 is cheaper than to 1 alone (non-monotone):
+    # the optimum batches the shortest with the longest request, {1, 3}, which is
+    # not a contiguous run of the sorted list, so Alg. 2's search space misses it
+    lens = [1, 2, 3]
+    tab = {(1, 1): 5.0, (2, 1): 1.0, (3, 1): 10.0, (1, 2): 9.0, (2, 2): 10.0, (3, 2): 1.0}
+    c = _table(3, 2, lambda L, k: tab[(L, k)])
+    sp, plan = oracle.schedule_setpartition_bruteforce(lens, c, 2)
+    ct, _ = oracle.schedule_bruteforce(lens, c, 2)
+    assert sorted(sorted(b) for b in plan) == [[0, 2], [1]] and sp == 2 * 1.0 + 1.0
+    assert ct == 2 * 1.0 + 5.0 and sp < ct
+
+
+def _monotone_table(rng, max_len, max_batch):
+    """cached_cost[L][k] nondecreasing in L for every k (positive increments)."""
+    c = np.full((max_len + 1, max_batch + 1), np.nan)
+    for k in range(1, max_batch + 1):
+        base = float(rng.uniform(0.1, 5.0))
+        inc = rng.uniform(0.0, 1.0, size=max_len) * (rng.uniform(size=max_len) < 0.6)
+        c[1:, k] = base + np.cumsum(inc)
+    return c
+
+
+@pytest.mark.parametrize("seed", range(30))
+def test_dp_equals_setpartition_minimum_when_cost_monotone_in_length(ttlib, seed):
+    """When cached_cost is nondecreasing in the padded length, restricting the
+    search to contiguous runs of the sorted list (Alg. 2's premise, PAPER.md
+    l.619-648) loses nothing: re-assigning any partition's batch sizes to the
+    sorted list in order never raises a batch's max length.  So the DP optimum
+    must equal the minimum over ALL set partitions."""
+    rng = np.random.Generator(np.random.PCG64(1000 + seed))
+    n = int(rng.integers(1, 10))
+    max_batch = int(rng.integers(1, n + 1))
+    lens = rng.integers(1, 30, size=n).tolist()
+    cost = _monotone_table(rng, 30, max_batch)
+    plans, total = ttlib.dp_schedule(lens, cost)
+    sp, _ = oracle.schedule_setpartition_bruteforce(lens, cost, max_batch)
+    assert abs(total - sp) <= 1e-9 * max(1.0, sp)
+
+
+def test_setpartition_never_above_contiguous():
+    rng = np.random.Generator(np.random.PCG64(77))
+    for _ in range(20):
+        n = int(rng.integers(1, 8))
+        mb = int(rng.integers(1, n + 1))
+        lens = rng.integers(1, 20, size=n).tolist()
+        cost = _table(20, mb, lambda L, k: float(rng.uniform(0.1, 3.0)))
+        sp, _ = oracle.schedule_setpartition_bruteforce(lens, cost, mb)
+        ct, _ = oracle.schedule_bruteforce(lens, cost, mb)
+        assert sp <= ct + 1e-12

@@ -25,6 +25,7 @@ def main():
     ap.add_argument("--tier", default=None)
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--ragged", action="store_true")
+    ap.add_argument("--c3", action="store_true", help="C3 lengths (64 x U{5..500}); dims = H")
     a = ap.parse_args()
     dt = W.DTYPES[a.dtype]
     if a.tier and a.op != "attention":
@@ -43,8 +44,12 @@ def main():
         for _ in range(a.reps):
             tt.tt_attention_fwd(o, q, k, v, L, 0.125)
     elif a.op == "softmax":
-        B, H, Sq, Sk = a.dims
-        lens = W.lengths_ragged(B, Sk) if a.ragged else W.lengths_full(B, Sk)
+        if a.c3:
+            lens = W.c3_lengths()
+            B, H, Sq, Sk = len(lens), a.dims[0], int(lens.max()), int(lens.max())
+        else:
+            B, H, Sq, Sk = a.dims
+            lens = W.lengths_ragged(B, Sk) if a.ragged else W.lengths_full(B, Sk)
         x = W.scores(B, H, Sq, Sk, dt, device="cuda")
         L = torch.as_tensor(lens).cuda()
         print("tier:", tt.softmax_plan(dt, B, H, Sq, Sk))
