@@ -63,3 +63,55 @@ def masked_bits_zero(y: torch.Tensor, lengths) -> bool:
     ib = torch.int32 if y.dtype == torch.float32 else torch.int16
     bits = y.view(ib)
     return bool((bits[mask] == 0).all().item())
+
+
+# ------------------------------------------------------------ every-row checks
+# Full-size configs (C3, C4, C5 batches) are compared with the fp64 oracle on
+# EVERY row: the oracle runs over row chunks on all host threads (its ctypes
+# calls release the GIL) and each chunk is compared as soon as it is done, so
+# no full-size float64 tensor is ever materialised.
+def _pool():
+    import concurrent.futures as cf
+    import os
+    return cf.ThreadPoolExecutor(max_workers=max(1, min(32, os.cpu_count() or 1)))
+
+
+def softmax_all_rows(x_before: torch.Tensor, y: torch.Tensor, lengths, scale: float,
+                     what: str = "") -> float:
+    """x_before, y: [B, H, Sq, Sk] (CPU input snapshot, GPU or CPU output).
+    Checks every row of every request against oracle.softmax_masked and every
+    padding key for +0.0 bits.  Returns the max abs error."""
+    import numpy as np
+    import oracle
+    B, H, Sq, Sk = x_before.shape
+    lens = np.asarray(lengths, dtype=np.int32)
+    yc = y.detach().to("cpu")
+    dtype = x_before.dtype
+
+    def one(b):
+        ref = oracle.softmax_masked(x_before[b:b + 1], lens[b:b + 1], scale)
+        err = assert_close("softmax", dtype, yc[b:b + 1], ref, f"{what} request {b}")
+        assert masked_bits_zero(yc[b:b + 1], lens[b:b + 1]), f"{what} request {b}"
+        return err
+
+    with _pool() as ex:
+        return max(ex.map(one, range(B)), default=0.0)
+
+
+def layernorm_all_rows(d: dict, y: torch.Tensor, eps: float, what: str = "",
+                       chunk: int = 2048) -> float:
+    """d: CPU inputs (x, residual, bias, gamma, beta); y: [rows, hidden] output.
+    Every row against oracle.add_bias_layernorm.  Returns the max abs error."""
+    import oracle
+    rows = d["x"].shape[0]
+    yc = y.detach().to("cpu")
+    dtype = d["x"].dtype
+
+    def one(lo):
+        hi = min(rows, lo + chunk)
+        ref = oracle.add_bias_layernorm(d["x"][lo:hi], d["residual"][lo:hi], d["bias"],
+                                        d["gamma"], d["beta"], eps)
+        return assert_close("layernorm", dtype, yc[lo:hi], ref, f"{what} rows {lo}..{hi}")
+
+    with _pool() as ex:
+        return max(ex.map(one, range(0, rows, chunk)), default=0.0)

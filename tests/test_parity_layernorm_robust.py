@@ -1,0 +1,115 @@
+"""GPU parity: the LN-2 robustness cases on EVERY compiled LayerNorm tier and
+on the automatic plan at the full-size row counts.
+
+The offset test (x ~ N(0,1) + 64 / + 1000) is the case that separates the
+kernels' shifted two-level moments from the paper's one-pass Eq. 1 RHS
+(SURVEY §8(c) "GPU robustness"; DESIGN R9); aliasing
+(out = x, out = residual, DESIGN R10), gamma = 0 (-> beta exactly) and a large
+eps are run beside it.  Every check names the tier it reached
+(`tt_add_bias_layernorm_plan`) and runs in every storage dtype."""
+import pytest
+import torch
+
+import oracle
+import workloads as W
+from _parity import assert_close, layernorm_all_rows
+
+pytestmark = pytest.mark.gpu
+DT = [torch.float32, torch.float16, torch.bfloat16]
+HIDDEN_CHOICES = (768, 1024, 512, 96, 37, 16, 2048, 4096, 12288, 32768)
+
+
+def _dev(d):
+    return {k: v.cuda() for k, v in d.items()}
+
+
+def _ln(tt, out, dd, eps):
+    tt.tt_add_bias_layernorm(out, dd["x"], dd["residual"], dd["bias"], dd["gamma"], dd["beta"],
+                             eps)
+    torch.cuda.synchronize()
+    return out
+
+
+def _ref(d, eps):
+    return oracle.add_bias_layernorm(d["x"], d["residual"], d["bias"], d["gamma"], d["beta"], eps)
+
+
+def robust_checks(tt, rows, hidden, dtype, tag, full=False):
+    """offset 64 / 1000, out = x, out = residual, gamma = 0, eps = 0.5."""
+    check = (lambda d, y, eps, what: layernorm_all_rows(d, y, eps, what)) if full else \
+        (lambda d, y, eps, what: assert_close("layernorm", dtype, y, _ref(d, eps), what))
+    for off, seed in ((64.0, 64), (1000.0, 65)):
+        d = W.ln_inputs(rows, hidden, dtype, seed=seed + hidden, offset=off)
+        dd = _dev(d)
+        y = _ln(tt, torch.empty_like(dd["x"]), dd, W.EPS_BERT)
+        check(d, y, W.EPS_BERT, f"{tag} offset {off:g}")
+        # the same offset rows, written over x and over residual
+        x = dd["x"].clone()
+        _ln(tt, x, dict(dd, x=x), W.EPS_BERT)
+        check(d, x, W.EPS_BERT, f"{tag} offset {off:g} out=x")
+        r = dd["residual"].clone()
+        _ln(tt, r, dict(dd, residual=r), W.EPS_BERT)
+        check(d, r, W.EPS_BERT, f"{tag} offset {off:g} out=residual")
+    d = W.ln_inputs(rows, hidden, dtype, seed=7 + hidden)
+    d["gamma"] = torch.zeros_like(d["gamma"])
+    y = _ln(tt, torch.empty_like(d["x"], device="cuda"), _dev(d), 1e-5)
+    assert torch.equal(y.cpu(), d["beta"].expand(rows, hidden)), f"{tag} gamma=0"
+    d = W.ln_inputs(rows, hidden, dtype, seed=8 + hidden)
+    y = _ln(tt, torch.empty_like(d["x"], device="cuda"), _dev(d), 0.5)
+    check(d, y, 0.5, f"{tag} eps=0.5")
+
+
+def _tier_shapes(tt, dtype, i, name, rows):
+    """Hidden sizes tier `name` (forced) serves, the first two that fit."""
+    out = []
+    for h in HIDDEN_CHOICES:
+        if tt.layernorm_plan(dtype, rows, h) == name:
+            out.append(h)
+        if len(out) == 2:
+            break
+    return out
+
+
+@pytest.mark.parametrize("dtype", DT)
+def test_robust_cases_on_every_compiled_tier(ttlib, dtype):
+    names = ttlib.tiers("layernorm", dtype)
+    reached = []
+    try:
+        for i, name in enumerate(names):
+            ttlib.force_tier("layernorm", dtype, i)
+            for h in _tier_shapes(ttlib, dtype, i, name, 3000):
+                # enough rows that persistent tiers walk several rows per group
+                rows = 3000 if h <= 2048 else 200
+                assert ttlib.layernorm_plan(dtype, rows, h) == name
+                robust_checks(ttlib, rows, h, dtype, f"{name} hidden {h}")
+                reached.append(name)
+    finally:
+        ttlib.force_tier("layernorm", dtype, -1)
+    assert len(set(reached)) == len(names), sorted(set(names) - set(reached))
+
+
+def _c5_rows():
+    return sorted({64 * int(b.max()) for b in W.c5_stream()})
+
+
+FULL = [(64 * int(W.c3_lengths().max()), 768, torch.float16, "C3"),
+        (64 * int(W.c3_lengths().max()), 768, torch.float32, "C3"),
+        (64 * 512, 1024, torch.bfloat16, "C4"),
+        (_c5_rows()[0], 768, torch.float16, "C5 min batch"),
+        (_c5_rows()[-1], 768, torch.bfloat16, "C5 max batch")]
+
+
+@pytest.mark.parametrize("rows,hidden,dtype,cfg", FULL, ids=[f"{c[3]}-{c[2]}" for c in FULL])
+def test_robust_cases_full_size_automatic_plan(ttlib, rows, hidden, dtype, cfg):
+    plan = ttlib.layernorm_plan(dtype, rows, hidden)
+    robust_checks(ttlib, rows, hidden, dtype, f"{cfg} {rows}x{hidden} [{plan}]", full=True)
+    print(f"{cfg}: {plan}")
+
+
+@pytest.mark.parametrize("rows", [40, 200, 1000, 2000, 6000, 10000])
+@pytest.mark.parametrize("dtype", DT)
+def test_robust_cases_every_row_band(ttlib, rows, dtype):
+    """The automatic plan changes with the row count at hidden 768 (micro /
+    mini / tiny / small / large bands, layernorm.cu kLnPref*): every band."""
+    plan = ttlib.layernorm_plan(dtype, rows, 768)
+    robust_checks(ttlib, rows, 768, dtype, f"{rows}x768 [{plan}]")

@@ -1,16 +1,18 @@
 """GPU parity: tt_softmax_masked_* (CUDA, through the C ABI) vs the fp64 oracle.
 
-Small configs are compared element by element on every row; full-size
-configs (C3, C4, C5 batches) in the launch configuration bench.py times are
-compared on seeded row samples, plus properties checked on every row
-(masked bits exactly 0, valid rows sum to 1, no NaN)."""
+Every config is compared element by element on every row: small ones
+directly, full-size ones (C3, C4, C5 batches, in the launch configuration
+bench.py times) by the threaded oracle request by request
+(`_parity.softmax_all_rows`).  The C2 shapes over 128 keys are compared on
+seeded row samples plus properties checked on every row (masked bits exactly
+0, valid rows sum to 1, no NaN)."""
 import numpy as np
 import pytest
 import torch
 
 import oracle
 import workloads as W
-from _parity import assert_close, masked_bits_zero
+from _parity import assert_close, masked_bits_zero, softmax_all_rows
 
 pytestmark = pytest.mark.gpu
 DT = [torch.float32, torch.float16, torch.bfloat16]
@@ -78,19 +80,30 @@ def test_c2_seq_sweep(ttlib, dtype, S, ragged):
 
 
 # ----------------------------------------------------------------- C3, C4, C5
+def _all_rows_check(tt, x_dev, lens, scale, what):
+    """In-place call on a full-size device tensor; every row vs the oracle."""
+    before = x_dev.cpu()
+    L = torch.as_tensor(np.asarray(lens, dtype=np.int32)).cuda()
+    tt.tt_softmax_masked(x_dev, L, scale)
+    torch.cuda.synchronize()
+    plan = tt.softmax_plan(x_dev.dtype, *x_dev.shape)
+    err = softmax_all_rows(before, x_dev, lens, scale, f"{what} [{plan}]")
+    print(f"{what}: {plan}: every row, max abs err {err:.3e}")
+
+
 @pytest.mark.parametrize("dtype", [torch.float16, torch.float32])
 def test_c3_variable_length_batch(ttlib, dtype):
     lens = W.c3_lengths()
     S = int(lens.max())
     x = W.scores(64, 12, S, S, dtype, device="cuda", seed=W.SEED + 3)
-    _sampled_check(ttlib, x, lens, W.SCALE_BERT, nsample=4096, what="C3")
+    _all_rows_check(ttlib, x, lens, W.SCALE_BERT, "C3")
 
 
 @pytest.mark.parametrize("ragged", [False, True])
 def test_c4_bert_large_full_size(ttlib, ragged):
     lens = W.lengths_ragged(64, 512, seed_offset=4) if ragged else W.lengths_full(64, 512)
     x = W.scores(64, 16, 512, 512, torch.bfloat16, device="cuda", seed=W.SEED + 4)
-    _sampled_check(ttlib, x, lens, W.SCALE_BERT, nsample=4096, what="C4")
+    _all_rows_check(ttlib, x, lens, W.SCALE_BERT, "C4")
 
 
 @pytest.mark.parametrize("dtype", [torch.float16, torch.bfloat16])
@@ -100,7 +113,22 @@ def test_c5_stream_batches(ttlib, dtype):
         lens = batches[bi]
         S = int(lens.max())
         x = W.scores(64, 12, S, S, dtype, device="cuda", seed=W.SEED + 5 + bi)
-        _sampled_check(ttlib, x, lens, W.SCALE_BERT, nsample=1024, seed=bi, what=f"C5 b{bi}")
+        _all_rows_check(ttlib, x, lens, W.SCALE_BERT, f"C5 b{bi}")
+
+
+@pytest.mark.parametrize("Sk", [37, 65, 127, 100])
+def test_fp32_ragged_many_rows_sub_warp_tiers(ttlib, Sk):
+    """fp32 rows of 33..128 keys in calls of more than 2048 rows take the G8
+    NV2 / NV4+prefetch tiers (softmax.cu kSmPref); 256 rows per request so
+    whole CTAs belong to one request (one-request narrow paths), odd pitches
+    (Sk % 4 != 0: head / tail code), poison in the padding."""
+    lens = [Sk, 1, 7, 8, 9, 15, 16, 17, 31, 32, 33, Sk // 2, Sk - 1, 0, Sk, 3]
+    x = W.scores(len(lens), 4, 64, Sk, torch.float32, seed=Sk + 11)
+    plan = ttlib.softmax_plan(torch.float32, len(lens), 4, 64, Sk)
+    assert len(lens) * 4 * 64 > 2048
+    _full_check(ttlib, x, lens, W.SCALE_BERT, f"fp32 many rows Sk={Sk} [{plan}]")
+    xp = W.poison_masked(x, lens)
+    _full_check(ttlib, xp, lens, -0.25, f"fp32 many rows poison Sk={Sk} [{plan}]")
 
 
 # ----------------------------------------------------------------- edge cases
