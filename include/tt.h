@@ -7,8 +7,12 @@
  * LayerNorm calculates the mean and variance".  Its two fused reduction
  * kernels, named `ApplyMaskAndSoftmax` and `AddBiasLayerNorm` (l.765), are
  * the non-GEMM hot spots of a BERT layer (Table 2, l.324-337).  This library
- * exports exactly those two operations, in fp32, fp16 and bf16 storage with
- * fp32 arithmetic.
+ * exports those two operations (plus host-buffer "staged" forms and plan
+ * queries), in fp32, fp16 and bf16 storage with fp32 arithmetic.  Beyond the
+ * hot path it also exports the SURVEY §8(f) NEXT rows: the packed
+ * (padding-free) softmax, the element-wise kernels between GEMMs (bias+GELU,
+ * QKV split, head merge), the tcgen05 fused attention, and -- in tt_sched.h
+ * -- the DP batch scheduler (Alg. 2).
  *
  * Conventions common to every entry point
  * ---------------------------------------
@@ -116,7 +120,7 @@ TT_API tt_status tt_softmax_masked_bf16(void* scores, const int32_t* lengths, in
  * max_seqlen  HOST upper bound of every L_r (selects the tier); a request
  *             longer than max_seqlen is undefined (memory-safe, values wrong).
  * Errors as above; max_seqlen > 1024 (fp32) / 2048 (fp16, bf16) or
- * H * total_tokens >= 2^32 gives TT_ERROR_NOT_SUPPORTED.
+ * H * total_tokens >= 2^32 - 1 gives TT_ERROR_NOT_SUPPORTED.
  * ---------------------------------------------------------------------- */
 TT_API tt_status tt_softmax_packed_f32(float* scores, const int32_t* cu_seqlens,
                                        const int64_t* cu_blocks, int64_t num_req, int64_t H,
@@ -175,7 +179,7 @@ TT_API tt_status tt_add_bias_layernorm_bf16(void* out, const void* x, const void
  *   Outputs must not overlap the inputs or each other.
  * tt_merge_heads:  in [B, H, S, D] -> out [B*S, H*D]: out[b*S+s, h*D+d] = in[b,h,s,d].
  *   out must not overlap in.
- * Index spaces must fit 32 bits (B*S*3*H*D < 2^32), else TT_ERROR_NOT_SUPPORTED.
+ * Index spaces must fit 32 bits (B*S*3*H*D < 2^32 - 1), else TT_ERROR_NOT_SUPPORTED.
  * ---------------------------------------------------------------------- */
 TT_API tt_status tt_add_bias_gelu(int dtype, void* out, const void* x, const void* bias,
                                   int64_t rows, int64_t n, int approximate, cudaStream_t stream);

@@ -134,6 +134,45 @@ def _dev(t: torch.Tensor, name: str):
         raise ValueError(f"{name} must be contiguous")
 
 
+def _host(t: torch.Tensor, name: str):
+    if t.is_cuda:
+        raise ValueError(f"{name} must be a host tensor")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+
+
+def _pair(h: torch.Tensor, d: torch.Tensor, name: str):
+    """host/device counterparts: same shape and dtype (the copies move
+    numel * element_size bytes between them)."""
+    _host(h, f"host_{name}")
+    _dev(d, f"dev_{name}")
+    if h.shape != d.shape or h.dtype != d.dtype:
+        raise ValueError(f"host_{name} / dev_{name} differ in shape or dtype")
+
+
+def _staged_softmax_args(host_scores, host_lengths, dev_scores, dev_lengths):
+    _pair(host_scores, dev_scores, "scores")
+    _pair(host_lengths, dev_lengths, "lengths")
+    if dev_scores.dim() != 4:
+        raise ValueError("scores must be [B, H, Sq, Sk]")
+    if dev_lengths.dtype != torch.int32 or dev_lengths.numel() != dev_scores.shape[0]:
+        raise ValueError("lengths must be int32[B]")
+
+
+def _staged_ln_args(host_out, host_x, host_residual, dev_out, dev_x, dev_residual, bias, gamma,
+                    beta):
+    for h, d, n in ((host_out, dev_out, "out"), (host_x, dev_x, "x"),
+                    (host_residual, dev_residual, "residual")):
+        _pair(h, d, n)
+        if d.shape != dev_x.shape or d.dtype != dev_x.dtype:
+            raise ValueError("out, x, residual must share one shape and dtype")
+    hidden = dev_x.shape[-1] if dev_x.dim() else 0
+    for t, n in ((bias, "bias"), (gamma, "gamma"), (beta, "beta")):
+        _dev(t, n)
+        if t.dtype != dev_x.dtype or t.numel() != hidden:
+            raise ValueError(f"{n} must have `hidden` elements of the operands' dtype")
+
+
 # --------------------------------------------------------------------- softmax
 def tt_softmax_masked(scores: torch.Tensor, lengths: torch.Tensor, scale: float, stream=None):
     """In place: scores[b,h,i,:] <- masked softmax (tt_softmax_masked_{f32,f16,bf16})."""
@@ -161,12 +200,7 @@ def tt_softmax_masked_staged(host_scores: torch.Tensor, host_lengths: torch.Tens
                              dev_scores: torch.Tensor, dev_lengths: torch.Tensor, scale: float,
                              stream=None):
     """H2D copy, kernel, D2H copy on one stream (host buffers pinned)."""
-    _dev(dev_scores, "dev_scores")
-    _dev(dev_lengths, "dev_lengths")
-    if host_scores.is_cuda or host_lengths.is_cuda:
-        raise ValueError("host_* must be host tensors")
-    if host_scores.shape != dev_scores.shape or host_scores.dtype != dev_scores.dtype:
-        raise ValueError("host/device scores mismatch")
+    _staged_softmax_args(host_scores, host_lengths, dev_scores, dev_lengths)
     B, H, Sq, Sk = dev_scores.shape
     _check(lib().tt_softmax_masked_staged(DTYPE_CODE[dev_scores.dtype], host_scores.data_ptr(),
                                           host_lengths.data_ptr(), dev_scores.data_ptr(),
@@ -180,12 +214,7 @@ def tt_softmax_masked_staged_overlap(host_scores: torch.Tensor, host_lengths: to
                                      scale: float, chunks: int, stream=None, copy_stream=None):
     """As tt_softmax_masked_staged, cut into `chunks` pieces whose D2H copies run
     on `copy_stream` under the next piece's H2D copy (include/tt.h)."""
-    _dev(dev_scores, "dev_scores")
-    _dev(dev_lengths, "dev_lengths")
-    if host_scores.is_cuda or host_lengths.is_cuda:
-        raise ValueError("host_* must be host tensors")
-    if host_scores.shape != dev_scores.shape or host_scores.dtype != dev_scores.dtype:
-        raise ValueError("host/device scores mismatch")
+    _staged_softmax_args(host_scores, host_lengths, dev_scores, dev_lengths)
     B, H, Sq, Sk = dev_scores.shape
     _check(lib().tt_softmax_masked_staged_overlap(
         DTYPE_CODE[dev_scores.dtype], host_scores.data_ptr(), host_lengths.data_ptr(),
@@ -273,9 +302,8 @@ def tt_add_bias_layernorm_raw(dtype: torch.dtype, out: int, x: int, residual: in
 
 def tt_add_bias_layernorm_staged(host_out, host_x, host_residual, dev_out, dev_x, dev_residual,
                                  bias, gamma, beta, eps: float, stream=None):
-    for t, n in ((dev_out, "dev_out"), (dev_x, "dev_x"), (dev_residual, "dev_residual"),
-                 (bias, "bias"), (gamma, "gamma"), (beta, "beta")):
-        _dev(t, n)
+    _staged_ln_args(host_out, host_x, host_residual, dev_out, dev_x, dev_residual, bias, gamma,
+                    beta)
     hidden = dev_x.shape[-1]
     rows = dev_x.numel() // hidden if hidden else 0
     _check(lib().tt_add_bias_layernorm_staged(
@@ -291,9 +319,8 @@ def tt_add_bias_layernorm_staged_overlap(host_out, host_x, host_residual, dev_ou
                                          stream=None, copy_stream=None):
     """As tt_add_bias_layernorm_staged, cut into `chunks` row ranges whose D2H
     copies run on `copy_stream` (include/tt.h)."""
-    for t, n in ((dev_out, "dev_out"), (dev_x, "dev_x"), (dev_residual, "dev_residual"),
-                 (bias, "bias"), (gamma, "gamma"), (beta, "beta")):
-        _dev(t, n)
+    _staged_ln_args(host_out, host_x, host_residual, dev_out, dev_x, dev_residual, bias, gamma,
+                    beta)
     hidden = dev_x.shape[-1]
     rows = dev_x.numel() // hidden if hidden else 0
     _check(lib().tt_add_bias_layernorm_staged_overlap(

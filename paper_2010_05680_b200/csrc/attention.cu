@@ -1023,16 +1023,6 @@ cudaError_t launch_attn(void* out, const void* q, const void* k, const void* v,
                         const int32_t* lengths, int64_t B, int64_t H, int64_t S, float scale,
                         cudaStream_t st) {
     constexpr size_t smem = attn_smem<NBUF, BN>();
-    static std::atomic<int> attr{0};
-    if (!attr.load()) {
-        for (auto kern : {attention_tc_kernel<T, NBUF, BN, true, LATE>,
-                          attention_tc_kernel<T, NBUF, BN, false, LATE>}) {
-            cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 (int)smem);
-            if (e != cudaSuccess) return e;
-        }
-        attr.store(1);
-    }
     dim3 grid((unsigned)((S + kBM - 1) / kBM), (unsigned)H, (unsigned)B);
     // c = scale * log2(e); scale 0 -> a tiny positive c (uniform weights, as the
     // softmax kernels do), so the masked-key sentinel still maps to p = +0
@@ -1054,15 +1044,6 @@ template <typename T>
 cudaError_t launch_attn_ws(void* out, const void* q, const void* k, const void* v,
                            const int32_t* lengths, int64_t B, int64_t H, int64_t S, float scale,
                            cudaStream_t st) {
-    static std::atomic<int> attr{0};
-    if (!attr.load()) {
-        for (auto kern : {attention_ws_kernel<T, true>, attention_ws_kernel<T, false>}) {
-            cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 (int)kWsSmem);
-            if (e != cudaSuccess) return e;
-        }
-        attr.store(1);
-    }
     dim3 grid((unsigned)((S + kBM - 1) / kBM), (unsigned)H, (unsigned)B);
     float c = scale * 1.4426950408889634f;
     if (c == 0.f) c = 1e-30f;
@@ -1078,16 +1059,6 @@ template <typename T, int MINB>
 cudaError_t launch_attn_split(void* out, const void* q, const void* k, const void* v,
                               const int32_t* lengths, int64_t B, int64_t H, int64_t S, float scale,
                               cudaStream_t st) {
-    static std::atomic<int> attr{0};
-    if (!attr.load()) {
-        for (auto kern : {attention_split_kernel<T, true, MINB>,
-                          attention_split_kernel<T, false, MINB>}) {
-            cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 (int)kSpSmem);
-            if (e != cudaSuccess) return e;
-        }
-        attr.store(1);
-    }
     dim3 grid((unsigned)((S + kBM - 1) / kBM), (unsigned)H, (unsigned)B);
     float c = scale * 1.4426950408889634f;
     if (c == 0.f) c = 1e-30f;

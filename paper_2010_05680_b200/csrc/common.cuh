@@ -47,6 +47,11 @@ struct PdlScope {
 
 bool pdl_enabled();  // tt_api.cu: process-wide switch (ttx_set_pdl), default on
 
+// Opt `kern` into `smem` bytes of dynamic shared memory (> 48 KB) on the
+// CURRENT device.  The attribute belongs to each device's context, so the
+// cache in tt_api.cu is keyed by (kernel, device); a no-op at <= 48 KB.
+cudaError_t smem_optin(const void* kern, size_t smem);
+
 // kern<<<grid, block, smem, st>>>(args...) with the programmatic-stream-
 // serialization attribute when PDL is enabled.
 template <typename... P, typename... A>
@@ -62,6 +67,10 @@ inline cudaError_t launch_k(void (*kern)(P...), dim3 grid, dim3 block, size_t sm
     at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    if (smem > 48 * 1024) {
+        const cudaError_t e = smem_optin(reinterpret_cast<const void*>(kern), smem);
+        if (e != cudaSuccess) return e;
+    }
     return cudaLaunchKernelEx(&cfg, kern, std::forward<A>(args)...);
 }
 

@@ -46,6 +46,7 @@ cudaError_t attention_launch(int dtype, void* out, const void* q, const void* k,
                              const int32_t* lengths, int64_t B, int64_t H, int64_t S,
                              float scale, cudaStream_t stream);
 bool attention_force_variant(int v);  // 0 auto, 1 single-buffered, 2 double-buffered
+cudaError_t smem_optin(const void* kern, size_t smem);  // per-device dynamic-smem opt-in
 
 // Tuning / test hooks (include/tt_tune.h): enumerate every compiled tier and
 // force one (-1 = automatic selection).  A forced tier that cannot serve the

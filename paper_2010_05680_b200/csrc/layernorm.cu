@@ -603,15 +603,10 @@ cudaError_t launch_ln_tma(void* out, const void* x, const void* res, const void*
     const size_t smem =
         prm_bytes + (size_t)((NW * D * 8 + 127) & ~127) + (size_t)NW * D * slot_bytes;
     if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
-    static std::atomic<int> attr_done{0};
-    if (smem > 48 * 1024 && attr_done.load() < (int)smem) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)smem);
-        if (e != cudaSuccess) return e;
-        attr_done.store((int)smem);
-    }
+    cudaError_t e = smem_optin(reinterpret_cast<const void*>(kern), smem);
+    if (e != cudaSuccess) return e;
     int occ = 0;
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NW * 32, smem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NW * 32, smem);
     if (e != cudaSuccess) return e;
     occ = max(occ, 1);
     const int64_t need = (rows + NW - 1) / NW;
@@ -661,15 +656,10 @@ cudaError_t launch_ln_warp(void* out, const void* x, const void* res, const void
     auto kern = PF ? ln_pf_kernel<T, VB, G, NV, NT, MINB, true>
                    : ln_warp_kernel<T, VB, G, NV, NT, MINB>;
     const size_t smem = (size_t)3 * hidden * sizeof(float);
-    static std::atomic<int> attr_done{0};
-    if (smem > 48 * 1024 && attr_done.load() < (int)smem) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)smem);
-        if (e != cudaSuccess) return e;
-        attr_done.store((int)smem);
-    }
+    cudaError_t e = smem_optin(reinterpret_cast<const void*>(kern), smem);
+    if (e != cudaSuccess) return e;
     int occ = 0;
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT, smem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT, smem);
     if (e != cudaSuccess) return e;
     occ = occ > 0 ? occ : 1;
     const int64_t need = (rows + GPB - 1) / GPB;

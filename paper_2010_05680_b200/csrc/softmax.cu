@@ -530,15 +530,10 @@ cudaError_t launch_softmax_tma(void* scores, const int32_t* lengths, int64_t nro
     const int slot_bytes = ((Sk * (int)sizeof(T) + 32) + 127) & ~127;
     const int D = tma_depth(slot_bytes);
     const size_t smem = (size_t)((NW * D * 8 + 127) & ~127) + (size_t)NW * D * slot_bytes;
-    static std::atomic<int> attr_done{0};
-    if (smem > 48 * 1024 && attr_done.load() < (int)smem) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)smem);
-        if (e != cudaSuccess) return e;
-        attr_done.store((int)smem);
-    }
+    cudaError_t e = smem_optin(reinterpret_cast<const void*>(kern), smem);
+    if (e != cudaSuccess) return e;
     int occ = 0;
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NW * 32, smem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NW * 32, smem);
     if (e != cudaSuccess) return e;
     occ = max(occ, 1);
     const int64_t need = (nrows + NW - 1) / NW;

@@ -1,4 +1,7 @@
 #include <atomic>
+#include <map>
+#include <mutex>
+#include <utility>
 // tt_api.cu -- the C ABI of libtt.so (contract: include/tt.h).
 //
 // Host-side validation happens before any CUDA call; the kernels themselves
@@ -284,6 +287,24 @@ void copy_name(const char* name, char* buf, int cap) {
 namespace tt {
 std::atomic<int> g_pdl{1};
 bool pdl_enabled() { return g_pdl.load(std::memory_order_relaxed) != 0; }
+
+// (kernel, device) -> dynamic shared memory bytes already opted in.  The
+// attribute is per device context: a process driving several GPUs must set it
+// on each.  Only launches above 48 KB come here.
+cudaError_t smem_optin(const void* kern, size_t smem) {
+    if (smem <= 48 * 1024) return cudaSuccess;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    static std::mutex mu;
+    static std::map<std::pair<const void*, int>, size_t> done;
+    std::lock_guard<std::mutex> lk(mu);
+    size_t& have = done[{kern, dev}];
+    if (have >= smem) return cudaSuccess;
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess) have = smem;
+    return e;
+}
 }  // namespace tt
 
 extern "C" {
@@ -390,6 +411,10 @@ tt_status tt_add_bias_layernorm_staged(int dtype, void* host_out, const void* ho
                               eps, true, &empty);
     if (s != TT_SUCCESS || empty) return s;
     if (!host_out || !host_x || !host_residual) return TT_ERROR_INVALID_VALUE;
+    // both are H2D copy targets: overlapping, the residual copy would overwrite x
+    if (overlaps(dev_x, rows * hidden * elem_bytes(dtype), dev_residual,
+                 rows * hidden * elem_bytes(dtype)))
+        return TT_ERROR_INVALID_VALUE;
     const size_t bytes = (size_t)(rows * hidden * elem_bytes(dtype));
     cudaError_t e = cudaMemcpyAsync(dev_x, host_x, bytes, cudaMemcpyHostToDevice, stream);
     if (e == cudaSuccess)
@@ -491,6 +516,10 @@ tt_status tt_add_bias_layernorm_staged_overlap(int dtype, void* host_out, const 
                               eps, true, &empty);
     if (s != TT_SUCCESS || empty) return s;
     if (!host_out || !host_x || !host_residual) return TT_ERROR_INVALID_VALUE;
+    // both are H2D copy targets: overlapping, the residual copy would overwrite x
+    if (overlaps(dev_x, rows * hidden * elem_bytes(dtype), dev_residual,
+                 rows * hidden * elem_bytes(dtype)))
+        return TT_ERROR_INVALID_VALUE;
     const int64_t row_bytes = hidden * elem_bytes(dtype);
     const int64_t per = chunk_units(rows, chunks, row_bytes);
     EventGuard g;

@@ -201,6 +201,12 @@ def test_staged_overlap_validation(ttlib):
     assert fl(2, FAKE, FAKE, FAKE, FAKE, FAKE, FAKE, FAKE, FAKE, FAKE, 4, 64, -1.0, 4, 0,
               FAKE) == INV                                                      # eps < 0
     assert fl(2, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 64, 1e-5, 4, 0, FAKE) == OK      # empty
+    # dev_x and dev_residual are both H2D targets: overlap is rejected
+    F2 = FAKE + (1 << 24)
+    for f, extra in ((fl, (4, 0, FAKE)), (L.tt_add_bias_layernorm_staged, (0,))):
+        args = (2, FAKE, FAKE, FAKE, F2, FAKE, FAKE + 64, F2 + (1 << 20), F2 + (1 << 21),
+                F2 + (1 << 22), 4, 64, 1e-5)
+        assert f(*args, *extra) == INV
 
 
 def test_softmax_preference_row_threshold(ttlib):

@@ -157,3 +157,28 @@ def test_every_compiled_tier(ttlib, dtype):
                 _check(ttlib, 37, hidden, dtype, eps=1e-5, seed=hidden + i, what=name)
     finally:
         ttlib.force_tier("layernorm", dtype, -1)
+
+
+def test_staged_wrappers_reject_mismatched_host_buffers(ttlib):
+    """The staged bindings validate host buffers like the device-only ones
+    (ADVICE r01): a short or wrongly typed host buffer would make the D2H copy
+    overrun it."""
+    d = W.ln_inputs(40, 768, torch.float16, seed=8)
+    dx, dr, do = (torch.empty_like(d["x"], device="cuda") for _ in range(3))
+    p = {k: d[k].cuda() for k in ("bias", "gamma", "beta")}
+    good = d["x"].clone()
+    for bad in (d["x"][:20].clone(), d["x"].float(), d["x"].cuda(), d["x"].t()):
+        with pytest.raises(ValueError):
+            ttlib.tt_add_bias_layernorm_staged(bad, good, good, do, dx, dr, p["bias"],
+                                               p["gamma"], p["beta"], W.EPS_BERT)
+    with pytest.raises(ttlib.TTError):   # dev_x and dev_residual alias
+        ttlib.tt_add_bias_layernorm_staged(good.clone(), good, good, do, dx, dx, p["bias"],
+                                           p["gamma"], p["beta"], W.EPS_BERT)
+    x = W.scores(2, 2, 8, 8, torch.float16, seed=1)
+    dxs = x.cuda()
+    for hl, dl in ((torch.tensor([8, 3], dtype=torch.int64), torch.zeros(2, dtype=torch.int64,
+                                                                         device="cuda")),
+                   (torch.tensor([8], dtype=torch.int32), torch.zeros(1, dtype=torch.int32,
+                                                                      device="cuda"))):
+        with pytest.raises(ValueError):
+            ttlib.tt_softmax_masked_staged(x.clone(), hl, dxs, dl, 0.125)
