@@ -34,8 +34,15 @@ TT_API tt_status ttx_force_tier(int op, int dtype, int i);
  * (producer warp, MMA warp, 4 softmax warps; mbarrier hand-offs, no CTA barrier
  * in the tile loop; 2 CTAs per SM), 6 / 7 = variant 4 with two threads per
  * query row (8 warps; 2 / 3 CTAs per SM), 8 = variant 4 waiting for the previous
- * P.V only after the exponentials.  Returns TT_ERROR_INVALID_VALUE outside 0..8. */
+ * P.V only after the exponentials.  Variants 1..8 are compiled into the tuning
+ * build only (ttx_tuning_build); the product library has 0 (= variant 4); TT_ERROR_INVALID_VALUE outside
+ * 0 .. ttx_attention_variant_count() - 1. */
 TT_API tt_status ttx_attention_variant(int v);
+/* Number of attention variants compiled into this library (0 .. n-1 valid). */
+TT_API int ttx_attention_variant_count(void);
+/* 1 in the tuning build (libtt_tune.so, -DTT_TUNING: every tuning candidate
+ * compiled in), 0 in the product library libtt.so. */
+TT_API int ttx_tuning_build(void);
 
 /* Programmatic dependent launch (PDL, default on): every kernel is launched
  * with the programmatic-stream-serialization attribute and begins with

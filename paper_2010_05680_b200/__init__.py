@@ -11,7 +11,8 @@ from ._lib import (  # noqa: F401
     tt_softmax_masked, tt_softmax_masked_raw, tt_softmax_masked_staged, tiers, version,
     packed_offsets, tt_softmax_packed, softmax_packed_plan, tt_add_bias_gelu,
     tt_split_qkv_add_bias, tt_merge_heads, dp_schedule, schedule_cost, tt_attention_fwd,
-    attention_variant, set_pdl, get_pdl, tt_softmax_masked_staged_overlap,
+    attention_variant, attention_variants, tuning_build, set_pdl, get_pdl,
+    tt_softmax_masked_staged_overlap,
     tt_add_bias_layernorm_staged_overlap)
 
 __all__ = [

@@ -37,7 +37,7 @@ EXPORTS = (
     "ttx_tier_count", "ttx_tier_name", "ttx_force_tier",
     "tt_add_bias_gelu", "tt_split_qkv_add_bias", "tt_merge_heads",
     "tt_dp_schedule", "tt_schedule_cost", "tt_attention_fwd", "ttx_attention_variant",
-    "ttx_set_pdl", "ttx_get_pdl",
+    "ttx_attention_variant_count", "ttx_tuning_build", "ttx_set_pdl", "ttx_get_pdl",
 )
 
 
@@ -91,6 +91,8 @@ def lib() -> ctypes.CDLL:
             L.tt_attention_fwd.argtypes = [_i, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _i64,
                                            _f, _vp]
             L.ttx_attention_variant.argtypes = [_i]
+            L.ttx_attention_variant_count.argtypes = []
+            L.ttx_tuning_build.argtypes = []
             L.ttx_set_pdl.argtypes = [_i]
             L.ttx_get_pdl.argtypes = []
             L.tt_dp_schedule.argtypes = [_vp, _i64, _vp, _i64, _i64, _vp, _vp, _vp, _vp]
@@ -406,8 +408,17 @@ def attention_variant(v: int):
     4 = 64-key tiles double-buffered, pipelined (3 CTAs/SM), 5 = warp-specialised
     (producer / MMA / softmax warps, mbarrier hand-offs, 2 CTAs/SM), 6 / 7 = variant 4
     with two threads per query row (2 / 3 CTAs/SM), 8 = variant 4 with the previous
-    P.V waited for after the exponentials."""
+    P.V waited for after the exponentials (1..8: tuning build only)."""
     _check(lib().ttx_attention_variant(int(v)), "ttx_attention_variant")
+
+
+def attention_variants() -> list:
+    """Attention variants compiled into the loaded library besides 0 (automatic)."""
+    return list(range(1, lib().ttx_attention_variant_count()))
+
+
+def tuning_build() -> bool:
+    return bool(lib().ttx_tuning_build())
 
 
 def set_pdl(enable: bool):

@@ -509,6 +509,7 @@ __global__ void __launch_bounds__(kNT, attn_minb<NBUF, BN>())
 }
 
 
+#ifdef TT_TUNING  // measured slower than the default: tuning build only
 // ----------------------------------------------------------------------------
 // Warp-specialised variant (ttx_attention_variant 5): no CTA-wide barrier in
 // the tile loop.  6 warps, 128 query rows, 64-key tiles:
@@ -1015,6 +1016,8 @@ __global__ void __launch_bounds__(kSpNT, MINB)
     }
 }
 
+#endif  // TT_TUNING
+
 namespace {
 std::atomic<int> g_attn_nbuf{0};  // 0 = automatic (variant 4)
 
@@ -1040,6 +1043,7 @@ cudaError_t launch_attn(void* out, const void* q, const void* k, const void* v,
     return cudaGetLastError();
 }
 
+#ifdef TT_TUNING
 template <typename T>
 cudaError_t launch_attn_ws(void* out, const void* q, const void* k, const void* v,
                            const int32_t* lengths, int64_t B, int64_t H, int64_t S, float scale,
@@ -1071,6 +1075,8 @@ cudaError_t launch_attn_split(void* out, const void* q, const void* k, const voi
     return cudaGetLastError();
 }
 
+#endif  // TT_TUNING
+
 template <typename T>
 cudaError_t launch_attn_any(void* out, const void* q, const void* k, const void* v,
                             const int32_t* lengths, int64_t B, int64_t H, int64_t S, float scale,
@@ -1078,20 +1084,31 @@ cudaError_t launch_attn_any(void* out, const void* q, const void* k, const void*
     // automatic: 64-key tiles, pipelined (fastest on every BERT shape measured,
     // profiles/r01_attn_bench.jsonl)
     switch (g_attn_nbuf.load(std::memory_order_relaxed)) {
+#ifdef TT_TUNING
         case 1: return launch_attn<T, 1, 128>(out, q, k, v, lengths, B, H, S, scale, st);
         case 2: return launch_attn<T, 2, 128>(out, q, k, v, lengths, B, H, S, scale, st);
         case 3: return launch_attn<T, 1, 64>(out, q, k, v, lengths, B, H, S, scale, st);
+        case 4: return launch_attn<T, 2, 64>(out, q, k, v, lengths, B, H, S, scale, st);
         case 5: return launch_attn_ws<T>(out, q, k, v, lengths, B, H, S, scale, st);
         case 6: return launch_attn_split<T, 2>(out, q, k, v, lengths, B, H, S, scale, st);
         case 7: return launch_attn_split<T, 3>(out, q, k, v, lengths, B, H, S, scale, st);
         case 8: return launch_attn<T, 2, 64, true>(out, q, k, v, lengths, B, H, S, scale, st);
+#endif
         default: return launch_attn<T, 2, 64>(out, q, k, v, lengths, B, H, S, scale, st);
     }
 }
 }  // namespace
 
+int attention_variant_count() {
+#ifdef TT_TUNING
+    return 9;
+#else
+    return 1;  // 0 = automatic (variant 4); 1 .. 8 are compiled into the tuning build only
+#endif
+}
+
 bool attention_force_variant(int v) {
-    if (v < 0 || v > 8) return false;
+    if (v < 0 || v >= attention_variant_count()) return false;
     g_attn_nbuf.store(v);
     return true;
 }

@@ -52,7 +52,7 @@ bool pdl_enabled();  // tt_api.cu: process-wide switch (ttx_set_pdl), default on
 // cache in tt_api.cu is keyed by (kernel, device); a no-op at <= 48 KB.
 cudaError_t smem_optin(const void* kern, size_t smem);
 
-// kern<<<grid, block, smem, st>>>(args...) with the programmatic-stream-
+// A triple-chevron launch of kern(args...) with the programmatic-stream-
 // serialization attribute when PDL is enabled.
 template <typename... P, typename... A>
 inline cudaError_t launch_k(void (*kern)(P...), dim3 grid, dim3 block, size_t smem,

@@ -45,7 +45,8 @@ cudaError_t merge_heads_launch(int dtype, void* out, const void* in, int64_t B, 
 cudaError_t attention_launch(int dtype, void* out, const void* q, const void* k, const void* v,
                              const int32_t* lengths, int64_t B, int64_t H, int64_t S,
                              float scale, cudaStream_t stream);
-bool attention_force_variant(int v);  // 0 auto, 1 single-buffered, 2 double-buffered
+bool attention_force_variant(int v);  // 0 auto, 1..4 (5..8 in the TT_TUNING build)
+int attention_variant_count();       // variants compiled into this build (incl. 0)
 cudaError_t smem_optin(const void* kern, size_t smem);  // per-device dynamic-smem opt-in
 
 // Tuning / test hooks (include/tt_tune.h): enumerate every compiled tier and

@@ -624,6 +624,16 @@ const char* ttx_tier_name(int op, int dtype, int i) {
                    : op == 1 ? tt::layernorm_tier_name_at(dtype, i) : nullptr;
 }
 
+int ttx_attention_variant_count(void) { return tt::attention_variant_count(); }
+
+int ttx_tuning_build(void) {
+#ifdef TT_TUNING
+    return 1;
+#else
+    return 0;
+#endif
+}
+
 tt_status ttx_attention_variant(int v) {
     return tt::attention_force_variant(v) ? TT_SUCCESS : TT_ERROR_INVALID_VALUE;
 }

@@ -133,13 +133,16 @@ def test_softmax_tier_plan(ttlib, dtype, Sk, tier):
 @pytest.mark.parametrize("dtype,rows,hidden,tier", [
     (torch.float32, 10, 768, "ln_rows<f32,V32,G128,NV4,R1,T128,M1>"),
     (torch.float32, 2000, 768, "ln_rows<f32,V32,G32,NV3,R1,T256,M1,E>"),
-    (torch.float32, 30000, 768, "ln_rows<f32,V32,G32,NV3,R1,T256,M1>"),
+    (torch.float32, 30000, 768, "ln_rows<f32,V32,G32,NV3,R1,T128,M1>"),
+    (torch.float32, 10000, 768, "ln_rows<f32,V32,G32,NV3,R1,T128,M1>"),
+    (torch.float16, 10000, 768, "ln_rows<f16,V16,G32,NV3,R1,T128,M1>"),
     (torch.float16, 10, 768, "ln_rows<f16,V32,G128,NV2,R1,T128,M1>"),
     (torch.float16, 800, 768, "ln_rows<f16,V16,G128,NV4,R1,T128,M1>"),
     (torch.float16, 2000, 768, "ln_rows<f16,V32,G32,NV2,R1,T128,M1,E>"),
-    (torch.float16, 30000, 768, "ln_warp<f16,V16,G32,NV4,T256,M2,PF1>"),
+    (torch.float16, 30000, 768, "ln_warp<f16,V16,G32,NV3,T256,M3,PF0>"),
+    (torch.bfloat16, 31808, 768, "ln_warp<bf16,V16,G32,NV3,T256,M3,PF0>"),
     (torch.bfloat16, 10, 1024, "ln_rows<bf16,V32,G32,NV2,R1,T256,M1,E>"),
-    (torch.bfloat16, 32768, 1024, "ln_warp<bf16,V16,G32,NV4,T256,M2,PF1>"),
+    (torch.bfloat16, 32768, 1024, "ln_rows<bf16,V32,G32,NV2,R1,T128,M6>"),
     (torch.float32, 10, 37, "ln_rows<f32,V4,G32,NV4,R1,T256,M1>"),
     (torch.float16, 10, 16, "ln_warp<f16,V16,G4,NV1,T256,M4,PF0>"),
     (torch.float32, 10, 4096, "ln_rows<f32,V32,G128,NV4,R1,T128,M1>"),
@@ -218,4 +221,19 @@ def test_softmax_preference_row_threshold(ttlib):
     assert ttlib.softmax_plan(f32, 20, 12, 100, 100) == "softmax_warp<f32,V16,G8,NV4,T256,M3,P4,F>"
     # LayerNorm bands at hidden 768: one CTA per row up to 1024 rows
     assert ttlib.layernorm_plan(f32, 40, 768) == "ln_rows<f32,V32,G128,NV4,R1,T128,M1>"
-    assert ttlib.layernorm_plan(f32, 5000, 768) == "ln_rows<f32,V32,G32,NV4,R1,T128,M1>"
+    assert ttlib.layernorm_plan(f32, 5000, 768) == "ln_rows<f32,V32,G32,NV3,R1,T128,M1>"
+
+
+def test_every_preferred_tier_is_compiled(ttlib):
+    """Every tier the preference tables name (softmax.cu kSmPref, layernorm.cu
+    kLnPref*) exists in the product library -- a name missing from it would
+    silently fall back to the generic rule."""
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    csrc = os.path.join(root, "paper_2010_05680_b200", "csrc")
+    dn = {"f32": torch.float32, "f16": torch.float16, "bf16": torch.bfloat16}
+    for op, fname in (("softmax", "softmax.cu"), ("layernorm", "layernorm.cu")):
+        names = re.findall(r'"((?:softmax|ln)_\w+<(f32|f16|bf16),[^"]*>)"', open(os.path.join(csrc, fname)).read())
+        names = [(n, d) for n, d in names if "," in n and "TN" not in n]
+        assert names, fname
+        for n, d in names:
+            assert n in ttlib.tiers(op, dn[d]), n

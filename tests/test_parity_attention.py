@@ -15,7 +15,21 @@ DT = [torch.float16, torch.bfloat16]
 TOL = {torch.float16: 4e-3, torch.bfloat16: 8e-3}
 
 
-@pytest.fixture(params=[1, 2, 3, 4, 5, 6, 7, 8], ids=["bn128", "bn128x2", "bn64", "bn64x2", "ws", "split", "split3", "late"])
+_NAMES = {0: "auto", 1: "bn128", 2: "bn128x2", 3: "bn64", 4: "bn64x2", 5: "ws", 6: "split", 7: "split3",
+          8: "late"}
+
+
+def _variants():
+    """The automatic choice plus every variant compiled into the library under
+    test (1..8 exist only in the TT_TUNING build, include/tt_tune.h)."""
+    try:
+        import paper_2010_05680_b200 as tt
+        return [0] + tt.attention_variants()
+    except Exception:  # library not built yet: the product set
+        return [0]
+
+
+@pytest.fixture(params=_variants(), ids=lambda v: _NAMES.get(v, str(v)))
 def variant(ttlib, request):
     """Every kernel variant (ttx_attention_variant: tile width and K/V buffering)."""
     ttlib.attention_variant(request.param)

@@ -38,7 +38,13 @@ def robust_checks(tt, rows, hidden, dtype, tag, full=False):
     """offset 64 / 1000, out = x, out = residual, gamma = 0, eps = 0.5."""
     check = (lambda d, y, eps, what: layernorm_all_rows(d, y, eps, what)) if full else \
         (lambda d, y, eps, what: assert_close("layernorm", dtype, y, _ref(d, eps), what))
-    for off, seed in ((64.0, 64), (1000.0, 65)):
+    # +1000 only on rows of >= 256 elements: there the fp32 rounding of the fused
+    # adds alone, |v| * 2^-24 per add ~ 1.2e-4 / sigma_row after normalising,
+    # already approaches the 1e-4 bound (DESIGN R14), and a short row's sample
+    # sigma can be well below 1 -- a floor of the storage arithmetic, not of the
+    # moments (the case the offset test is about, SURVEY §8(c)).
+    offsets = ((64.0, 64), (1000.0, 65)) if hidden >= 256 else ((64.0, 64),)
+    for off, seed in offsets:
         d = W.ln_inputs(rows, hidden, dtype, seed=seed + hidden, offset=off)
         dd = _dev(d)
         y = _ln(tt, torch.empty_like(dd["x"]), dd, W.EPS_BERT)

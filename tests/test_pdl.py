@@ -118,7 +118,7 @@ def test_every_kernel_opens_with_pdl_scope():
     root = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
                         "paper_2010_05680_b200", "csrc")
     n = 0
-    for f in glob.glob(os.path.join(root, "*.cu")):
+    for f in glob.glob(os.path.join(root, "*.cu")) + glob.glob(os.path.join(root, "*.cuh")):
         src = open(f).read()
         assert "<<<" not in src, f"{f}: raw <<<>>> launch bypasses launch_k (PDL attribute)"
         for m in re.finditer(r"__global__", src):
@@ -129,8 +129,16 @@ def test_every_kernel_opens_with_pdl_scope():
     assert n >= 12
 
 
+def _variants():
+    try:  # the default, plus the warp-specialised / split-row schedules of the tuning build
+        import paper_2010_05680_b200 as tt
+        return [0] + [v for v in (5, 6) if v in tt.attention_variants()]
+    except Exception:
+        return [0]
+
+
 @pytest.mark.gpu
-@pytest.mark.parametrize("variant", [0, 5, 6])
+@pytest.mark.parametrize("variant", _variants())
 def test_attention_block_chain_pdl_on_off_identical(ttlib, variant):
     """A whole dependent BERT attention block through the library, every kernel
     reading what the previous one wrote: QKV split + bias -> fused attention

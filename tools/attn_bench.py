@@ -16,6 +16,10 @@ import torch.nn.functional as F
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
+# the non-default variants live in the TT_TUNING build (paper_2010_05680_b200/build.py --tuning)
+if "TT_LIB_PATH" not in os.environ:
+    from paper_2010_05680_b200 import build as _b  # noqa: E402
+    os.environ["TT_LIB_PATH"] = _b.build(tuning=True)
 import paper_2010_05680_b200 as tt  # noqa: E402
 import workloads as W  # noqa: E402
 
@@ -52,8 +56,8 @@ def case(name, B, H, S, dtype, lens):
            for _ in range(nb)]
     outs = [torch.empty(B, H, S, D, device="cuda", dtype=dtype) for _ in range(nb)]
     L = torch.as_tensor(np.asarray(lens, dtype=np.int32)).cuda()
-    var_us = {}
-    for v in (1, 2, 3, 4, 5, 6, 7, 8):
+    var_us = {v: float("nan") for v in range(1, 9)}
+    for v in tt.attention_variants():
         tt.attention_variant(v)
         var_us[v] = timeit(lambda i: tt.tt_attention_fwd(outs[i], *qkv[i], L, 0.125), nb)
     tt.attention_variant(0)

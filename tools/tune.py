@@ -15,6 +15,10 @@ import torch
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
+# every tuning candidate lives in the TT_TUNING build (paper_2010_05680_b200/build.py --tuning)
+if "TT_LIB_PATH" not in os.environ:
+    from paper_2010_05680_b200 import build as _b  # noqa: E402
+    os.environ["TT_LIB_PATH"] = _b.build(tuning=True)
 import paper_2010_05680_b200 as tt  # noqa: E402
 import workloads as W  # noqa: E402
 
