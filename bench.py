@@ -138,7 +138,7 @@ class ClockSampler:
         0x100: "display_clock_setting",
     }
 
-    def __init__(self, dev: torch.device, period_s: float = 0.005):
+    def __init__(self, dev: torch.device, period_s: float = 0.00025):
         self.samples, self.reasons, self.ok = [], 0, False
         self.period, self.stop_ev = period_s, threading.Event()
         try:
@@ -213,21 +213,9 @@ def ncu_traffic(kernel_key: str):
 
 
 # ------------------------------------------------------------------ our arm
-def run_ours(args, rank, world, local_rank):
-    import paper_2010_05680_b200 as tt
-    from paper_2010_05680_b200 import sharding
-
-    dev = torch.device("cuda", local_rank)
-    torch.cuda.set_device(dev)
-    dist = None
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
-    tt.lib()
-    wl, desc, scaling = make_workload(args.workload, rank, world)
-    stream = torch.cuda.Stream(device=dev)
-
-    # inputs resident in HBM before the timed region (generated on device)
+def _units(tt, wl, rank, scaling, dev, stream):
+    """This rank's batches, generated on the device (resident in HBM before
+    any timed region)."""
     units = []
     with torch.cuda.stream(stream):
         for bi, lens in enumerate(wl.batches):
@@ -242,19 +230,14 @@ def run_ours(args, rank, world, local_rank):
                 x = x.reshape(-1)
             else:
                 cu = blocks = total = None
-            units.append(dict(lens=lens, scores=x, L=torch.as_tensor(lens).to(dev), cu=cu,
-                              blocks=blocks, total=total, maxlen=int(lens.max()),
+            units.append(dict(lens=lens, bid=bid, scores=x, L=torch.as_tensor(lens).to(dev),
+                              cu=cu, blocks=blocks, total=total, maxlen=int(lens.max()),
                               out=torch.empty_like(d["x"]), **d))
     stream.synchronize()
+    return units
 
-    plan_sm = (tt.softmax_packed_plan(wl.dtype, max(u["maxlen"] for u in units)) if wl.packed
-               else tt.softmax_plan(wl.dtype, *units[0]["scores"].shape))
-    plan_ln = tt.layernorm_plan(wl.dtype, *units[0]["x"].shape)
-    b_sm = sum(wl.bytes_softmax(u["lens"]) for u in units)
-    b_ln = sum(wl.bytes_ln(u["lens"]) for u in units)
-    rows_sm = sum(wl.rows(u["lens"])[0] for u in units)
-    rows_ln = sum(wl.rows(u["lens"])[1] for u in units)
 
+def _step_fn(tt, wl, units, stream):
     def step(ev=None):
         for u in units:
             if ev is not None:
@@ -270,15 +253,16 @@ def run_ours(args, rank, world, local_rank):
                                      u["beta"], wl.eps, stream=stream)
             if ev is not None:
                 ev[2].record(stream)
+    return step
 
-    for _ in range(args.warmup):
-        step()
-    stream.synchronize()
 
-    # ---- timed region: K steps, barrier + synchronize on both sides
-    K = args.steps
+def _timed(step, K, n_events, dist, dev, stream, coll_dev):
+    """K steps bracketed by barrier + synchronize on both sides, CUDA events on
+    the launching stream, NVML clocks sampled during the region; returns
+    (max-over-ranks ms, local ms, per-kernel event triples, clock summary)."""
+    from paper_2010_05680_b200 import sharding
     per_kernel = [[torch.cuda.Event(enable_timing=True) for _ in range(3)]
-                  for _ in range(min(K, args.kernel_events))]
+                  for _ in range(min(K, n_events))]
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if dist:
         dist.barrier()
@@ -286,52 +270,137 @@ def run_ours(args, rank, world, local_rank):
     with ClockSampler(dev) as clk:
         t0.record(stream)
         for k in range(K):
-            step(per_kernel[k] if (k < len(per_kernel) and len(units) == 1) else None)
+            step(per_kernel[k] if k < len(per_kernel) else None)
         t1.record(stream)
         stream.synchronize()
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
     ms_local = t0.elapsed_time(t1)
-    ms = sharding.max_over_ranks(ms_local, dev) if dist else ms_local
-    sm_ms = [e[0].elapsed_time(e[1]) for e in per_kernel] if len(units) == 1 else []
-    ln_ms = [e[1].elapsed_time(e[2]) for e in per_kernel] if len(units) == 1 else []
+    ms = sharding.max_over_ranks(ms_local, coll_dev) if dist else ms_local
+    return ms, ms_local, per_kernel, clk.summary()
 
-    # ---- per-rank record: digest of this rank's outputs, gathered over NCCL
-    digests, checksum = [], 0.0
-    for u in units:
-        digests.append(sharding.tensor_digest(u["out"][:64]))
-        checksum += float(u["out"].float().sum().item())
-    rec = sharding.make_record(sharding.combine_digests(digests), checksum, b_sm + b_ln,
-                               rows_sm + rows_ln, ms_local * 1000.0, len(units), rank).to(dev)
-    recs = sharding.gather_records(rec) if dist else rec.reshape(1, -1)
-    tot_bytes = float(recs[:, 3].sum().item())   # per step, all ranks
-    tot_rows = torch.tensor([float(rows_sm), float(rows_ln)], dtype=torch.float64, device=dev)
-    if dist:
-        dist.all_reduce(tot_rows)
-    tot_rows_sm, tot_rows_ln = (float(v) for v in tot_rows.tolist())
+
+def _digests(units):
+    """Per-batch digests of the FULL softmax output (in place) and LN output."""
+    from paper_2010_05680_b200 import sharding
+    return {int(u["bid"]): (sharding.device_digest(u["scores"]), sharding.device_digest(u["out"]))
+            for u in units}
+
+
+def _stream_record(dist, units, digests, ms, ms_local, rank, world, wl, K, scaling):
+    """Gather (rank, ms, batches, per-batch digests) to every rank; returns the
+    whole-stream aggregate seen by rank 0."""
+    from paper_2010_05680_b200 import sharding
+    mine = {"rank": rank, "ms": ms_local, "batches": sorted(digests),
+            "digests": digests,
+            "bytes": sum(wl.bytes_softmax(u["lens"]) + wl.bytes_ln(u["lens"]) for u in units),
+            "rows": [sum(wl.rows(u["lens"])[0] for u in units),
+                     sum(wl.rows(u["lens"])[1] for u in units)]}
+    allr = sharding.gather_objects(mine) if dist else [mine]
+    bd = {}
+    for r in allr:
+        for k, v in r["digests"].items():
+            bd[int(k)] = sharding.combine_digests(v)
+    tot_bytes = sum(r["bytes"] for r in allr)
+    return {
+        "value": round(tot_bytes * K / (ms / 1e3) / 1e9, 2), "ms_per_step": round(ms / K, 6),
+        "bytes_per_step": int(tot_bytes),
+        "rows_per_s": {"softmax": round(sum(r["rows"][0] for r in allr) * K / (ms / 1e3), 1),
+                       "layernorm": round(sum(r["rows"][1] for r in allr) * K / (ms / 1e3), 1)},
+        "stream_digest": f"{sharding.stream_digest(bd):016x}",
+        "batches": len(bd),
+        "ranks": [{"rank": r["rank"], "ms": round(r["ms"], 3), "batches": len(r["batches"]),
+                   "digest": f"{sharding.stream_digest({int(k): sharding.combine_digests(v) for k, v in r['digests'].items()}):016x}"}
+                  for r in sorted(allr, key=lambda r: r["rank"])],
+    }
+
+
+def run_ours(args, rank, world, local_rank):
+    import datetime
+    import paper_2010_05680_b200 as tt
+
+    ndev = torch.cuda.device_count()
+    dev = torch.device("cuda", local_rank % max(ndev, 1))
+    torch.cuda.set_device(dev)
+    dist = None
+    coll_dev = dev
+    if world > 1:
+        import torch.distributed as dist
+        timeout = datetime.timedelta(seconds=args.dist_timeout)
+        if args.backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev, timeout=timeout)
+        else:   # gloo: several ranks may share one GPU (tests); collectives on host tensors
+            dist.init_process_group("gloo", timeout=timeout)
+            coll_dev = torch.device("cpu")
+    tt.lib()
+    wl, desc, scaling = make_workload(args.workload, rank, world)
+    stream = torch.cuda.Stream(device=dev)
+    units = _units(tt, wl, rank, scaling, dev, stream)
+
+    plan_sm = (tt.softmax_packed_plan(wl.dtype, max(u["maxlen"] for u in units)) if wl.packed
+               else tt.softmax_plan(wl.dtype, *units[0]["scores"].shape))
+    plan_ln = tt.layernorm_plan(wl.dtype, *units[0]["x"].shape)
+    b_sm = sum(wl.bytes_softmax(u["lens"]) for u in units)
+    b_ln = sum(wl.bytes_ln(u["lens"]) for u in units)
+
+    step = _step_fn(tt, wl, units, stream)
+    for _ in range(args.warmup):
+        step()
+    stream.synchronize()
+
+    # ---- timed region: K steps
+    K = args.steps
+    n_ev = args.kernel_events if len(units) == 1 else 0
+    ms, ms_local, per_kernel, clocks = _timed(step, K, n_ev, dist, dev, stream, coll_dev)
+    sm_ms = [e[0].elapsed_time(e[1]) for e in per_kernel]
+    ln_ms = [e[1].elapsed_time(e[2]) for e in per_kernel]
+
+    # ---- per-batch digests of every output, gathered over the process group
+    rec = _stream_record(dist, units, _digests(units), ms, ms_local, rank, world, wl, K, scaling)
 
     # ---- end to end through the staged C-ABI call with pinned host buffers
-    e2e = (run_e2e(args, tt, wl, units, stream, dist, dev, world)
+    e2e = (run_e2e(args, tt, wl, units, stream, dist, dev, world, coll_dev)
            if args.e2e_steps > 0 and not wl.packed else None)
+
+    # ---- C5 strong-scaling sub-record (the BASELINE config-5 stream, LPT-sharded)
+    c5 = None
+    if args.workload == "c4" and args.c5_steps > 0:
+        del units, step
+        torch.cuda.empty_cache()
+        wl5, desc5, sc5 = make_workload("c5", rank, world)
+        u5 = _units(tt, wl5, rank, sc5, dev, stream)
+        st5 = _step_fn(tt, wl5, u5, stream)
+        for _ in range(3):
+            st5()
+        stream.synchronize()
+        ms5, ms5_local, _, clk5 = _timed(st5, args.c5_steps, 0, dist, dev, stream, coll_dev)
+        c5 = _stream_record(dist, u5, _digests(u5), ms5, ms5_local, rank, world, wl5,
+                            args.c5_steps, sc5)
+        c5.update({"workload": desc5["workload"], "scaling": sc5, "steps": args.c5_steps,
+                   "warmup": 3, "clocks": clk5,
+                   "kernels": {"softmax": tt.softmax_plan(wl5.dtype, *u5[0]["scores"].shape),
+                               "layernorm": tt.layernorm_plan(wl5.dtype, *u5[0]["x"].shape)}})
+        del u5, st5
 
     if rank != 0:
         if dist:
             dist.destroy_process_group()
         return None
 
-    value = tot_bytes * K / (ms / 1e3) / 1e9
+    value = rec["value"]
     peak, peak_src = measured_peak()
     out = {
-        "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world, "steps": K,
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
         "warmup": args.warmup, "ms_per_step": round(ms / K, 6), "higher_is_better": True,
         "scaling": scaling, "vs_baseline": None, "dtype": W.DTYPE_NAMES[wl.dtype],
+        "arith": "fp32",
         "data": "synthetic (seeded; logits N(0,8^2), LN inputs N(0,1); SURVEY §8(d) recipe)",
         "config": desc,
-        "rows_per_s": {"softmax": round(tot_rows_sm * K / (ms / 1e3), 1),
-                       "layernorm": round(tot_rows_ln * K / (ms / 1e3), 1)},
+        "rows_per_s": rec["rows_per_s"],
         "pct_of_peak": round(100.0 * value / (peak * world), 2),
-        "gpu_launches": 2 * len(units) * K,
+        "pct_of_nominal_8TBps": round(100.0 * value / (8000.0 * world), 2),
+        "gpu_launches": 2 * len(wl.batches) * K,
         "kernels": {"softmax": plan_sm, "layernorm": plan_ln},
     }
     if sm_ms:
@@ -352,11 +421,14 @@ def run_ours(args, rank, world, local_rank):
             "bytes_alg_per_launch": b_ln, "avg_launch_us": round(ln_avg * 1e3, 2),
             "share_of_step": round(ln_avg / (ms_local / K), 4),
         }
-    out["clocks"] = clk.summary()
+    out["clocks"] = clocks
     out["e2e"] = e2e
-    out["ranks"] = [{"rank": int(r[7]), "digest": f"{sharding.record_digest(r):016x}",
-                     "ms": round(float(r[5]) / 1e3, 3), "batches": int(r[6])}
-                    for r in recs.cpu().tolist()] if world > 1 else None
+    out["stream_digest"] = rec["stream_digest"]
+    out["ranks"] = rec["ranks"] if world > 1 else None
+    if c5 is not None:
+        out["c5_stream"] = c5
+    if world > 1:
+        out["backend"] = args.backend
     if not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(wl, budget_s=args.cpu_budget)
     if dist:
@@ -364,7 +436,7 @@ def run_ours(args, rank, world, local_rank):
     return out
 
 
-def run_e2e(args, tt, wl, units, stream, dist, dev, world):
+def run_e2e(args, tt, wl, units, stream, dist, dev, world, coll_dev):
     """Same metric end to end: per step, H2D of the step's inputs from pinned
     host memory, both kernels, D2H of both results, through the staged C ABI."""
     hosts = []
@@ -409,7 +481,7 @@ def run_e2e(args, tt, wl, units, stream, dist, dev, world):
     ms = a.elapsed_time(b)
     if dist:
         from paper_2010_05680_b200 import sharding
-        ms = sharding.max_over_ranks(ms, dev)
+        ms = sharding.max_over_ranks(ms, coll_dev)
     per_step_bytes = sum(wl.bytes_softmax(u["lens"]) + wl.bytes_ln(u["lens"]) for u in units)
     mult = world
     value = per_step_bytes * mult * E / (ms / 1e3) / 1e9
@@ -500,12 +572,33 @@ def _calibrate(wl, cores, target_s):
     return min(1.0, frac * max(target_s, 0.01) / max(dt, 1e-6))
 
 
+def _cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
 def cpu_baseline(wl, budget_s=10.0):
+    """The oracle as it stands on this box's host cores: all threads (the
+    reported value) and one thread (same sample, for the per-core figure)."""
     cores = os.cpu_count() or 1
     frac = _calibrate(wl, cores, budget_s)
-    dt, nbytes, rows = _oracle_run(_oracle_sample(wl, frac, seed=1), wl, cores)
+    sample = _oracle_sample(wl, frac, seed=1)
+    dt, nbytes, rows = _oracle_run(sample, wl, cores)
+    frac1 = frac / max(1, cores)
+    s1 = _oracle_sample(wl, frac1, seed=1)
+    dt1, nb1, rows1 = _oracle_run(s1, wl, 1)
     return {"value": round(nbytes / dt / 1e9, 4), "unit": UNIT, "cores": cores, "kind": "oracle",
             "rows_per_s": round(rows / dt, 1), "seconds": round(dt, 2),
+            "one_thread": {"value": round(nb1 / dt1 / 1e9, 4), "unit": UNIT,
+                           "rows_per_s": round(rows1 / dt1, 1), "seconds": round(dt1, 2),
+                           "sample": f"{frac1:.4%} of the rows"},
+            "cpu_model": _cpu_model(),
             "sample": f"{frac:.4%} of the {wl.name} softmax rows and LN rows "
                       f"(same shapes and value distributions), fp64 C oracle, "
                       f"row-partitioned over {cores} host threads"}
@@ -545,6 +638,25 @@ def run_reference(args, rank, world):
             "rows_per_s": round(tot_r / tot_t, 1)}
 
 
+def _spawn(n: int) -> int:
+    """`--gpus N` without torchrun: start N copies of this script with the
+    torch.distributed environment (one process per GPU, rendezvous on
+    127.0.0.1); rank 0's stdout is this process's stdout.  Returns the worst
+    exit code."""
+    import socket
+    import subprocess
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    procs = []
+    for r in range(n):
+        env = dict(os.environ, RANK=str(r), LOCAL_RANK=str(r), WORLD_SIZE=str(n),
+                   LOCAL_WORLD_SIZE=str(n), MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        procs.append(subprocess.Popen([sys.executable, os.path.abspath(__file__), *sys.argv[1:]],
+                                      env=env, stdout=None if r == 0 else subprocess.DEVNULL))
+    return max(p.wait() for p in procs)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -560,15 +672,22 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=10.0)
     ap.add_argument("--ref-budget", type=float, default=90.0)
+    ap.add_argument("--backend", choices=["nccl", "gloo"], default="nccl",
+                    help="process-group backend for N > 1 (gloo: ranks may share a GPU; tests)")
+    ap.add_argument("--dist-timeout", type=float, default=600.0,
+                    help="process-group timeout, seconds")
+    ap.add_argument("--c5-steps", type=int, default=10,
+                    help="timed steps of the C5 strong-scaling sub-record (c4 workload; 0: off)")
     args = ap.parse_args()
     if args.warmup < 3:
         raise SystemExit("--warmup must be >= 3")
+    if "RANK" not in os.environ and args.gpus > 1:
+        raise SystemExit(_spawn(args.gpus))
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
-        if world == 1 and args.gpus > 1:
-            raise SystemExit("launch N>1 under torchrun (one process per GPU)")
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     if args.impl == "reference":
         out = run_reference(args, rank, world)
     else:

@@ -217,8 +217,7 @@ struct LnTier {
     /* selected through the preference tables kLnPref* */                                    \
     TT_LN_TIER(false, T, TN, 32, 32, 3, 1, 256, 1), TT_LN_TIER(false, T, TN, 32, 32, 4, 1, 256, 1), \
     TT_LN_TIER(false, T, TN, 32, 32, 4, 1, 128, 1), TT_LN_TIER(false, T, TN, 32, 32, 2, 1, 256, 1), \
-    TT_LN_TIER(false, T, TN, 16, 32, 3, 1, 256, 1), TT_LN_TIER(false, T, TN, 32, 128, 4, 1, 128, 1), \
-    TT_LN_TIER(false, T, TN, 32, 128, 2, 1, 128, 1), TT_LN_TIER(false, T, TN, 16, 128, 4, 1, 128, 1), \
+    TT_LN_TIER(false, T, TN, 16, 32, 3, 1, 256, 1),                                        \
     TT_LN_EARLY(false, T, TN, 16, 32, 3, 128), TT_LN_EARLY(false, T, TN, 16, 32, 3, 256),        \
     TT_LN_EARLY(false, T, TN, 32, 32, 2, 128), TT_LN_EARLY(false, T, TN, 32, 32, 2, 256),        \
     TT_LN_EARLY(false, T, TN, 32, 32, 3, 256), TT_LN_EARLY(false, T, TN, 32, 32, 4, 256),        \

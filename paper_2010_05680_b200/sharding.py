@@ -53,6 +53,45 @@ def tensor_digest(t: torch.Tensor) -> int:
     return int.from_bytes(hashlib.blake2b(b, digest_size=8).digest(), "little")
 
 
+_M64 = (1 << 64) - 1
+_K1 = 0x9E3779B97F4A7C15 - (1 << 64)   # as signed int64
+_K2 = 0xBF58476D1CE4E5B9 - (1 << 64)
+
+
+def device_digest(t: torch.Tensor, chunk: int = 1 << 24) -> int:
+    """64-bit positional digest of a tensor's bytes computed where the tensor
+    lives (no host copy of multi-GB outputs): sum over 32-bit words w_i of
+    mix(w_i, i) modulo 2^64.  Integer addition modulo 2^64 is associative and
+    commutative, so the value does not depend on the reduction order -- the
+    same bytes give the same digest on any device and at any world size."""
+    b = t.detach().contiguous().view(-1).view(torch.uint8)
+    if b.numel() % 4:
+        b = torch.cat([b, b.new_zeros(4 - b.numel() % 4)])
+    w = b.view(torch.int32)
+    acc = 0
+    for off in range(0, w.numel(), chunk):
+        v = w[off:off + chunk].to(torch.int64) & 0xFFFFFFFF
+        idx = torch.arange(off, off + v.numel(), device=v.device, dtype=torch.int64)
+        h = (v ^ (idx * _K1)) * _K2
+        h = h ^ (h >> 31)
+        acc = (acc + int(h.sum().item())) & _M64
+    return acc ^ (t.numel() * 0x100000001B3 & _M64)
+
+
+def gather_objects(obj, group=None) -> list:
+    """all_gather_object over the default group (nccl or gloo)."""
+    import torch.distributed as dist
+    out = [None] * dist.get_world_size(group)
+    dist.all_gather_object(out, obj, group=group)
+    return out
+
+
+def stream_digest(batch_digests: dict) -> int:
+    """Digest of a whole request stream from {batch_id: digest}: independent
+    of which rank processed which batch (sharding invariance)."""
+    return combine_digests([batch_digests[k] for k in sorted(batch_digests)])
+
+
 def combine_digests(digests: Sequence[int]) -> int:
     h = hashlib.blake2b(digest_size=8)
     for d in digests:

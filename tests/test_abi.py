@@ -237,3 +237,7 @@ def test_every_preferred_tier_is_compiled(ttlib):
         assert names, fname
         for n, d in names:
             assert n in ttlib.tiers(op, dn[d]), n
+    for op in ("softmax", "layernorm"):
+        for dt in dn.values():
+            names = ttlib.tiers(op, dt)
+            assert len(names) == len(set(names)), (op, dt)   # one entry per kernel

@@ -1,8 +1,11 @@
 #!/usr/bin/env python
 """Sweep BASELINE.json's configurations through both operations; one JSON line
 per (config, op, dtype, lengths) with time per call, algorithmic GB/s, % of
-the measured copy peak and the same-traffic torch reference, plus an
-empty-kernel launch floor for the launch-bound small shapes.
+the measured copy peak and of the nominal 8 TB/s, the same-traffic torch
+reference (an SM element-wise kernel moving the same bytes: torch.neg for the
+softmax, torch.add for the LayerNorm), the max abs error against the fp64
+oracle on sampled rows, plus an empty-kernel launch floor for the
+launch-bound small shapes.
 
   python tools/sweep.py > gpurun_out/sweep.jsonl
 """
@@ -15,8 +18,11 @@ import torch
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
+import oracle  # noqa: E402  (error column only: the timed calls never touch it)
 import paper_2010_05680_b200 as tt  # noqa: E402
 import workloads as W  # noqa: E402
+
+NOMINAL_GBPS = 8000.0
 
 L2 = 126 * 1024 * 1024
 
@@ -65,14 +71,28 @@ def softmax_case(cfg, dtype, B, H, S, lens, pk):
     L = torch.as_tensor(np.asarray(lens, dtype=np.int32)).cuda()
     reps = 200 if nbytes < 64 << 20 else 50
     us = timeit(lambda i: tt.tt_softmax_masked(bufs[i], L, 0.125), nb, reps)
+    # same-traffic reference: an SM element-wise kernel reading and writing the
+    # buffer once (torch.neg), scaled to the softmax's algorithmic bytes.  (A
+    # D2D copy_ is a copy-engine memcpy inside a graph, ~3 TB/s: not a peer.)
     other = [torch.empty_like(b) for b in bufs]
-    us_copy = timeit(lambda i: other[i].copy_(bufs[i]), nb, reps)
+    us_ref = timeit(lambda i: torch.neg(bufs[i], out=other[i]), nb, reps)
     alg = W.softmax_bytes_alg(lens, H, S, S, e)
+    # max abs error vs the oracle on 256 sampled rows of a fresh input
+    x = W.scores(B, H, S, S, dtype, device="cuda", seed=12345)
+    nrows = B * H * S
+    idx = torch.randint(0, nrows, (min(256, nrows),), generator=torch.Generator().manual_seed(1))
+    before = x.view(nrows, S)[idx.cuda()].cpu()
+    tt.tt_softmax_masked(x, L, 0.125)
+    got = x.view(nrows, S)[idx.cuda()].cpu().double()
+    ref = oracle.softmax_rows(before, np.asarray(lens, dtype=np.int32)[(idx // (H * S)).numpy()],
+                              0.125)
+    err = float((got - ref).abs().max())
     return dict(config=cfg, op="softmax", dtype=W.DTYPE_NAMES[dtype], shape=[B, H, S, S],
                 ragged=bool(np.any(np.asarray(lens) < S)), us=round(us, 2),
                 GBps=round(alg / us / 1e3, 1), pct_peak=round(100 * alg / us / 1e3 / pk, 1),
-                copy_same_bytes_us=round(us_copy * alg / (2 * nbytes), 2),
-                tier=tt.softmax_plan(dtype, B, H, S, S))
+                pct_nominal=round(100 * alg / us / 1e3 / NOMINAL_GBPS, 1),
+                ref_same_traffic_us=round(us_ref * alg / (2 * nbytes), 2),
+                max_abs_err=err, tier=tt.softmax_plan(dtype, B, H, S, S))
 
 
 def ln_case(cfg, dtype, rows, hidden, pk):
@@ -87,9 +107,18 @@ def ln_case(cfg, dtype, rows, hidden, pk):
                                                    1e-12), nb, reps)
     us_add = timeit(lambda i: torch.add(ds[i]["x"], ds[i]["residual"], out=outs[i]), nb, reps)
     alg = W.ln_bytes_alg(rows, hidden, e)
+    d = W.ln_inputs(rows, hidden, dtype, device="cuda", seed=12345)
+    o = torch.empty_like(d["x"])
+    tt.tt_add_bias_layernorm(o, d["x"], d["residual"], d["bias"], d["gamma"], d["beta"], 1e-12)
+    idx = torch.randint(0, rows, (min(256, rows),), generator=torch.Generator().manual_seed(1)).cuda()
+    ref = oracle.add_bias_layernorm(d["x"][idx].cpu(), d["residual"][idx].cpu(), d["bias"].cpu(),
+                                    d["gamma"].cpu(), d["beta"].cpu(), 1e-12)
+    err = float((o[idx].cpu().double() - ref).abs().max())
     return dict(config=cfg, op="layernorm", dtype=W.DTYPE_NAMES[dtype], shape=[rows, hidden],
                 ragged=False, us=round(us, 2), GBps=round(alg / us / 1e3, 1),
-                pct_peak=round(100 * alg / us / 1e3 / pk, 1), torch_add_same_traffic_us=round(us_add, 2),
+                pct_peak=round(100 * alg / us / 1e3 / pk, 1),
+                pct_nominal=round(100 * alg / us / 1e3 / NOMINAL_GBPS, 1),
+                ref_same_traffic_us=round(us_add, 2), max_abs_err=err,
                 tier=tt.layernorm_plan(dtype, rows, hidden))
 
 
@@ -107,12 +136,12 @@ def next2_cases(pk):
         b = torch.zeros(n, dtype=dtype, device="cuda")
         ys = [torch.empty_like(x) for x in xs]
         us = timeit(lambda i: tt.tt_add_bias_gelu(ys[i], xs[i], b), nb, 50)
-        us_c = timeit(lambda i: ys[i].copy_(xs[i]), nb, 50)
+        us_c = timeit(lambda i: torch.neg(xs[i], out=ys[i]), nb, 50)
         alg = 2 * rows * n * e + n * e
         out.append(dict(config=f"BERT b{B} s{S}", op="add_bias_gelu", dtype=W.DTYPE_NAMES[dtype],
                         shape=[rows, n], ragged=False, us=round(us, 2),
                         GBps=round(alg / us / 1e3, 1), pct_peak=round(100 * alg / us / 1e3 / pk, 1),
-                        copy_same_bytes_us=round(us_c, 2), tier="add_bias_gelu<V16>"))
+                        ref_same_traffic_us=round(us_c, 2), tier="add_bias_gelu<V16>"))
         # QKV split [rows, 3*hid] -> 3 x [B, H, S, D]; head merge [B, H, S, D] -> [rows, hid]
         nb = nbufs_for(2 * rows * 3 * hid * e)
         qkv = [W.scores(1, 1, rows, 3 * hid, dtype, device="cuda", seed=i).reshape(rows, 3 * hid)
@@ -121,20 +150,20 @@ def next2_cases(pk):
         outs = [[torch.empty(B, H, S, D, dtype=dtype, device="cuda") for _ in range(3)]
                 for _ in range(nb)]
         us = timeit(lambda i: tt.tt_split_qkv_add_bias(*outs[i], qkv[i], bias, B, S, H, D), nb, 50)
-        us_c = timeit(lambda i: outs[i][0].view(-1).copy_(qkv[i].view(-1)[:rows * hid]), nb, 50)
+        us_c = timeit(lambda i: torch.neg(qkv[i].view(-1)[:rows * hid], out=outs[i][0].view(-1)), nb, 50)
         alg = 2 * rows * 3 * hid * e + 3 * hid * e
         out.append(dict(config=f"BERT b{B} s{S}", op="split_qkv_add_bias", dtype=W.DTYPE_NAMES[dtype],
                         shape=[rows, 3 * hid], ragged=False, us=round(us, 2),
                         GBps=round(alg / us / 1e3, 1), pct_peak=round(100 * alg / us / 1e3 / pk, 1),
-                        copy_same_bytes_us=round(3 * us_c, 2), tier="split_qkv<V16>"))
+                        ref_same_traffic_us=round(3 * us_c, 2), tier="split_qkv<V16>"))
         ms = [torch.empty(rows, hid, dtype=dtype, device="cuda") for _ in range(nb)]
         us = timeit(lambda i: tt.tt_merge_heads(ms[i], outs[i][0], B, S, H, D), nb, 50)
-        us_c = timeit(lambda i: ms[i].view(-1).copy_(outs[i][0].view(-1)), nb, 50)
+        us_c = timeit(lambda i: torch.neg(outs[i][0].view(-1), out=ms[i].view(-1)), nb, 50)
         alg = 2 * rows * hid * e
         out.append(dict(config=f"BERT b{B} s{S}", op="merge_heads", dtype=W.DTYPE_NAMES[dtype],
                         shape=[B, H, S, D], ragged=False, us=round(us, 2),
                         GBps=round(alg / us / 1e3, 1), pct_peak=round(100 * alg / us / 1e3 / pk, 1),
-                        copy_same_bytes_us=round(us_c, 2), tier="merge_heads<V16>"))
+                        ref_same_traffic_us=round(us_c, 2), tier="merge_heads<V16>"))
     return out
 
 
