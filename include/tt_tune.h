@@ -34,12 +34,18 @@ TT_API tt_status ttx_force_tier(int op, int dtype, int i);
  * (producer warp, MMA warp, 4 softmax warps; mbarrier hand-offs, no CTA barrier
  * in the tile loop; 2 CTAs per SM), 6 / 7 = variant 4 with two threads per
  * query row (8 warps; 2 / 3 CTAs per SM), 8 = variant 4 waiting for the previous
- * P.V only after the exponentials.  Variants 1..8 are compiled into the tuning
- * build only (ttx_tuning_build); the product library has 0 (= variant 4); TT_ERROR_INVALID_VALUE outside
- * 0 .. ttx_attention_variant_count() - 1. */
+ * P.V only after the exponentials, 9 = warp-specialised: two 128-row query tiles
+ * per CTA sharing K / V loaded by TMA, a producer warp, an MMA warp and two
+ * ping-ponging softmax warpgroups, P kept in TMEM (attention_fa.cu), 128-key
+ * tiles; 10 = the same with 64-key tiles and two S buffers per query tile.
+ * Variants 1..10 are compiled into the tuning build only (ttx_tuning_build);
+ * TT_ERROR_INVALID_VALUE for a variant not compiled in (ttx_attention_variant_ok). */
 TT_API tt_status ttx_attention_variant(int v);
-/* Number of attention variants compiled into this library (0 .. n-1 valid). */
+/* Variant ids are 0 .. ttx_attention_variant_count() - 1; ttx_attention_variant_ok
+ * says whether variant v is compiled into this library (0 always; 1..10
+ * in the tuning build only). */
 TT_API int ttx_attention_variant_count(void);
+TT_API int ttx_attention_variant_ok(int v);
 /* 1 in the tuning build (libtt_tune.so, -DTT_TUNING: every tuning candidate
  * compiled in), 0 in the product library libtt.so. */
 TT_API int ttx_tuning_build(void);

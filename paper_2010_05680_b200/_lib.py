@@ -37,7 +37,7 @@ EXPORTS = (
     "ttx_tier_count", "ttx_tier_name", "ttx_force_tier",
     "tt_add_bias_gelu", "tt_split_qkv_add_bias", "tt_merge_heads",
     "tt_dp_schedule", "tt_schedule_cost", "tt_attention_fwd", "ttx_attention_variant",
-    "ttx_attention_variant_count", "ttx_tuning_build", "ttx_set_pdl", "ttx_get_pdl",
+    "ttx_attention_variant_count", "ttx_attention_variant_ok", "ttx_tuning_build", "ttx_set_pdl", "ttx_get_pdl",
 )
 
 
@@ -92,6 +92,7 @@ def lib() -> ctypes.CDLL:
                                            _f, _vp]
             L.ttx_attention_variant.argtypes = [_i]
             L.ttx_attention_variant_count.argtypes = []
+            L.ttx_attention_variant_ok.argtypes = [_i]
             L.ttx_tuning_build.argtypes = []
             L.ttx_set_pdl.argtypes = [_i]
             L.ttx_get_pdl.argtypes = []
@@ -408,13 +409,15 @@ def attention_variant(v: int):
     4 = 64-key tiles double-buffered, pipelined (3 CTAs/SM), 5 = warp-specialised
     (producer / MMA / softmax warps, mbarrier hand-offs, 2 CTAs/SM), 6 / 7 = variant 4
     with two threads per query row (2 / 3 CTAs/SM), 8 = variant 4 with the previous
-    P.V waited for after the exponentials (1..8: tuning build only)."""
+    P.V waited for after the exponentials, 9 / 10 = warp-specialised TMA schedules
+    with 128- / 64-key tiles (1..10: tuning build only)."""
     _check(lib().ttx_attention_variant(int(v)), "ttx_attention_variant")
 
 
 def attention_variants() -> list:
     """Attention variants compiled into the loaded library besides 0 (automatic)."""
-    return list(range(1, lib().ttx_attention_variant_count()))
+    L = lib()
+    return [v for v in range(1, L.ttx_attention_variant_count()) if L.ttx_attention_variant_ok(v)]
 
 
 def tuning_build() -> bool:

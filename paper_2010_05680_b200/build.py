@@ -28,9 +28,9 @@ BUILD_DIR = os.path.join(PKG, "_build")
 TUNE_LIB = os.path.join(PKG, "libtt_tune.so")
 TUNE_BUILD_DIR = os.path.join(PKG, "_build_tune")
 SOURCES = ["tt_api.cu", "softmax.cu", "softmax_packed.cu", "layernorm.cu", "elementwise.cu",
-           "scheduler.cpp", "attention.cu"]
+           "scheduler.cpp", "attention.cu", "attention_fa.cu"]
 HEADERS = ["common.cuh", "launch.h", "softmax_row.cuh", "layernorm_kernels.cuh",
-           "softmax_kernels.cuh"]
+           "softmax_kernels.cuh", "tcgen05.cuh"]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 GENCODE = ["-gencode", "arch=compute_100a,code=sm_100a"]

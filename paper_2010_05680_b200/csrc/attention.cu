@@ -32,6 +32,7 @@
 
 #include "common.cuh"
 #include "launch.h"
+#include "tcgen05.cuh"
 
 namespace tt {
 
@@ -39,117 +40,6 @@ namespace {
 
 constexpr int kBM = 128, kD = 64, kNT = 128;
 constexpr int kTile = kBM * kD * 2;  // 16 KB: 128 rows x 128 B
-
-// ---- PTX wrappers (tcgen05 / cp.async) -------------------------------------
-__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint32_t src_bytes) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src),
-                 "r"(src_bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() {
-    asm volatile("cp.async.commit_group;" ::: "memory");
-}
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
-__device__ __forceinline__ void tc_fence_before() {
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-}
-__device__ __forceinline__ void tc_fence_after() {
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-}
-__device__ __forceinline__ void tc_mma(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
-                                       uint32_t idesc, uint32_t accumulate) {
-    asm volatile(
-        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
-        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
-        : "memory");
-}
-__device__ __forceinline__ void tc_commit(uint64_t* bar) {
-    asm volatile(
-        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-            smem_u32(bar))
-        : "memory");
-}
-// 32 consecutive TMEM columns of this thread's lane
-__device__ __forceinline__ void tc_ld32(uint32_t taddr, float (&v)[32]) {
-    uint32_t r[32];
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
-        "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
-          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
-          "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]),
-          "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
-          "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),
-          "=r"(r[31])
-        : "r"(taddr));
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-    for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-}
-
-// the same without the wait (several loads in flight, then tc_wait_ld)
-__device__ __forceinline__ void tc_ld32_nowait(uint32_t taddr, uint32_t (&r)[32]) {
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
-        "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
-          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
-          "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]),
-          "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
-          "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),
-          "=r"(r[31])
-        : "r"(taddr));
-}
-__device__ __forceinline__ void tc_wait_ld() {
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-}
-// 32 consecutive TMEM columns of this thread's lane <- registers
-__device__ __forceinline__ void tc_st32(uint32_t taddr, const float (&v)[32]) {
-    asm volatile(
-        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"
-        "%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(
-            taddr),
-        "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]),
-        "f"(v[8]), "f"(v[9]), "f"(v[10]), "f"(v[11]), "f"(v[12]), "f"(v[13]), "f"(v[14]),
-        "f"(v[15]), "f"(v[16]), "f"(v[17]), "f"(v[18]), "f"(v[19]), "f"(v[20]), "f"(v[21]),
-        "f"(v[22]), "f"(v[23]), "f"(v[24]), "f"(v[25]), "f"(v[26]), "f"(v[27]), "f"(v[28]),
-        "f"(v[29]), "f"(v[30]), "f"(v[31])
-        : "memory");
-    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-}
-
-// bounded wait: a fault in the async units traps instead of hanging the GPU
-__device__ __forceinline__ void mbar_wait_bounded(uint64_t* bar, uint32_t parity) {
-    uint32_t done = 0, spins = 0;
-    while (true) {
-        asm volatile(
-            "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
-            "selp.u32 %0, 1, 0, p;\n}\n"
-            : "=r"(done)
-            : "r"(smem_u32(bar)), "r"(parity)
-            : "memory");
-        if (done) return;
-        if (++spins > (1u << 26)) __trap();
-    }
-}
-
-// SWIZZLE_128B shared-memory matrix descriptor (version 1, base offset 0):
-// start >> 4 in [0,14), LBO >> 4 in [16,30), SBO >> 4 in [32,46), layout in [61,64)
-__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
-    return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
-           ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46) | (2ull << 61);
-}
-
-// instruction descriptor, kind::f16: fp32 accumulate, A/B format (0 f16, 1 bf16),
-// A K-major, B K- or MN-major, N >> 3 at [17,23), M >> 4 at [24,29)
-__host__ __device__ constexpr uint32_t f16_idesc(int ab_fmt, int b_mn_major, int M, int N) {
-    return (1u << 4) | ((uint32_t)ab_fmt << 7) | ((uint32_t)ab_fmt << 10) |
-           ((uint32_t)b_mn_major << 16) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
-}
 
 // tile row r (128 B = 64 x 16-bit), 16-byte chunk c -> swizzled smem offset
 __device__ __forceinline__ uint32_t sw_off(int r, int c) {
@@ -1077,6 +967,12 @@ cudaError_t launch_attn_split(void* out, const void* q, const void* k, const voi
 
 #endif  // TT_TUNING
 
+}  // namespace
+cudaError_t attention_fa_launch(int dtype, int bn, void* out, const void* q, const void* k,
+                                const void* v, const int32_t* lengths, int64_t B, int64_t H,
+                                int64_t S, float scale, cudaStream_t stream);  // attention_fa.cu
+namespace {
+
 template <typename T>
 cudaError_t launch_attn_any(void* out, const void* q, const void* k, const void* v,
                             const int32_t* lengths, int64_t B, int64_t H, int64_t S, float scale,
@@ -1085,6 +981,12 @@ cudaError_t launch_attn_any(void* out, const void* q, const void* k, const void*
     // profiles/r01_attn_bench.jsonl)
     switch (g_attn_nbuf.load(std::memory_order_relaxed)) {
 #ifdef TT_TUNING
+        case 9:
+            return attention_fa_launch(std::is_same<T, __half>::value ? 1 : 2, 128, out, q, k, v,
+                                       lengths, B, H, S, scale, st);
+        case 10:
+            return attention_fa_launch(std::is_same<T, __half>::value ? 1 : 2, 64, out, q, k, v,
+                                       lengths, B, H, S, scale, st);
         case 1: return launch_attn<T, 1, 128>(out, q, k, v, lengths, B, H, S, scale, st);
         case 2: return launch_attn<T, 2, 128>(out, q, k, v, lengths, B, H, S, scale, st);
         case 3: return launch_attn<T, 1, 64>(out, q, k, v, lengths, B, H, S, scale, st);
@@ -1099,16 +1001,21 @@ cudaError_t launch_attn_any(void* out, const void* q, const void* k, const void*
 }
 }  // namespace
 
-int attention_variant_count() {
+// Variants compiled into this build: 0 (automatic = the pipelined 64-key
+// schedule) and, in the TT_TUNING build, the measured-slower schedules 1 .. 8
+// and the warp-specialised TMA / two-Q-tile ones (9, 10; attention_fa.cu).
+bool attention_variant_ok(int v) {
 #ifdef TT_TUNING
-    return 9;
+    return v >= 0 && v <= 10;
 #else
-    return 1;  // 0 = automatic (variant 4); 1 .. 8 are compiled into the tuning build only
+    return v == 0;
 #endif
 }
 
+int attention_variant_count() { return 11; }
+
 bool attention_force_variant(int v) {
-    if (v < 0 || v >= attention_variant_count()) return false;
+    if (!attention_variant_ok(v)) return false;
     g_attn_nbuf.store(v);
     return true;
 }

@@ -46,7 +46,8 @@ cudaError_t attention_launch(int dtype, void* out, const void* q, const void* k,
                              const int32_t* lengths, int64_t B, int64_t H, int64_t S,
                              float scale, cudaStream_t stream);
 bool attention_force_variant(int v);  // 0 auto, 1..4 (5..8 in the TT_TUNING build)
-int attention_variant_count();       // variants compiled into this build (incl. 0)
+int attention_variant_count();       // variant ids are 0 .. count-1
+bool attention_variant_ok(int v);    // variant v compiled into this build
 cudaError_t smem_optin(const void* kern, size_t smem);  // per-device dynamic-smem opt-in
 
 // Tuning / test hooks (include/tt_tune.h): enumerate every compiled tier and

@@ -167,14 +167,16 @@ struct PackedTier {
             "softmax_packed<" TN ",V32,NV" #NV ",T256,M" #MINB ",P4>"                      \
     }
 
-// register caps as in the padded warp tiers (NV * VE fp32 values per lane)
+// register caps as in the padded warp tiers (NV * VE fp32 values per lane),
+// lowered by one CTA per SM where ptxas would spill at the padded tier's cap
+// (f32 NV3, f16 NV1, 16-bit NV3)
 const PackedTier kPk_f32[] = {TT_PK(float, "f32", 1, 6), TT_PK(float, "f32", 2, 3),
-                              TT_PK(float, "f32", 3, 5), TT_PK(float, "f32", 4, 4)};
-const PackedTier kPk_f16[] = {TT_PK(__half, "f16", 1, 6), TT_PK(__half, "f16", 2, 4),
-                              TT_PK(__half, "f16", 3, 3), TT_PK(__half, "f16", 4, 2)};
+                              TT_PK(float, "f32", 3, 4), TT_PK(float, "f32", 4, 4)};
+const PackedTier kPk_f16[] = {TT_PK(__half, "f16", 1, 5), TT_PK(__half, "f16", 2, 4),
+                              TT_PK(__half, "f16", 3, 2), TT_PK(__half, "f16", 4, 2)};
 const PackedTier kPk_bf16[] = {TT_PK(__nv_bfloat16, "bf16", 1, 6),
                                TT_PK(__nv_bfloat16, "bf16", 2, 4),
-                               TT_PK(__nv_bfloat16, "bf16", 3, 3),
+                               TT_PK(__nv_bfloat16, "bf16", 3, 2),
                                TT_PK(__nv_bfloat16, "bf16", 4, 2)};
 
 const PackedTier* pick(int dtype, int64_t max_len) {

@@ -626,6 +626,8 @@ const char* ttx_tier_name(int op, int dtype, int i) {
 
 int ttx_attention_variant_count(void) { return tt::attention_variant_count(); }
 
+int ttx_attention_variant_ok(int v) { return tt::attention_variant_ok(v) ? 1 : 0; }
+
 int ttx_tuning_build(void) {
 #ifdef TT_TUNING
     return 1;

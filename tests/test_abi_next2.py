@@ -61,12 +61,14 @@ def test_attention_validation(ttlib, dt):
 
 
 def test_attention_variant_hook(ttlib):
-    h = ttlib.lib().ttx_attention_variant
-    n = ttlib.lib().ttx_attention_variant_count()
-    # the product library holds the automatic schedule only; the tuning build
-    # (ttx_tuning_build) adds variants 1..8
-    assert n == (9 if ttlib.tuning_build() else 1)
+    L = ttlib.lib()
+    h, ok = L.ttx_attention_variant, L.ttx_attention_variant_ok
+    n = L.ttx_attention_variant_count()
+    # the product library holds the automatic choice only; the tuning build
+    # (ttx_tuning_build) adds variants 1..10
+    want = set(range(11)) if ttlib.tuning_build() else {0}
+    assert n == 11 and {v for v in range(n) if ok(v)} == want
     for v in range(n):
-        assert h(v) == OK
+        assert h(v) == (OK if v in want else INV)
     assert h(-1) == INV and h(n) == INV
     assert h(0) == OK

@@ -56,7 +56,7 @@ def case(name, B, H, S, dtype, lens):
            for _ in range(nb)]
     outs = [torch.empty(B, H, S, D, device="cuda", dtype=dtype) for _ in range(nb)]
     L = torch.as_tensor(np.asarray(lens, dtype=np.int32)).cuda()
-    var_us = {v: float("nan") for v in range(1, 9)}
+    var_us = {v: float("nan") for v in range(1, 11)}
     for v in tt.attention_variants():
         tt.attention_variant(v)
         var_us[v] = timeit(lambda i: tt.tt_attention_fwd(outs[i], *qkv[i], L, 0.125), nb)
@@ -70,7 +70,8 @@ def case(name, B, H, S, dtype, lens):
                bn128_us=round(var_us[1], 2), bn128x2_us=round(var_us[2], 2),
                bn64_us=round(var_us[3], 2), bn64x2_us=round(var_us[4], 2),
                ws_us=round(var_us[5], 2), split_us=round(var_us[6], 2),
-               split3_us=round(var_us[7], 2), late_us=round(var_us[8], 2))
+               split3_us=round(var_us[7], 2), late_us=round(var_us[8], 2),
+               fa_us=round(var_us[9], 2), fa64_us=round(var_us[10], 2))
     # unfused: QK^T (cuBLAS), masked softmax (ours, in place), PV (cuBLAS)
     sc = torch.empty(B, H, S, S, device="cuda", dtype=dtype)
 

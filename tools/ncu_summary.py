@@ -49,6 +49,16 @@ for rep in sys.argv[1:]:
         for w in WANT:
             if w in m:
                 print(f"    {w:34s} {m[w]}")
+    for d in raw(rep, ["pipe"]):
+        pipes = []
+        for h, (v, u) in d.items():
+            if "pct_of_peak_sustained_active" in h and ("inst_executed_pipe" in h or "pipe_" in h):
+                try:
+                    pipes.append((float(v.replace(",", "")), h))
+                except ValueError:
+                    pass
+        for v, h in sorted(pipes, reverse=True)[:10]:
+            print(f"    {h:70s} {v:.1f} %")
     for d in raw(rep, ["dram__bytes_read.sum", "dram__bytes_write.sum",
                        "smsp__average_warp_latency_issue_stalled", "smsp__pcsamp_warps_issue_stalled"]):
         st = [(h, v) for h, (v, u) in d.items() if "stalled" in h]
