@@ -75,7 +75,7 @@ typedef enum {
 } tt_status;
 
 /* Largest supported row lengths (elements). */
-#define TT_MAX_SOFTMAX_COLS 32768
+#define TT_MAX_SOFTMAX_COLS 131072
 #define TT_MAX_LN_HIDDEN 32768
 
 /* ------------------------------------------------------------------------

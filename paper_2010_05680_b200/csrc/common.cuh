@@ -74,6 +74,27 @@ inline cudaError_t launch_k(void (*kern)(P...), dim3 grid, dim3 block, size_t sm
     return cudaLaunchKernelEx(&cfg, kern, std::forward<A>(args)...);
 }
 
+// The same, as thread-block clusters of cluster_x CTAs along x.
+template <typename... P, typename... A>
+inline cudaError_t launch_kc(void (*kern)(P...), dim3 grid, dim3 block, size_t smem,
+                             cudaStream_t st, unsigned cluster_x, A&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = cluster_x;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl_enabled() ? 2 : 1;
+    return cudaLaunchKernelEx(&cfg, kern, std::forward<A>(args)...);
+}
+
 // ----------------------------------------------------------------------------
 // Raw vectors of VB bytes (VB in {2, 4, 8, 16, 32}); 32-byte accesses compile
 // to LDG.E.256 / STG.E.256 on sm_100a.

@@ -11,7 +11,9 @@
 //   SM-5  y_j = e_j / s for j < L, +0.0 for L <= j < Sk; RNE narrow; vector store
 // Every element is read at most once and written exactly once: the row lives
 // in registers between the load and the store, so no smem staging or online
-// (m, s) rescaling is needed up to TT_MAX_SOFTMAX_COLS (CTA tier).
+// (m, s) rescaling is needed up to one CTA's capacity (16 384 keys); longer
+// rows (up to TT_MAX_SOFTMAX_COLS) are split over a thread-block cluster that
+// merges its CTAs' (max, sum) pairs through distributed shared memory.
 //
 // Rows of any length: a row starts at an arbitrary element offset, so each row
 // is split into an unaligned head (< VE elements, scalar), an aligned body of
@@ -161,6 +163,24 @@ cudaError_t launch_softmax_warp(void* scores, const int32_t* lengths, int64_t nr
     return cudaGetLastError();
 }
 
+// Rows longer than one CTA's registers hold: a cluster of ceil(Sk / W) CTAs
+// per row (softmax_cluster_kernel), W = NT * NV * VE keys per CTA, <= 8 CTAs
+// (portable cluster size).
+template <typename T, int VB, int NV, int NT>
+cudaError_t launch_softmax_cluster(void* scores, const int32_t* lengths, int64_t nrows,
+                                   int64_t rpb, int Sk, float scale, cudaStream_t st) {
+    constexpr int W = NT * NV * (VB / (int)sizeof(T));
+    const int ncl = (Sk + W - 1) / W;
+    if (ncl < 1 || ncl > 8) return cudaErrorInvalidConfiguration;
+    const int64_t grid = nrows * ncl;
+    if (grid > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
+    const cudaError_t le = launch_kc(softmax_cluster_kernel<T, VB, NV, NT>, (unsigned)grid, NT, 0,
+                                     st, (unsigned)ncl, static_cast<T*>(scores), lengths, rpb, Sk,
+                                     scale * kLog2e);
+    if (le != cudaSuccess) return le;
+    return cudaGetLastError();
+}
+
 using SoftmaxFn = cudaError_t (*)(void*, const int32_t*, int64_t, int64_t, int, float,
                                   cudaStream_t);
 
@@ -176,6 +196,13 @@ struct SoftmaxTier {
         (G) * (NV) * ((VB) / (int)sizeof(T)), AUTO,                                        \
             &launch_softmax<T, VB, G, NV, R, NT, MINB>,                                    \
             "softmax_rows<" TN ",V" #VB ",G" #G ",NV" #NV ",R" #R ",T" #NT ",M" #MINB ">" \
+    }
+
+#define TT_SM_CLUSTER(AUTO, T, TN, VB, NV, NT)                                             \
+    SoftmaxTier {                                                                          \
+        8 * (NT) * (NV) * ((VB) / (int)sizeof(T)), AUTO,                                   \
+            &launch_softmax_cluster<T, VB, NV, NT>,                                        \
+            "softmax_cluster<" TN ",V" #VB ",NV" #NV ",T" #NT ",C8>"                        \
     }
 
 #define TT_SM_WARP_R(AUTO, T, TN, VB, G, NV, NT, MINB, RPG)                               \
@@ -214,7 +241,7 @@ struct SoftmaxTier {
     TT_SM_WARP(true, T, TN, 32, 32, 3, 256, M3), TT_SM_WARP(true, T, TN, 32, 32, 4, 256, M4),   \
     TT_SM_TIER(true, T, TN, 32, 64, NVC, 1, 64, 1), TT_SM_TIER(true, T, TN, 32, 128, NVC, 1, 128, 1), \
     TT_SM_TIER(true, T, TN, 32, 256, NVC, 1, 256, 1), TT_SM_TIER(true, T, TN, 32, 512, NVC, 1, 512, 1), \
-    TT_SM_TIER(true, T, TN, 32, 1024, NVC, 1, 1024, 1),                                     \
+    TT_SM_CLUSTER(true, T, TN, 32, NVC, 512),                                               \
     /* selected through the preference table kSmPref */                                      \
     TT_SM_WARP(false, T, TN, 16, 8, 2, 256, 6), TT_SM_WARP_F(false, T, TN, 16, 8, 4, 256, 3, 4), \
     TT_SM_WARP_R(false, T, TN, 32, 32, 1, 256, 6, 2), TT_SM_WARP_R(false, T, TN, 32, 32, 2, 256, 3, 2), \

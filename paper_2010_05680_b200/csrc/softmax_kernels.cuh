@@ -487,4 +487,152 @@ __global__ void __launch_bounds__(NW * 32) softmax_tma_kernel(T* __restrict__ sc
     }
 }
 
+// ----------------------------------------------------------------------------
+// Cluster tier (rows longer than one CTA holds in registers; north_star "rows
+// are mapped to warps or clusters by length"): the row is cut into segments of
+// W = NT * NV * VE keys, one per CTA of a thread-block cluster of ceil(Sk / W)
+// CTAs (<= 8, portable).  Each CTA keeps its segment in registers (SM-2),
+// takes its local max m_c and local sum s_c = sum 2^(t - m_c) (SM-3 / SM-4),
+// and publishes (m_c, s_c) in its shared memory; after one cluster barrier
+// every CTA reads all partners' pairs through distributed shared memory and
+// merges them, (M, S) = (max m_c, sum s_c 2^(m_c - M)) -- the (m, s) merge of
+// then writes y = e 2^(m_c - M) / S (SM-5).  Every key is
+// read from HBM once and written once; a second cluster barrier keeps each
+// CTA's shared memory alive until its partners have read it.
+// t = x * c is computed explicitly (c = scale * log2 e, either sign).
+// ----------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ uint32_t cluster_nctarank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n"
+                 "barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// float at the same shared-memory offset in CTA `rank` of this cluster
+__device__ __forceinline__ float ld_dsmem_f32(const float* local, uint32_t rank) {
+    uint32_t remote;
+    float v;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(local)), "r"(rank));
+    asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(remote) : "memory");
+    return v;
+}
+
+template <typename T, int VB, int NV, int NT>
+__global__ void __launch_bounds__(NT, 1) softmax_cluster_kernel(T* __restrict__ scores,
+                                                                const int32_t* __restrict__ lengths,
+                                                                int64_t rows_per_batch, int Sk,
+                                                                float c) {
+    PdlScope pdl_;  // griddepcontrol.wait first: no global access before it (PDL)
+    constexpr int VE = VB / (int)sizeof(T);
+    constexpr int W = NT * NV * VE;          // keys per CTA segment
+    constexpr int HI = (VE - 1 + NT - 1) / NT;
+    constexpr int NW = NT / 32;
+    __shared__ float red_m[NW], red_s[NW];
+    __shared__ float part[2];                // this CTA's (m_c, s_c), read by the cluster
+
+    const uint32_t cr = cluster_ctarank(), ncl = cluster_nctarank();
+    const int64_t row = (int64_t)(blockIdx.x / ncl);
+    const int q = threadIdx.x;
+    const int seg0 = (int)cr * W;
+    const int Sks = min(W, Sk - seg0);       // keys in this segment (>= 1)
+    T* p = scores + row * (int64_t)Sk + seg0;
+    const int L = min(max(__ldg(lengths + row / rows_per_batch), 0), Sk);
+    const int Ls = min(max(L - seg0, 0), Sks);  // valid keys in this segment
+    const int mis = (int)((reinterpret_cast<uintptr_t>(p) & (VB - 1)) / sizeof(T));
+    const int hd = mis ? min(VE - mis, Sks) : 0;
+    const int nv = (Sks - hd) / VE;
+    const int tl0 = hd + nv * VE;
+
+    // ---- SM-2: the valid prefix of this segment, t = x * c (log2 domain)
+    float v[NV][VE], hv[HI], tv[HI];
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+        const int vi = q + k * NT;
+        const int j0 = hd + vi * VE;
+        if (vi < nv && j0 < Ls) {
+            Raw<VB> w;
+            ld_stream<VB>(p + j0, w);
+            Elem<T>::template unpack<VB>(w, v[k]);
+#pragma unroll
+            for (int e = 0; e < VE; ++e) v[k][e] = (j0 + e < Ls) ? v[k][e] * c : -INFINITY;
+        } else {
+#pragma unroll
+            for (int e = 0; e < VE; ++e) v[k][e] = -INFINITY;
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < HI; ++i) {
+        const int jh = q + i * NT, jt = tl0 + q + i * NT;
+        hv[i] = (jh < hd && jh < Ls) ? Elem<T>::to_f(p[jh]) * c : -INFINITY;
+        tv[i] = (jt < Sks && jt < Ls) ? Elem<T>::to_f(p[jt]) * c : -INFINITY;
+    }
+    // ---- SM-3: local max m_c
+    float m[1] = {-INFINITY};
+#pragma unroll
+    for (int k = 0; k < NV; ++k)
+#pragma unroll
+        for (int e = 0; e < VE; ++e) m[0] = fmaxf(m[0], v[k][e]);
+#pragma unroll
+    for (int i = 0; i < HI; ++i) m[0] = fmaxf(m[0], fmaxf(hv[i], tv[i]));
+    group_max<NT, 1>(m, red_m);
+    const float mc = m[0];
+    const float mm = mc == -INFINITY ? 0.f : mc;  // empty segment: e = 0 everywhere
+    // ---- SM-4: e = 2^(t - m_c) once, local sum s_c
+    float s[1] = {0.f};
+#pragma unroll
+    for (int k = 0; k < NV; ++k)
+#pragma unroll
+        for (int e = 0; e < VE; ++e) {
+            v[k][e] = ex2_approx(v[k][e] - mm);
+            s[0] += v[k][e];
+        }
+#pragma unroll
+    for (int i = 0; i < HI; ++i) {
+        hv[i] = ex2_approx(hv[i] - mm);
+        tv[i] = ex2_approx(tv[i] - mm);
+        s[0] += hv[i] + tv[i];
+    }
+    group_sum<NT, 1>(s, red_s);
+    // ---- the cluster merge: (M, S) over the segments' (m_c, s_c)
+    if (q == 0) {
+        part[0] = mc;
+        part[1] = s[0];
+    }
+    cluster_sync_all();
+    float M = -INFINITY, Sum = 0.f;
+    for (uint32_t r = 0; r < ncl; ++r) M = fmaxf(M, ld_dsmem_f32(&part[0], r));
+    for (uint32_t r = 0; r < ncl; ++r) {
+        const float mr = ld_dsmem_f32(&part[0], r);
+        if (mr != -INFINITY) Sum += ld_dsmem_f32(&part[1], r) * ex2_approx(mr - M);
+    }
+    cluster_sync_all();  // partners are done reading this CTA's `part`
+    // ---- SM-5: y = e 2^(m_c - M) / S; +0.0 past L (e = 0 there); L = 0: all zero
+    const float f = (L > 0 && mc != -INFINITY) ? ex2_approx(mc - M) / Sum : 0.f;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+        const int vi = q + k * NT;
+        if (vi < nv) {
+            float y[VE];
+#pragma unroll
+            for (int e = 0; e < VE; ++e) y[e] = v[k][e] * f;
+            Raw<VB> w;
+            Elem<T>::template pack<VB>(y, w);
+            st_stream<VB>(p + hd + vi * VE, w);
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < HI; ++i) {
+        const int jh = q + i * NT, jt = tl0 + q + i * NT;
+        if (jh < hd) p[jh] = Elem<T>::from_f(hv[i] * f);
+        if (jt < Sks) p[jt] = Elem<T>::from_f(tv[i] * f);
+    }
+}
+
 }  // namespace tt

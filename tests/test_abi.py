@@ -124,7 +124,9 @@ def test_launch_without_device_fails_loudly(ttlib):
     (torch.float16, 491, "softmax_warp<f16,V32,G32,NV1,T256,M6,P2>"),
     (torch.float32, 500, "softmax_warp<f32,V32,G32,NV2,T256,M3,P2>"),
     (torch.float32, 4096, "softmax_rows<f32,V32,G128,NV4,R1,T128,M1>"),
-    (torch.bfloat16, 32768, "softmax_rows<bf16,V32,G1024,NV2,R1,T1024,M1>"),
+    (torch.bfloat16, 16384, "softmax_rows<bf16,V32,G512,NV2,R1,T512,M1>"),
+    (torch.bfloat16, 16385, "softmax_cluster<bf16,V32,NV2,T512,C8>"),
+    (torch.float32, 131072, "softmax_cluster<f32,V32,NV4,T512,C8>"),
 ])
 def test_softmax_tier_plan(ttlib, dtype, Sk, tier):
     assert ttlib.softmax_plan(dtype, 2, 12, 3, Sk) == tier

@@ -12,6 +12,7 @@ import torch
 
 import oracle
 import workloads as W
+import workloads as W_
 from _parity import assert_close, masked_bits_zero, softmax_all_rows
 
 pytestmark = pytest.mark.gpu
@@ -144,7 +145,8 @@ def test_every_row_length_1_to_160(ttlib, dtype):
 
 @pytest.mark.parametrize("dtype", DT)
 @pytest.mark.parametrize("Sk", [255, 256, 257, 511, 513, 767, 1000, 1023, 1024, 1025, 2047, 2048,
-                                2049, 4095, 4096, 4099, 8192, 16384, 32768])
+                                2049, 4095, 4096, 4099, 8192, 16384, 16385, 32768, 32771,
+                                65536, 100003, 131072])
 def test_long_rows_and_tier_boundaries(ttlib, dtype, Sk):
     lens = [Sk, Sk - 1, 1, Sk // 3]
     x = W.scores(4, 1, 2, Sk, dtype, seed=Sk + 7)
@@ -307,3 +309,19 @@ def test_every_compiled_tier(ttlib, dtype):
                 _full_check(ttlib, x, lens, W.SCALE_BERT, f"{name} Sk={Sk}")
     finally:
         ttlib.force_tier("softmax", dtype, -1)
+
+
+@pytest.mark.parametrize("dtype", DT)
+def test_cluster_tier_segments_and_masks(ttlib, dtype):
+    """Rows split over a thread-block cluster (softmax_cluster: one 16 384-key
+    segment per CTA, (max, sum) merged through distributed shared memory):
+    valid lengths ending inside each segment, on a segment boundary, in the
+    first segment only (later CTAs hold only padding), 0 and 1; odd pitch so
+    segments start unaligned; poison in the padding; negative scale."""
+    W = 16384
+    Sk = 3 * W + 5
+    lens = [Sk, 1, 0, W, W + 1, 2 * W - 3, 3 * W, Sk - 1, 17]
+    x = W_.scores(len(lens), 1, 1, Sk, dtype, seed=5)
+    assert ttlib.softmax_plan(dtype, len(lens), 1, 1, Sk).startswith("softmax_cluster<")
+    _full_check(ttlib, x, lens, W_.SCALE_BERT, "cluster")
+    _full_check(ttlib, W_.poison_masked(x, lens), lens, -0.25, "cluster poison")
