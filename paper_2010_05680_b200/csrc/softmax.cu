@@ -147,8 +147,16 @@ cudaError_t launch_softmax_warp(void* scores, const int32_t* lengths, int64_t nr
         const int64_t need = (nrows + spread - 1) / spread;
         if (need < rpg) rpg = need > 0 ? (int)need : 1;
     }
+    // requests of very few rows (far fewer than a CTA's groups): the CTA-tier
+    // kernel, which looks each row's length up itself
+    if (rpb * 4 < GPB)
+        return launch_softmax<T, VB, G, NV, 1, NT, 1>(scores, lengths, nrows, rpb, Sk, scale, st);
+    if ((int64_t)GPB * rpg > rpb) rpg = (int)((rpb + GPB - 1) / GPB);
+    // cpr CTAs per request, each within one request (softmax_warp_body)
     const int64_t per_cta = (int64_t)GPB * rpg;
-    const int64_t grid = (nrows + per_cta - 1) / per_cta;
+    const int64_t cpr = (rpb + per_cta - 1) / per_cta;
+    const int64_t grid = (nrows / rpb) * cpr;
+    if (grid > 0x7fffffffLL || cpr > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
     // c = 0 (scale 0: uniform softmax) is mapped to a tiny positive c so the
     // masked-key sentinel still exponentiates to exactly +0.0; for finite x,
     // 2^(x * 1e-30 - m * 1e-30) rounds to exactly 1.0f.
@@ -156,8 +164,8 @@ cudaError_t launch_softmax_warp(void* scores, const int32_t* lengths, int64_t nr
     if (c == 0.f) c = 1e-30f;
     {
         const cudaError_t le_ = launch_k(kern, (unsigned)grid, NT, 0, st,
-            static_cast<T*>(scores), lengths, (uint32_t)nrows,
-                                       FastDivU32::make((uint32_t)rpb), Sk, c, rpg);
+            static_cast<T*>(scores), lengths, FastDivU32::make((uint32_t)cpr), (uint32_t)rpb, Sk,
+            c, rpg);
         if (le_ != cudaSuccess) return le_;
     }
     return cudaGetLastError();

@@ -172,54 +172,49 @@ __global__ void __launch_bounds__(NT, MINB) softmax_rows_kernel(T* __restrict__ 
 //   * ALIGNED (row pitch and base are multiples of VB) drops the scalar head /
 //     tail code entirely.
 // ----------------------------------------------------------------------------
-// Rows [first, row_end) of this CTA, GC lanes per row, walked in warp-uniform
-// slabs (every lane of a warp runs the same number of passes).
+// Rows [first, row_end) of this CTA -- all of ONE request, so one valid
+// length L -- GC lanes per row, walked in warp-uniform slabs (every lane of a
+// warp runs the same number of passes).
 // PF: cross-row prefetch -- the loads of a group's next row are issued
 // before the current row is computed, so each warp keeps two rows in flight
 // (for rows under ~1 KB one row per warp is too few bytes in flight per SM).
 template <typename T, int VB, int GC, int NVC, int NT, bool ALIGNED, bool NARROW, bool UP,
           bool PF = false, bool EF = false>
-__device__ __forceinline__ void softmax_cta_rows(T* __restrict__ scores,
-                                                 const int32_t* __restrict__ lengths,
-                                                 uint32_t first, uint32_t row_end, FastDivU32 rpb,
-                                                 int Sk, float c, bool one_req, int Lcta) {
+__device__ __forceinline__ void softmax_cta_rows(T* __restrict__ scores, uint32_t first,
+                                                 uint32_t row_end, int Sk, float c, int L) {
     constexpr int GPW = 32 / GC;  // rows per warp per pass
     const int lane = threadIdx.x & 31;
     const int q = lane % GC;
     const uint32_t step = (NT / 32) * GPW;
-    auto len_of = [&](uint32_t r) { return min(max(__ldg(lengths + rpb.div(r)), 0), Sk); };
     uint32_t row = first + (threadIdx.x >> 5) * GPW + lane / GC;
     if constexpr (PF) {
         using RR = RowRaw<T, VB, GC, NVC, ALIGNED>;
         uint32_t base = first + (threadIdx.x >> 5) * GPW;
         if (base >= row_end) return;  // warp-uniform
         bool live = row < row_end;
-        int L = live ? (one_req ? Lcta : len_of(row)) : 0;
         T* pc = scores + (size_t)(live ? row : first) * (size_t)Sk;
         RR cur;
-        row_load<T, VB, GC, NVC, ALIGNED>(pc, L, Sk, q, cur);
+        row_load<T, VB, GC, NVC, ALIGNED>(pc, live ? L : 0, Sk, q, cur);
         for (; base < row_end; base += step, row += step) {
             const uint32_t rn = row + step;
             const bool ln = rn < row_end;
-            const int Ln = ln ? (one_req ? Lcta : len_of(rn)) : 0;
             T* pn = scores + (size_t)(ln ? rn : first) * (size_t)Sk;
             RR nxt;
             if (base + step < row_end)  // warp-uniform: another pass follows
-                row_load<T, VB, GC, NVC, ALIGNED>(pn, Ln, Sk, q, nxt);
-            row_finish<T, VB, GC, NVC, ALIGNED, NARROW, UP, EF>(pc, live, L, Sk, c, q, cur);
+                row_load<T, VB, GC, NVC, ALIGNED>(pn, ln ? L : 0, Sk, q, nxt);
+            row_finish<T, VB, GC, NVC, ALIGNED, NARROW, UP, EF>(pc, live, live ? L : 0, Sk, c, q,
+                                                               cur);
             cur = nxt;
             pc = pn;
-            L = Ln;
             live = ln;
         }
         return;
     }
-    int Lnext = one_req ? Lcta : (row < row_end ? len_of(row) : 0);
     for (uint32_t base = first + (threadIdx.x >> 5) * GPW; base < row_end; base += step, row += step) {
         const bool live = row < row_end;
-        const int L = Lnext;
-        if (!one_req && row + step < row_end) Lnext = len_of(row + step);
-        T* p = scores + (size_t)(live ? row : first) * (size_t)Sk;
+        // a dead slot re-reads the range's last row (any row of the range is a
+        // valid address; `first` is then not needed inside the loop)
+        T* p = scores + (size_t)(live ? row : row_end - 1) * (size_t)Sk;
         const int Lr = live ? L : 0;
         RowRaw<T, VB, GC, NVC, ALIGNED> rr;
         row_load<T, VB, GC, NVC, ALIGNED>(p, Lr, Sk, q, rr);
@@ -230,53 +225,44 @@ __device__ __forceinline__ void softmax_cta_rows(T* __restrict__ scores,
 // Rows of one request with L <= G * K * VE on a tier of NV > K vectors per lane:
 // run them with K vectors per lane (K = 1 .. NV-1, smallest that fits).
 template <typename T, int VB, int G, int K, int NV, int NT, bool ALIGNED, bool UP, bool PF, bool EF>
-__device__ __forceinline__ bool softmax_narrow_nv(T* __restrict__ scores,
-                                                  const int32_t* __restrict__ lengths,
-                                                  uint32_t first, uint32_t row_end, FastDivU32 rpb,
-                                                  int Sk, float c, int Lcta) {
+__device__ __forceinline__ bool softmax_narrow_nv(T* __restrict__ scores, uint32_t first,
+                                                  uint32_t row_end, int Sk, float c, int L) {
     if constexpr (K >= NV) {
         return false;
     } else {
         constexpr int VE = VB / (int)sizeof(T);
-        if (Lcta <= G * K * VE) {
-            softmax_cta_rows<T, VB, G, K, NT, ALIGNED, true, UP, PF, EF>(
-                scores, lengths, first, row_end, rpb, Sk, c, true, Lcta);
+        if (L <= G * K * VE) {
+            softmax_cta_rows<T, VB, G, K, NT, ALIGNED, true, UP, PF, EF>(scores, first, row_end,
+                                                                          Sk, c, L);
             return true;
         }
-        return softmax_narrow_nv<T, VB, G, K + 1, NV, NT, ALIGNED, UP, PF, EF>(
-            scores, lengths, first, row_end, rpb, Sk, c, Lcta);
+        return softmax_narrow_nv<T, VB, G, K + 1, NV, NT, ALIGNED, UP, PF, EF>(scores, first,
+                                                                               row_end, Sk, c, L);
     }
 }
 
+// One request segment [first, row_end), valid length L: the tier's full path,
+// or a narrower one when L is short.
 template <typename T, int VB, int G, int NV, int NT, bool ALIGNED, bool UP, bool PF, bool EF>
-__device__ __forceinline__ void softmax_warp_body(T* __restrict__ scores,
-                                                  const int32_t* __restrict__ lengths,
-                                                  uint32_t nrows, FastDivU32 rpb, int Sk, float c,
-                                                  int rpg) {
+__device__ __forceinline__ void softmax_segment(T* __restrict__ scores, uint32_t first,
+                                                uint32_t row_end, int Sk, float c, int L) {
     constexpr int VE = VB / (int)sizeof(T);
-    constexpr int GPB = NT / G;
-    static_assert(G <= 32, "warp tier");
-    const uint32_t first = blockIdx.x * (uint32_t)(GPB * rpg);
-    const uint32_t row_end = min(nrows, first + (uint32_t)(GPB * rpg));
-    // one request for the whole CTA?  (uniform; rpb = H * Sq rows per request)
-    const bool one_req = rpb.div(first) == rpb.div(row_end - 1);
-    const int Lcta = one_req ? min(max(__ldg(lengths + rpb.div(first)), 0), Sk) : 0;
     if constexpr (G == 32 && NV == 1) {
         // short request: compute on narrower groups (more rows per warp pass)
         // and zero-fill the padding vectors
         // (unaligned rows: only widths whose scalar head / tail fit one pass,
         // GC >= VE - 1, so the narrow paths do not raise register pressure)
         constexpr bool ok4 = ALIGNED || 4 >= VE - 1, ok8 = ALIGNED || 8 >= VE - 1;
-        if (one_req && Lcta < Sk) {
-            if (ok4 && Lcta <= 4 * VE)
+        if (L < Sk) {
+            if (ok4 && L <= 4 * VE)
                 return softmax_cta_rows<T, VB, 4, 1, NT, ALIGNED, ok4, UP, PF, EF>(
-                    scores, lengths, first, row_end, rpb, Sk, c, true, Lcta);
-            if (ok8 && Lcta <= 8 * VE)
+                    scores, first, row_end, Sk, c, L);
+            if (ok8 && L <= 8 * VE)
                 return softmax_cta_rows<T, VB, 8, 1, NT, ALIGNED, ok8, UP, PF, EF>(
-                    scores, lengths, first, row_end, rpb, Sk, c, true, Lcta);
-            if (Lcta <= 16 * VE)
+                    scores, first, row_end, Sk, c, L);
+            if (L <= 16 * VE)
                 return softmax_cta_rows<T, VB, 16, 1, NT, ALIGNED, true, UP, PF, EF>(
-                    scores, lengths, first, row_end, rpb, Sk, c, true, Lcta);
+                    scores, first, row_end, Sk, c, L);
         }
     }
     // (not compiled into the G8 x NV5 tier: there the extra paths made ptxas
@@ -285,28 +271,46 @@ __device__ __forceinline__ void softmax_warp_body(T* __restrict__ scores,
         // short request on a multi-vector tier: the fewest vectors per lane that
         // hold its valid keys; the padding vectors are zero-filled without
         // arithmetic (NARROW), so a row's cost follows L_b instead of Sk
-        if (one_req && Lcta < Sk) {
-            if (softmax_narrow_nv<T, VB, G, 1, NV, NT, ALIGNED, UP, PF, EF>(
-                    scores, lengths, first, row_end, rpb, Sk, c, Lcta))
+        if (L < Sk) {
+            if (softmax_narrow_nv<T, VB, G, 1, NV, NT, ALIGNED, UP, PF, EF>(scores, first, row_end,
+                                                                            Sk, c, L))
                 return;
         }
     }
-    softmax_cta_rows<T, VB, G, NV, NT, ALIGNED, false, UP, PF, EF>(scores, lengths, first, row_end,
-                                                               rpb, Sk, c, one_req, Lcta);
+    softmax_cta_rows<T, VB, G, NV, NT, ALIGNED, false, UP, PF, EF>(scores, first, row_end, Sk, c, L);
+}
+
+// CTA b owns rows [first, row_end) of ONE request: the grid is laid out as
+// `cpr` CTAs per request (cpr = ceil(rows_per_request / rows_per_cta)), so the
+// request -- and its valid length, loaded once -- is known per CTA and no
+// per-row length lookup, division or test exists in the row loop.
+template <typename T, int VB, int G, int NV, int NT, bool ALIGNED, bool UP, bool PF, bool EF>
+__device__ __forceinline__ void softmax_warp_body(T* __restrict__ scores,
+                                                  const int32_t* __restrict__ lengths,
+                                                  FastDivU32 cpr, uint32_t rpb, int Sk, float c,
+                                                  int rpg) {
+    constexpr int GPB = NT / G;
+    static_assert(G <= 32, "warp tier");
+    const uint32_t per_cta = (uint32_t)(GPB * rpg);
+    const uint32_t req = cpr.div(blockIdx.x);
+    const uint32_t first = req * rpb + (blockIdx.x - req * cpr.d) * per_cta;
+    const uint32_t row_end = min(first + per_cta, (req + 1) * rpb);
+    const int L = min(max(__ldg(lengths + req), 0), Sk);
+    softmax_segment<T, VB, G, NV, NT, ALIGNED, UP, PF, EF>(scores, first, row_end, Sk, c, L);
 }
 
 template <typename T, int VB, int G, int NV, int NT, int MINB, bool ALIGNED, bool PF, bool EF>
 __global__ void __launch_bounds__(NT, MINB) softmax_warp_kernel(T* __restrict__ scores,
                                                                 const int32_t* __restrict__ lengths,
-                                                                uint32_t nrows, FastDivU32 rpb,
+                                                                FastDivU32 cpr, uint32_t rpb,
                                                                 int Sk, float c, int rpg) {
     PdlScope pdl_;  // griddepcontrol.wait first: no global access before it (PDL)
     if (c > 0.f)  // uniform: the sign of the scale picks the max or min reduction
-        softmax_warp_body<T, VB, G, NV, NT, ALIGNED, true, PF, EF>(scores, lengths, nrows, rpb, Sk, c,
+        softmax_warp_body<T, VB, G, NV, NT, ALIGNED, true, PF, EF>(scores, lengths, cpr, rpb, Sk, c,
                                                                rpg);
     else
-        softmax_warp_body<T, VB, G, NV, NT, ALIGNED, false, PF, EF>(scores, lengths, nrows, rpb, Sk, c,
-                                                                rpg);
+        softmax_warp_body<T, VB, G, NV, NT, ALIGNED, false, PF, EF>(scores, lengths, cpr, rpb, Sk,
+                                                                c, rpg);
 }
 
 // ----------------------------------------------------------------------------

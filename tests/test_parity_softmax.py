@@ -139,8 +139,11 @@ def test_every_row_length_1_to_160(ttlib, dtype):
     for Sk in range(1, 161):
         B = 3
         lens = [Sk, max(Sk // 2, 1), 0]
-        x = W.scores(B, 2, 3, Sk, dtype, seed=Sk)
-        _full_check(ttlib, x, lens, W.SCALE_BERT, f"Sk={Sk}")
+        # 6 rows per request (requests far smaller than a CTA: per-row lengths)
+        # and 64 rows per request (the warp tiers' one-request CTAs)
+        for H, Sq in ((2, 3), (4, 16)):
+            x = W.scores(B, H, Sq, Sk, dtype, seed=Sk)
+            _full_check(ttlib, x, lens, W.SCALE_BERT, f"Sk={Sk} H={H} Sq={Sq}")
 
 
 @pytest.mark.parametrize("dtype", DT)

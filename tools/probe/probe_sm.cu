@@ -7,5 +7,5 @@ namespace tt {
 bool pdl_enabled() { return true; }
 cudaError_t smem_optin(const void*, size_t) { return cudaSuccess; }
 template __global__ void softmax_warp_kernel<PT, PVB, PG, PNV, 256, PMINB, (bool)PAL, false, false>(
-    PT*, const int32_t*, uint32_t, FastDivU32, int, float, int);
+    PT*, const int32_t*, FastDivU32, uint32_t, int, float, int);
 }  // namespace tt
