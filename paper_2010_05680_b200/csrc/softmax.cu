@@ -120,7 +120,10 @@ cudaError_t launch_softmax_warp(void* scores, const int32_t* lengths, int64_t nr
     const bool lines = aligned && (reinterpret_cast<uintptr_t>(scores) % 128) == 0 &&
                        ((int64_t)Sk * (int64_t)sizeof(T)) % 128 == 0;
     const int kv = lines ? 2 : aligned ? 1 : 0;
-    auto kern = lines     ? softmax_warp_kernel<T, VB, G, NV, NT, MINB, true, PF, true>
+    // (evict_first stores compiled for every tier but the 16-bit G8 x NV5 one, where the
+    // extra policy register made ptxas spill; there whole-line rows store plainly)
+    constexpr bool kEF = !(sizeof(T) == 2 && G == 8 && NV == 5);
+    auto kern = lines     ? softmax_warp_kernel<T, VB, G, NV, NT, MINB, true, PF, kEF>
                 : aligned ? softmax_warp_kernel<T, VB, G, NV, NT, MINB, true, PF, false>
                           : softmax_warp_kernel<T, VB, G, NV, NT,
                                                 sm_minb_unaligned<T, VB, G, NV, MINB>(), false, PF,

@@ -265,9 +265,7 @@ __device__ __forceinline__ void softmax_segment(T* __restrict__ scores, uint32_t
                     scores, first, row_end, Sk, c, L);
         }
     }
-    // (not compiled into the G8 x NV5 tier: there the extra paths made ptxas
-    // spill the main path, -2.5 % on full fp16 S = 300 rows)
-    if constexpr (NV > 1 && !(G == 8 && NV == 5)) {
+    if constexpr (NV > 1) {
         // short request on a multi-vector tier: the fewest vectors per lane that
         // hold its valid keys; the padding vectors are zero-filled without
         // arithmetic (NARROW), so a row's cost follows L_b instead of Sk
