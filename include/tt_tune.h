@@ -37,12 +37,13 @@ TT_API tt_status ttx_force_tier(int op, int dtype, int i);
  * P.V only after the exponentials, 9 = warp-specialised: two 128-row query tiles
  * per CTA sharing K / V loaded by TMA, a producer warp, an MMA warp and two
  * ping-ponging softmax warpgroups, P kept in TMEM (attention_fa.cu), 128-key
- * tiles; 10 = the same with 64-key tiles and two S buffers per query tile.
- * Variants 1..10 are compiled into the tuning build only (ttx_tuning_build);
+ * tiles; 10 = the same with 64-key tiles and two S buffers per query tile;
+ * 11 = variant 4 with Q / K / V loaded by TMA tensor copies on mbarriers.
+ * Variants 1..11 are compiled into the tuning build only (ttx_tuning_build);
  * TT_ERROR_INVALID_VALUE for a variant not compiled in (ttx_attention_variant_ok). */
 TT_API tt_status ttx_attention_variant(int v);
 /* Variant ids are 0 .. ttx_attention_variant_count() - 1; ttx_attention_variant_ok
- * says whether variant v is compiled into this library (0 always; 1..10
+ * says whether variant v is compiled into this library (0 always; 1..11
  * in the tuning build only). */
 TT_API int ttx_attention_variant_count(void);
 TT_API int ttx_attention_variant_ok(int v);

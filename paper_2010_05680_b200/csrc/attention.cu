@@ -83,9 +83,16 @@ constexpr int attn_tmem_cols() {
     return BN + kD <= 128 ? 128 : 256;
 }
 
-template <typename T, int NBUF, int BN, bool UP, bool LATE = false>
+// TMA (NBUF = 2 only): Q, K and V arrive by cp.async.bulk.tensor.3d (tensor maps
+// over [B*H, S, 64], SWIZZLE_128B) issued by one thread and completing on
+// mbarriers, instead of 16-byte cp.async by every thread; V rows of keys >= L
+// in the last partial tile are zeroed in shared memory before the P.V MMA.
+template <typename T, int NBUF, int BN, bool UP, bool LATE = false, bool TMA = false>
 __global__ void __launch_bounds__(kNT, attn_minb<NBUF, BN>())
-    attention_tc_kernel(T* __restrict__ out, const T* __restrict__ q, const T* __restrict__ k,
+    attention_tc_kernel(const __grid_constant__ CUtensorMap tq,
+                        const __grid_constant__ CUtensorMap tk,
+                        const __grid_constant__ CUtensorMap tv, T* __restrict__ out,
+                        const T* __restrict__ q, const T* __restrict__ k,
                         const T* __restrict__ v, const int32_t* __restrict__ lengths, int H,
                         int S, float c) {
     PdlScope pdl_;  // griddepcontrol.wait first: no global access before it (PDL)
@@ -96,8 +103,9 @@ __global__ void __launch_bounds__(kNT, attn_minb<NBUF, BN>())
     unsigned char* sbase = smem_raw + (base - smem_u32(smem_raw));
     const uint32_t sQ = base, sK = base + kTile, sV = base + kTile + NBUF * kKV,
                    sP = base + kTile + 2 * NBUF * kKV;
+    // bars: [0] S done, [1] P.V done, [2] Q (+ K0, V0) landed, [3..4] K(b), [5..6] V(b)
     uint64_t* bars = reinterpret_cast<uint64_t*>(sbase + kTile + 2 * NBUF * kKV + BN * 256);
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sbase + kTile + 2 * NBUF * kKV + BN * 256 + 16);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sbase + kTile + 2 * NBUF * kKV + BN * 256 + 56);
 
     const int qt = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
     const int tid = threadIdx.x, warp = tid >> 5;
@@ -122,18 +130,40 @@ __global__ void __launch_bounds__(kNT, attn_minb<NBUF, BN>())
                      : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
+    const int nkt = (L + BN - 1) / BN;
+    const int bh = b * H + h;
+    // TMA: K(t) into buffer t & 1 on bars[3 + (t & 1)], V(t) on bars[5 + (t & 1)]
+    auto tma_k = [&](int t) {
+        mbar_arrive_expect_tx(&bars[3 + (t & 1)], (uint32_t)kKV);
+        tma_load_3d(sK + (t & 1) * kKV, &tk, &bars[3 + (t & 1)], 0, t * BN, bh);
+    };
+    auto tma_v = [&](int t) {
+        mbar_arrive_expect_tx(&bars[5 + (t & 1)], (uint32_t)kKV);
+        tma_load_3d(sV + (t & 1) * kKV, &tv, &bars[5 + (t & 1)], 0, t * BN, bh);
+    };
     if (tid == 0) {
         mbar_init(&bars[0], 1);
         mbar_init(&bars[1], 1);
+        if constexpr (TMA) {
+            for (int i = 2; i < 7; ++i) mbar_init(&bars[i], 1);
+        }
         fence_mbar_init();
+        if constexpr (TMA) {
+            mbar_arrive_expect_tx(&bars[2], (uint32_t)kTile);
+            tma_load_3d(sQ, &tq, &bars[2], 0, qt * kBM, bh);
+            tma_k(0);
+            tma_v(0);
+            if (nkt > 1) tma_k(1);
+        }
     }
-    const int nkt = (L + BN - 1) / BN;
-    load_tile<T>(sQ, q + head, qt * kBM, S);
-    load_tile<T, BN>(sK, k + head, 0, L);
-    load_tile<T, BN>(sV, v + head, 0, L);
-    cp_async_commit();
-    if (NBUF == 2 && nkt > 1) load_tile<T, BN>(sK + kKV, k + head, BN, L);  // K(1)
-    cp_async_commit();
+    if constexpr (!TMA) {
+        load_tile<T>(sQ, q + head, qt * kBM, S);
+        load_tile<T, BN>(sK, k + head, 0, L);
+        load_tile<T, BN>(sV, v + head, 0, L);
+        cp_async_commit();
+        if (NBUF == 2 && nkt > 1) load_tile<T, BN>(sK + kKV, k + head, BN, L);  // K(1)
+        cp_async_commit();
+    }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -315,7 +345,12 @@ __global__ void __launch_bounds__(kNT, attn_minb<NBUF, BN>())
         // runs under the next iteration's S wait and is only waited for when its
         // buffers (P, V, O) are reused.  cp.async commit order: prologue {Q, K0,
         // V0}, {K1}; then per iteration E: {K(kt+2)}, F: {V(kt+1)}.
-        cp_async_wait<1>();  // Q, K0, V0
+        if constexpr (TMA) {
+            mbar_wait_bounded(&bars[2], 0);  // Q
+            mbar_wait_bounded(&bars[3], 0);  // K(0)
+        } else {
+            cp_async_wait<1>();  // Q, K0, V0
+        }
         sync_for_mma();
         issue_s(0);
         for (int kt = 0; kt < nkt; ++kt) {
@@ -325,16 +360,25 @@ __global__ void __launch_bounds__(kNT, attn_minb<NBUF, BN>())
             float sv[BN];
             load_s(sv);  // B
             if (kt + 1 < nkt) {  // C, D: K(kt+1) ready and S read by every warp -> S(kt+1)
-                if (kt == 0)
-                    cp_async_wait<0>();
-                else
-                    cp_async_wait<1>();
+                if constexpr (TMA) {
+                    mbar_wait_bounded(&bars[3 + ((kt + 1) & 1)], (uint32_t)((kt + 1) >> 1) & 1u);
+                } else {
+                    if (kt == 0)
+                        cp_async_wait<0>();
+                    else
+                        cp_async_wait<1>();
+                }
                 sync_for_mma();
                 issue_s(kt + 1);
             }
             // E: K(kt) buffer is free (S(kt) completed)
-            if (kt + 2 < nkt) load_tile<T, BN>(sK + (kt & 1) * kKV, k + head, (kt + 2) * BN, L);
-            cp_async_commit();
+            if constexpr (TMA) {
+                if (tid == 0 && kt + 2 < nkt) tma_k(kt + 2);
+            } else {
+                if (kt + 2 < nkt)
+                    load_tile<T, BN>(sK + (kt & 1) * kKV, k + head, (kt + 2) * BN, L);
+                cp_async_commit();
+            }
             // F: P.V(kt-1) done -> P, O and V((kt+1) & 1) are free (LATE: waited
             // for inside the softmax, after the exponentials)
             bool pv_done = kt == 0;
@@ -346,20 +390,37 @@ __global__ void __launch_bounds__(kNT, attn_minb<NBUF, BN>())
                     pv_done = true;
                 }
             };
+            auto load_v_next = [&]() {
+                if constexpr (TMA) {
+                    // (every thread has passed wait_pv: the buffer's last reader,
+                    // P.V(kt-1), has completed)
+                    if (tid == 0 && kt + 1 < nkt) tma_v(kt + 1);
+                } else {
+                    if (kt + 1 < nkt)
+                        load_tile<T, BN>(sV + ((kt + 1) & 1) * kKV, v + head, (kt + 1) * BN, L);
+                    cp_async_commit();
+                }
+            };
             if constexpr (!LATE) {
                 wait_pv();
-                if (kt + 1 < nkt)
-                    load_tile<T, BN>(sV + ((kt + 1) & 1) * kKV, v + head, (kt + 1) * BN, L);
-                cp_async_commit();
+                load_v_next();
             }
             softmax_tile(sv, kt, wait_pv);
             if constexpr (LATE) {
                 wait_pv();
-                if (kt + 1 < nkt)
-                    load_tile<T, BN>(sV + ((kt + 1) & 1) * kKV, v + head, (kt + 1) * BN, L);
-                cp_async_commit();
+                load_v_next();
             }
-            cp_async_wait<2>();  // G: V(kt) (K(kt+2), V(kt+1) may still be in flight)
+            if constexpr (TMA) {  // G: V(kt) landed; keys >= L of a partial last tile -> 0
+                mbar_wait_bounded(&bars[5 + (kt & 1)], (uint32_t)(kt >> 1) & 1u);
+                const int vrows = L - kt * BN;
+                if (vrows < BN) {
+                    unsigned char* vp = sbase + (sV + (kt & 1) * kKV - base);
+                    for (int idx = vrows * 8 + tid; idx < BN * 8; idx += kNT)
+                        *reinterpret_cast<uint4*>(vp + idx * 16) = make_uint4(0, 0, 0, 0);
+                }
+            } else {
+                cp_async_wait<2>();  // G: V(kt) (K(kt+2), V(kt+1) may still be in flight)
+            }
             sync_for_mma();
             issue_pv(kt);
         }
@@ -911,20 +972,27 @@ __global__ void __launch_bounds__(kSpNT, MINB)
 namespace {
 std::atomic<int> g_attn_nbuf{0};  // 0 = automatic (variant 4)
 
-template <typename T, int NBUF, int BN, bool LATE = false>
+template <typename T, int NBUF, int BN, bool LATE = false, bool TMA = false>
 cudaError_t launch_attn(void* out, const void* q, const void* k, const void* v,
                         const int32_t* lengths, int64_t B, int64_t H, int64_t S, float scale,
                         cudaStream_t st) {
     constexpr size_t smem = attn_smem<NBUF, BN>();
     dim3 grid((unsigned)((S + kBM - 1) / kBM), (unsigned)H, (unsigned)B);
+    CUtensorMap mq{}, mk{}, mv{};  // read only by the TMA instantiation
+    if constexpr (TMA) {
+        constexpr int dt = std::is_same<T, __half>::value ? 1 : 2;
+        if (!make_map(&mq, q, dt, B * H, S, kBM) || !make_map(&mk, k, dt, B * H, S, BN) ||
+            !make_map(&mv, v, dt, B * H, S, BN))
+            return cudaErrorNotSupported;
+    }
     // c = scale * log2(e); scale 0 -> a tiny positive c (uniform weights, as the
     // softmax kernels do), so the masked-key sentinel still maps to p = +0
     float c = scale * 1.4426950408889634f;
     if (c == 0.f) c = 1e-30f;
-    auto kern = c > 0.f ? attention_tc_kernel<T, NBUF, BN, true, LATE>
-                        : attention_tc_kernel<T, NBUF, BN, false, LATE>;
+    auto kern = c > 0.f ? attention_tc_kernel<T, NBUF, BN, true, LATE, TMA>
+                        : attention_tc_kernel<T, NBUF, BN, false, LATE, TMA>;
     {
-        const cudaError_t le_ = launch_k(kern, grid, kNT, smem, st,
+        const cudaError_t le_ = launch_k(kern, grid, kNT, smem, st, mq, mk, mv,
             static_cast<T*>(out), static_cast<const T*>(q),
                                   static_cast<const T*>(k), static_cast<const T*>(v), lengths,
                                   (int)H, (int)S, c);
@@ -996,23 +1064,27 @@ cudaError_t launch_attn_any(void* out, const void* q, const void* k, const void*
         case 7: return launch_attn_split<T, 3>(out, q, k, v, lengths, B, H, S, scale, st);
         case 8: return launch_attn<T, 2, 64, true>(out, q, k, v, lengths, B, H, S, scale, st);
 #endif
+#ifdef TT_TUNING
+        case 11: return launch_attn<T, 2, 64, false, true>(out, q, k, v, lengths, B, H, S, scale, st);
+#endif
         default: return launch_attn<T, 2, 64>(out, q, k, v, lengths, B, H, S, scale, st);
     }
 }
 }  // namespace
 
 // Variants compiled into this build: 0 (automatic = the pipelined 64-key
-// schedule) and, in the TT_TUNING build, the measured-slower schedules 1 .. 8
-// and the warp-specialised TMA / two-Q-tile ones (9, 10; attention_fa.cu).
+// schedule) and, in the TT_TUNING build, the measured-slower schedules 1 .. 8,
+// the warp-specialised TMA / two-Q-tile ones (9, 10; attention_fa.cu) and the
+// default schedule fed by TMA instead of cp.async (11: 4 % slower on C4).
 bool attention_variant_ok(int v) {
 #ifdef TT_TUNING
-    return v >= 0 && v <= 10;
+    return v >= 0 && v <= 11;
 #else
     return v == 0;
 #endif
 }
 
-int attention_variant_count() { return 11; }
+int attention_variant_count() { return 12; }
 
 bool attention_force_variant(int v) {
     if (!attention_variant_ok(v)) return false;

@@ -65,9 +65,9 @@ def test_attention_variant_hook(ttlib):
     h, ok = L.ttx_attention_variant, L.ttx_attention_variant_ok
     n = L.ttx_attention_variant_count()
     # the product library holds the automatic choice only; the tuning build
-    # (ttx_tuning_build) adds variants 1..10
-    want = set(range(11)) if ttlib.tuning_build() else {0}
-    assert n == 11 and {v for v in range(n) if ok(v)} == want
+    # (ttx_tuning_build) adds variants 1..11
+    want = set(range(12)) if ttlib.tuning_build() else {0}
+    assert n == 12 and {v for v in range(n) if ok(v)} == want
     for v in range(n):
         assert h(v) == (OK if v in want else INV)
     assert h(-1) == INV and h(n) == INV

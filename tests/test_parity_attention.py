@@ -16,7 +16,7 @@ TOL = {torch.float16: 4e-3, torch.bfloat16: 8e-3}
 
 
 _NAMES = {0: "auto", 1: "bn128", 2: "bn128x2", 3: "bn64", 4: "bn64x2", 5: "ws", 6: "split", 7: "split3",
-          8: "late", 9: "fa128", 10: "fa64"}
+          8: "late", 9: "fa128", 10: "fa64", 11: "tma"}
 
 
 def _variants():
