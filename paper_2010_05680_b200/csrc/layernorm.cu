@@ -247,7 +247,11 @@ struct LnTier {
     TT_LN_WARP(false, T, TN, 32, 32, 2, 128, 6), TT_LN_WARP(false, T, TN, 32, 32, 3, 128, 6),   \
     TT_LN_TIER(false, T, TN, 32, 32, 3, 2, 256, 1), TT_LN_TIER(false, T, TN, 32, 32, 4, 2, 256, 1), \
     TT_LN_TIER(false, T, TN, 32, 16, 3, 1, 256, 1), TT_LN_TIER(false, T, TN, 32, 16, 4, 1, 256, 1), \
-    TT_LN_TIER(false, T, TN, 16, 32, 4, 1, 256, 1), TT_LN_TIER(false, T, TN, 16, 32, 6, 1, 256, 1)
+    TT_LN_TIER(false, T, TN, 16, 32, 4, 1, 256, 1), TT_LN_TIER(false, T, TN, 16, 32, 6, 1, 256, 1), \
+    TT_LN_TIER(false, T, TN, 32, 32, 2, 2, 128, 4), TT_LN_TIER(false, T, TN, 32, 32, 2, 1, 64, 12), \
+    TT_LN_TIER(false, T, TN, 32, 32, 2, 1, 256, 3), TT_LN_TIER(false, T, TN, 16, 32, 4, 1, 128, 6), \
+    TT_LN_TIER(false, T, TN, 16, 32, 3, 2, 128, 4), TT_LN_TIER(false, T, TN, 16, 32, 3, 1, 64, 12), \
+    TT_LN_TIER(false, T, TN, 32, 32, 3, 1, 64, 10)
 
 #ifdef TT_TUNING
 #define TT_LN_ALL(T, TN, SB, NVC32, NVC16, MA, MB, MC) \
