@@ -237,22 +237,41 @@ def _units(tt, wl, rank, scaling, dev, stream):
     return units
 
 
-def _step_fn(tt, wl, units, stream):
+def _step_fn(tt, wl, units, stream, nstreams=1):
+    """One step over this rank's batches.  With several batches and nstreams > 1
+    the batches are dealt round-robin over that many CUDA streams forked from
+    and joined back into `stream` every step (a batch's softmax and LayerNorm
+    stay in order on one stream), so one kernel's tail overlaps the next
+    batch's kernels -- how a server would issue independent requests."""
+    streams = [stream] + [torch.cuda.Stream(device=stream.device)
+                          for _ in range(max(1, nstreams) - 1)] if len(units) > 1 else [stream]
+    fork = torch.cuda.Event()
+    joins = [torch.cuda.Event() for _ in streams]
+
     def step(ev=None):
-        for u in units:
+        if len(streams) > 1:
+            fork.record(stream)
+            for st in streams[1:]:
+                st.wait_event(fork)
+        for i, u in enumerate(units):
+            st = streams[i % len(streams)]
             if ev is not None:
-                ev[0].record(stream)
+                ev[0].record(st)
             if wl.packed:
                 tt.tt_softmax_packed(u["scores"], u["cu"], u["blocks"], wl.heads, u["total"],
-                                     u["maxlen"], wl.scale, stream=stream)
+                                     u["maxlen"], wl.scale, stream=st)
             else:
-                tt.tt_softmax_masked(u["scores"], u["L"], wl.scale, stream=stream)
+                tt.tt_softmax_masked(u["scores"], u["L"], wl.scale, stream=st)
             if ev is not None:
-                ev[1].record(stream)
+                ev[1].record(st)
             tt.tt_add_bias_layernorm(u["out"], u["x"], u["residual"], u["bias"], u["gamma"],
-                                     u["beta"], wl.eps, stream=stream)
+                                     u["beta"], wl.eps, stream=st)
             if ev is not None:
-                ev[2].record(stream)
+                ev[2].record(st)
+        if len(streams) > 1:
+            for st, j in zip(streams[1:], joins[1:]):
+                j.record(st)
+                stream.wait_event(j)
     return step
 
 
@@ -338,13 +357,15 @@ def run_ours(args, rank, world, local_rank):
     stream = torch.cuda.Stream(device=dev)
     units = _units(tt, wl, rank, scaling, dev, stream)
 
+    if len(units) > 1:
+        desc["streams"] = args.streams
     plan_sm = (tt.softmax_packed_plan(wl.dtype, max(u["maxlen"] for u in units)) if wl.packed
                else tt.softmax_plan(wl.dtype, *units[0]["scores"].shape))
     plan_ln = tt.layernorm_plan(wl.dtype, *units[0]["x"].shape)
     b_sm = sum(wl.bytes_softmax(u["lens"]) for u in units)
     b_ln = sum(wl.bytes_ln(u["lens"]) for u in units)
 
-    step = _step_fn(tt, wl, units, stream)
+    step = _step_fn(tt, wl, units, stream, args.streams)
     for _ in range(args.warmup):
         step()
     stream.synchronize()
@@ -370,7 +391,7 @@ def run_ours(args, rank, world, local_rank):
         torch.cuda.empty_cache()
         wl5, desc5, sc5 = make_workload("c5", rank, world)
         u5 = _units(tt, wl5, rank, sc5, dev, stream)
-        st5 = _step_fn(tt, wl5, u5, stream)
+        st5 = _step_fn(tt, wl5, u5, stream, args.streams)
         for _ in range(3):
             st5()
         stream.synchronize()
@@ -378,6 +399,7 @@ def run_ours(args, rank, world, local_rank):
         c5 = _stream_record(dist, u5, _digests(u5), ms5, ms5_local, rank, world, wl5,
                             args.c5_steps, sc5)
         c5.update({"workload": desc5["workload"], "scaling": sc5, "steps": args.c5_steps,
+                   "streams": args.streams,
                    "warmup": 3, "clocks": clk5,
                    "kernels": {"softmax": tt.softmax_plan(wl5.dtype, *u5[0]["scores"].shape),
                                "layernorm": tt.layernorm_plan(wl5.dtype, *u5[0]["x"].shape)}})
@@ -676,6 +698,8 @@ def main():
                     help="process-group backend for N > 1 (gloo: ranks may share a GPU; tests)")
     ap.add_argument("--dist-timeout", type=float, default=600.0,
                     help="process-group timeout, seconds")
+    ap.add_argument("--streams", type=int, default=2,
+                    help="CUDA streams the batches of a multi-batch step are dealt over")
     ap.add_argument("--c5-steps", type=int, default=10,
                     help="timed steps of the C5 strong-scaling sub-record (c4 workload; 0: off)")
     args = ap.parse_args()

@@ -222,7 +222,7 @@ struct LnTier {
     TT_LN_EARLY(false, T, TN, 32, 32, 2, 128), TT_LN_EARLY(false, T, TN, 32, 32, 2, 256),        \
     TT_LN_EARLY(false, T, TN, 32, 32, 3, 256), TT_LN_EARLY(false, T, TN, 32, 32, 4, 256),        \
     TT_LN_TIER(false, T, TN, 32, 32, 3, 1, 128, 1), TT_LN_TIER(false, T, TN, 16, 32, 3, 1, 128, 1), \
-    TT_LN_TIER(false, T, TN, 32, 32, 2, 1, 128, 6)
+    TT_LN_TIER(false, T, TN, 32, 32, 2, 1, 128, 6), TT_LN_TIER(false, T, TN, 32, 32, 2, 1, 64, 12)
 
 // Tuning candidates (tools/tune.py): compiled into the TT_TUNING build only.
 #define TT_LN_TUNE_LIST(T, TN)                                                                 \
@@ -248,7 +248,7 @@ struct LnTier {
     TT_LN_TIER(false, T, TN, 32, 32, 3, 2, 256, 1), TT_LN_TIER(false, T, TN, 32, 32, 4, 2, 256, 1), \
     TT_LN_TIER(false, T, TN, 32, 16, 3, 1, 256, 1), TT_LN_TIER(false, T, TN, 32, 16, 4, 1, 256, 1), \
     TT_LN_TIER(false, T, TN, 16, 32, 4, 1, 256, 1), TT_LN_TIER(false, T, TN, 16, 32, 6, 1, 256, 1), \
-    TT_LN_TIER(false, T, TN, 32, 32, 2, 2, 128, 4), TT_LN_TIER(false, T, TN, 32, 32, 2, 1, 64, 12), \
+    TT_LN_TIER(false, T, TN, 32, 32, 2, 2, 128, 4),                                        \
     TT_LN_TIER(false, T, TN, 32, 32, 2, 1, 256, 3), TT_LN_TIER(false, T, TN, 16, 32, 4, 1, 128, 6), \
     TT_LN_TIER(false, T, TN, 16, 32, 3, 2, 128, 4), TT_LN_TIER(false, T, TN, 16, 32, 3, 1, 64, 12), \
     TT_LN_TIER(false, T, TN, 32, 32, 3, 1, 64, 10)
@@ -329,15 +329,16 @@ const Pref kLnPrefTiny[] = {
     {2, 768, 1024, "ln_rows<bf16,V32,G32,NV2,R1,T256,M1,E>"},
 };
 // More rows (C3, C4, C5): the persistent warp tier with exact-width rows at
-// hidden 768 (16-bit C3 25.4 us vs 32.9 round 1), 128-thread ln_rows at 1024
-// (C4 33.2 us vs 35.1) and for fp32 (C3 45.4 us vs 46.1).
+// hidden 768 (16-bit C3 25.4 us vs 32.9 round 1), 64-thread ln_rows (12 CTAs
+// per SM) at 1024 (C4 32.4 us vs 35.1 round 1, profiles/r02_ln/) and 128-thread
+// ln_rows for fp32 (C3 45.4 us vs 46.1).
 const Pref kLnPref[] = {
     {0, 512, 768, "ln_rows<f32,V32,G32,NV3,R1,T128,M1>"},
     {0, 768, 1024, "ln_rows<f32,V32,G32,NV4,R1,T128,M1>"},
     {1, 512, 768, "ln_warp<f16,V16,G32,NV3,T256,M3,PF0>"},
-    {1, 768, 1024, "ln_rows<f16,V32,G32,NV2,R1,T128,M6>"},
+    {1, 768, 1024, "ln_rows<f16,V32,G32,NV2,R1,T64,M12>"},
     {2, 512, 768, "ln_warp<bf16,V16,G32,NV3,T256,M3,PF0>"},
-    {2, 768, 1024, "ln_rows<bf16,V32,G32,NV2,R1,T128,M6>"},
+    {2, 768, 1024, "ln_rows<bf16,V32,G32,NV2,R1,T64,M12>"},
 };
 
 const LnTier* by_name(const LnTier* tab, const char* name) {

@@ -144,7 +144,7 @@ def test_softmax_tier_plan(ttlib, dtype, Sk, tier):
     (torch.float16, 30000, 768, "ln_warp<f16,V16,G32,NV3,T256,M3,PF0>"),
     (torch.bfloat16, 31808, 768, "ln_warp<bf16,V16,G32,NV3,T256,M3,PF0>"),
     (torch.bfloat16, 10, 1024, "ln_rows<bf16,V32,G32,NV2,R1,T256,M1,E>"),
-    (torch.bfloat16, 32768, 1024, "ln_rows<bf16,V32,G32,NV2,R1,T128,M6>"),
+    (torch.bfloat16, 32768, 1024, "ln_rows<bf16,V32,G32,NV2,R1,T64,M12>"),
     (torch.float32, 10, 37, "ln_rows<f32,V4,G32,NV4,R1,T256,M1>"),
     (torch.float16, 10, 16, "ln_warp<f16,V16,G4,NV1,T256,M4,PF0>"),
     (torch.float32, 10, 4096, "ln_rows<f32,V32,G128,NV4,R1,T128,M1>"),
