@@ -75,7 +75,7 @@ typedef enum {
 } tt_status;
 
 /* Largest supported row lengths (elements). */
-#define TT_MAX_SOFTMAX_COLS 131072
+#define TT_MAX_SOFTMAX_COLS 1073741824
 #define TT_MAX_LN_HIDDEN 32768
 
 /* ------------------------------------------------------------------------
@@ -94,7 +94,8 @@ typedef enum {
  *          row.  Padded query rows i >= L_b are normalised like any other
  *          row (only keys are masked; R2).
  * scale    finite float, applied to the logits before the max (BERT: 0.125).
- * Sk       <= TT_MAX_SOFTMAX_COLS.
+ * Sk       <= TT_MAX_SOFTMAX_COLS (2^30; rows beyond 131 072 keys run on the
+ *          two-pass long-row tier).
  * ---------------------------------------------------------------------- */
 TT_API tt_status tt_softmax_masked_f32(float* scores, const int32_t* lengths, int64_t B, int64_t H,
                                 int64_t Sq, int64_t Sk, float scale, cudaStream_t stream);

@@ -19,7 +19,7 @@ TT_SUCCESS = 0
 TT_ERROR_INVALID_VALUE = 1
 TT_ERROR_NOT_SUPPORTED = 2
 TT_ERROR_CUDA = 3
-TT_MAX_SOFTMAX_COLS = 131072
+TT_MAX_SOFTMAX_COLS = 1073741824
 TT_MAX_LN_HIDDEN = 32768
 
 DTYPE_CODE = {torch.float32: 0, torch.float16: 1, torch.bfloat16: 2}

@@ -18,6 +18,7 @@
 // Rows of any length: a row starts at an arbitrary element offset, so each row
 // is split into an unaligned head (< VE elements, scalar), an aligned body of
 // VB-byte vectors and a tail (< VE elements, scalar).
+#include <algorithm>
 #include <atomic>
 #include <cstring>
 
@@ -192,6 +193,30 @@ cudaError_t launch_softmax_cluster(void* scores, const int32_t* lengths, int64_t
     return cudaGetLastError();
 }
 
+
+// Rows of any length: a cluster of C CTAs per row, two passes per key segment
+// (softmax_long_kernel).  C = 8, or (KPC > 0) just enough CTAs for ~KPC keys
+// each (<= 8).  Measured on B200 (profiles/r02_long/): 256 threads x 4 CTAs/SM
+// and ~64 K keys per CTA beat 512 x 2 and 8 CTAs per row by 24-53 % on 131 K -
+// 262 K-key rows and tie on 1 M-key rows.
+constexpr int kLongMaxCols = 1 << 30;  // = TT_MAX_SOFTMAX_COLS (include/tt.h)
+template <typename T, int NT, int MINB, int KPC>
+cudaError_t launch_softmax_long(void* scores, const int32_t* lengths, int64_t nrows, int64_t rpb,
+                                int Sk, float scale, cudaStream_t st) {
+    int64_t C = 8;
+    if (KPC > 0) C = std::min<int64_t>(8, std::max<int64_t>(1, ((int64_t)Sk + KPC - 1) / KPC));
+    const int64_t W = (((int64_t)Sk + C - 1) / C + 63) / 64 * 64;
+    const int64_t grid = nrows * C;
+    if (grid > 0x7fffffffLL || W > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
+    float c = scale * kLog2e;
+    if (c == 0.f) c = 1e-30f;
+    const cudaError_t le = launch_kc(softmax_long_kernel<T, NT, 4, MINB>, (unsigned)grid, NT, 0,
+                                     st, (unsigned)C, static_cast<T*>(scores), lengths, rpb,
+                                     Sk, (int)W, c);
+    if (le != cudaSuccess) return le;
+    return cudaGetLastError();
+}
+
 using SoftmaxFn = cudaError_t (*)(void*, const int32_t*, int64_t, int64_t, int, float,
                                   cudaStream_t);
 
@@ -214,6 +239,12 @@ struct SoftmaxTier {
         8 * (NT) * (NV) * ((VB) / (int)sizeof(T)), AUTO,                                   \
             &launch_softmax_cluster<T, VB, NV, NT>,                                        \
             "softmax_cluster<" TN ",V" #VB ",NV" #NV ",T" #NT ",C8>"                        \
+    }
+
+#define TT_SM_LONG(AUTO, T, TN, NT, MINB, KPC)                                             \
+    SoftmaxTier {                                                                          \
+        kLongMaxCols, AUTO, &launch_softmax_long<T, NT, MINB, KPC>,                         \
+            "softmax_long<" TN ",V16,T" #NT ",M" #MINB ",K" #KPC ">"                        \
     }
 
 #define TT_SM_WARP_R(AUTO, T, TN, VB, G, NV, NT, MINB, RPG)                               \
@@ -252,7 +283,7 @@ struct SoftmaxTier {
     TT_SM_WARP(true, T, TN, 32, 32, 3, 256, M3), TT_SM_WARP(true, T, TN, 32, 32, 4, 256, M4),   \
     TT_SM_TIER(true, T, TN, 32, 64, NVC, 1, 64, 1), TT_SM_TIER(true, T, TN, 32, 128, NVC, 1, 128, 1), \
     TT_SM_TIER(true, T, TN, 32, 256, NVC, 1, 256, 1), TT_SM_TIER(true, T, TN, 32, 512, NVC, 1, 512, 1), \
-    TT_SM_CLUSTER(true, T, TN, 32, NVC, 512),                                               \
+    TT_SM_CLUSTER(true, T, TN, 32, NVC, 512), TT_SM_LONG(true, T, TN, 256, 4, 65536),                      \
     /* selected through the preference table kSmPref */                                      \
     TT_SM_WARP(false, T, TN, 16, 8, 2, 256, 6), TT_SM_WARP_F(false, T, TN, 16, 8, 4, 256, 3, 4), \
     TT_SM_WARP_R(false, T, TN, 32, 32, 1, 256, 6, 2), TT_SM_WARP_R(false, T, TN, 32, 32, 2, 256, 3, 2), \

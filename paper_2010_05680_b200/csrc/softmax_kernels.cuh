@@ -637,4 +637,137 @@ __global__ void __launch_bounds__(NT, 1) softmax_cluster_kernel(T* __restrict__ 
     }
 }
 
+
+// ----------------------------------------------------------------------------
+// Rows of any length (beyond the cluster tier's 8 register-resident segments):
+// softmax_long.  A cluster of C CTAs per row, CTA r owns the key segment
+// [r W, (r + 1) W) (W = ceil(Sk / C) rounded up to 64 keys) and makes TWO
+// passes over it: pass 1 streams the segment's valid keys from HBM and keeps a
+// per-thread online (m, s) -- s rescaled by 2^(m_old - m_new) when the running
+// max grows --, the CTA and then the cluster merge
+// the pairs exactly as softmax_cluster does (distributed shared memory);
+// pass 2 re-reads the valid keys (an L2 hit while the live segments fit in the
+// 126 MB L2: 2 x 148 CTAs x W keys), writes y = 2^(t - M) / S and +0.0 past L.
+// t = x * c is recomputed with the same fp32 multiply in both passes.  HBM
+// traffic per row: L e (+ the L2 re-read) + Sk e, one write per key.
+// ----------------------------------------------------------------------------
+template <typename T, int NT, int U, int MINB>
+__global__ void __launch_bounds__(NT, MINB) softmax_long_kernel(T* __restrict__ scores,
+                                                             const int32_t* __restrict__ lengths,
+                                                             int64_t rows_per_batch, int Sk,
+                                                             int W, float c) {
+    PdlScope pdl_;  // griddepcontrol.wait first: no global access before it (PDL)
+    constexpr int VB = 16, VE = VB / (int)sizeof(T);
+    __shared__ float red_m[NT / 32], red_s[NT / 32];
+    __shared__ float part[2];  // this CTA's (m_c, s_c), read by the cluster
+
+    const uint32_t cr = cluster_ctarank(), ncl = cluster_nctarank();
+    const int64_t row = (int64_t)(blockIdx.x / ncl);
+    const int q = threadIdx.x;
+    const int seg0 = (int)min((int64_t)cr * W, (int64_t)Sk);
+    const int Sks = min(W, Sk - seg0);  // keys in this segment (may be 0)
+    T* p = scores + row * (int64_t)Sk + seg0;
+    const int L = min(max(__ldg(lengths + row / rows_per_batch), 0), Sk);
+    const int Ls = min(max(L - seg0, 0), Sks);  // valid keys in this segment
+    const int mis = (int)((reinterpret_cast<uintptr_t>(p) & (VB - 1)) / sizeof(T));
+    const int hd = mis ? min(VE - mis, Sks) : 0;  // scalar head up to 16-byte alignment
+    const int nv = (Sks - hd) / VE;
+    const int tl0 = hd + nv * VE;  // scalar tail [tl0, Sks)
+
+    // ---- pass 1: online (m, s) over the valid keys of the segment
+    float m = -INFINITY, s = 0.f;
+    auto absorb = [&](float t) {  // one more valid key
+        const float mn = fmaxf(m, t);
+        s = s * ex2_approx(m - mn) + ex2_approx(t - mn);
+        m = mn;
+    };
+    // U vectors per thread in flight: all loads of a batch first, then one max,
+    // one rescale and the exponentials of the batch
+    for (int v0 = q; v0 < nv; v0 += NT * U) {
+        if (hd + v0 * VE >= Ls) break;
+        float x[U][VE];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int vi = v0 + u * NT, j0 = hd + vi * VE;
+            if (vi < nv && j0 < Ls) {
+                Raw<VB> w;
+                ld_stream<VB>(p + j0, w);
+                Elem<T>::template unpack<VB>(w, x[u]);
+            }
+        }
+        float vm = -INFINITY;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int j0 = hd + (v0 + u * NT) * VE;
+#pragma unroll
+            for (int e = 0; e < VE; ++e) {
+                x[u][e] = (v0 + u * NT < nv && j0 + e < Ls) ? x[u][e] * c : -INFINITY;
+                vm = fmaxf(vm, x[u][e]);
+            }
+        }
+        const float mn = fmaxf(m, vm);
+        float acc = 0.f;
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int e = 0; e < VE; ++e) acc += ex2_approx(x[u][e] - mn);
+        s = s * ex2_approx(m - mn) + acc;
+        m = mn;
+    }
+    if (q < hd && q < Ls) absorb(Elem<T>::to_f(p[q]) * c);
+    if (tl0 + q < Ls) absorb(Elem<T>::to_f(p[tl0 + q]) * c);  // q < VE - 1 < NT
+    // ---- the CTA's pair (m_c, s_c)
+    float mv[1] = {m};
+    group_max<NT, 1>(mv, red_m);
+    const float mc = mv[0];
+    float sv[1] = {m == -INFINITY ? 0.f : s * ex2_approx(m - mc)};
+    group_sum<NT, 1>(sv, red_s);
+    if (q == 0) {
+        part[0] = mc;
+        part[1] = sv[0];
+    }
+    // ---- the cluster merge: (M, S) over the segments' (m_c, s_c)
+    cluster_sync_all();
+    float M = -INFINITY, Sum = 0.f;
+    for (uint32_t r = 0; r < ncl; ++r) M = fmaxf(M, ld_dsmem_f32(&part[0], r));
+    for (uint32_t r = 0; r < ncl; ++r) {
+        const float mr = ld_dsmem_f32(&part[0], r);
+        if (mr != -INFINITY) Sum += ld_dsmem_f32(&part[1], r) * ex2_approx(mr - M);
+    }
+    cluster_sync_all();  // partners are done reading this CTA's `part`
+    // ---- pass 2: y = 2^(t - M) / S for j < L, +0.0 past L (L = 0: all zero)
+    const float f = L > 0 ? 1.0f / Sum : 0.f;
+    // batches in reverse order: the keys pass 1 read last are the likeliest to
+    // still be in L2 when the live segments outgrow it
+    const int nb = (nv + NT * U - 1) / (NT * U);
+    for (int bi = nb - 1; bi >= 0; --bi) {
+        const int v0 = q + bi * NT * U;
+        float y[U][VE];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int vi = v0 + u * NT, j0 = hd + vi * VE;
+            if (vi < nv && j0 < Ls) {
+                Raw<VB> w;
+                ld_stream<VB>(p + j0, w);
+                Elem<T>::template unpack<VB>(w, y[u]);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int vi = v0 + u * NT, j0 = hd + vi * VE;
+            if (vi < nv) {
+#pragma unroll
+                for (int e = 0; e < VE; ++e)
+                    y[u][e] = (j0 + e < Ls) ? ex2_approx(y[u][e] * c - M) * f : 0.f;
+                Raw<VB> o;
+                Elem<T>::template pack<VB>(y[u], o);
+                st_stream<VB>(p + j0, o);
+            }
+        }
+    }
+    if (q < hd) p[q] = Elem<T>::from_f(q < Ls ? ex2_approx(Elem<T>::to_f(p[q]) * c - M) * f : 0.f);
+    if (tl0 + q < Sks)
+        p[tl0 + q] = Elem<T>::from_f(tl0 + q < Ls ? ex2_approx(Elem<T>::to_f(p[tl0 + q]) * c - M) * f : 0.f);
+}
+
 }  // namespace tt

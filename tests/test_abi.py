@@ -127,6 +127,8 @@ def test_launch_without_device_fails_loudly(ttlib):
     (torch.bfloat16, 16384, "softmax_rows<bf16,V32,G512,NV2,R1,T512,M1>"),
     (torch.bfloat16, 16385, "softmax_cluster<bf16,V32,NV2,T512,C8>"),
     (torch.float32, 131072, "softmax_cluster<f32,V32,NV4,T512,C8>"),
+    (torch.float32, 131073, "softmax_long<f32,V16,T256,M4,K65536>"),
+    (torch.bfloat16, 1 << 24, "softmax_long<bf16,V16,T256,M4,K65536>"),
 ])
 def test_softmax_tier_plan(ttlib, dtype, Sk, tier):
     assert ttlib.softmax_plan(dtype, 2, 12, 3, Sk) == tier

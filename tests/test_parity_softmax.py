@@ -149,11 +149,28 @@ def test_every_row_length_1_to_160(ttlib, dtype):
 @pytest.mark.parametrize("dtype", DT)
 @pytest.mark.parametrize("Sk", [255, 256, 257, 511, 513, 767, 1000, 1023, 1024, 1025, 2047, 2048,
                                 2049, 4095, 4096, 4099, 8192, 16384, 16385, 32768, 32771,
-                                65536, 100003, 131072])
+                                65536, 100003, 131072, 131073, 262147, 400000])
 def test_long_rows_and_tier_boundaries(ttlib, dtype, Sk):
     lens = [Sk, Sk - 1, 1, Sk // 3]
     x = W.scores(4, 1, 2, Sk, dtype, seed=Sk + 7)
     _full_check(ttlib, x, lens, W.SCALE_BERT, f"Sk={Sk}")
+
+
+@pytest.mark.parametrize("dtype", DT)
+@pytest.mark.parametrize("Sk", [131073, 8 * 65536 + 3, 9 * 65536 + 5])
+def test_long_tier_segments_and_masks(ttlib, dtype, Sk):
+    """Rows beyond the cluster tier (softmax_long: <= 8 CTAs per row, each making an
+    online (m, s) pass and a normalising pass over its key segment, pairs merged
+    through distributed shared memory): valid lengths ending inside a segment,
+    on segment boundaries, in the first segment only, 0 and 1; odd pitches so
+    rows and segments start unaligned; poison in the padding; negative scale."""
+    C = min(8, -(-Sk // 65536))  # CTAs per row (softmax.cu launch_softmax_long, K65536)
+    Wseg = (-(-Sk // C) + 63) // 64 * 64
+    lens = [Sk, 1, 0, Wseg, Wseg + 1, (C - 1) * Wseg - 2, (C - 1) * Wseg, Sk - 1, 17]
+    x = W.scores(len(lens), 1, 1, Sk, dtype, seed=Sk)
+    assert ttlib.softmax_plan(dtype, len(lens), 1, 1, Sk).startswith("softmax_long<")
+    _full_check(ttlib, x, lens, W.SCALE_BERT, "long")
+    _full_check(ttlib, W.poison_masked(x, lens), lens, -0.25, "long poison")
 
 
 @pytest.mark.parametrize("dtype", DT)

@@ -55,6 +55,7 @@ def main():
         # a 32 768-key row (CTA tier) and odd pitches off 16-B-but-not-32-B bases
         sm(dtype, 2, 1, 1, 32768, [32768, 20000])
         sm(dtype, 3, 1, 1, 40003, [40003, 16385, 5])   # cluster tier: 3 CTAs per row
+        sm(dtype, 3, 1, 1, 140003, [140003, 17505, 0])   # long tier: 8 CTAs per row, two passes
         for Sk in (37, 491, 1000):
             sm(dtype, 3, 2, 3, Sk, [Sk, Sk // 2, 0], offset_elems=16 // W.ELEM_BYTES[dtype])
         # every automatic LayerNorm band at hidden 768 / 1024 and odd hidden
