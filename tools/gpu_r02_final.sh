@@ -21,4 +21,4 @@ python tools/sweep_table.py gpurun_out/sweep.jsonl > profiles/r02_sweep.txt
 python tools/sweep_table.py gpurun_out/sweep_next2.jsonl > profiles/r02_sweep_next2.txt
 mkdir -p gpurun_out/profiles_box && cp profiles/r02_launches.csv profiles/r02_ncu_full.txt profiles/r02_sass_*.txt profiles/r02_bench.json profiles/traffic.json profiles/r02_sweep.txt profiles/r02_sweep_next2.txt gpurun_out/profiles_box/ 2>/dev/null
 rm -f gpurun_out/prof_c4.ncu-rep
-tail -3 gpurun_out/final/pytest_gpu.txt gpurun_out/final/pytest_tune.txt
+tail -n 3 gpurun_out/final/pytest_gpu.txt gpurun_out/final/pytest_tune.txt
