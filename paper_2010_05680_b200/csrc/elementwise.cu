@@ -64,6 +64,36 @@ __device__ __forceinline__ float erf_as(float x) {
     return copysignf(fmaf(-p, e, 1.0f), x);
 }
 
+// The same A&S 7.1.26 erf for a pair of arguments on packed fp32 (FFMA2 /
+// FMUL2): the polynomial and the argument scaling cost one issue slot per two
+// elements; rcp and ex2 stay on the MUFU.  Returns gelu(v) = 0.5 v (1 + erf(v / sqrt 2))
+// for the pair v2.
+__device__ __forceinline__ F2 gelu_erf2(F2 v2) {
+    const F2 hv2 = f2_mul(v2, f2_make(0.5f, 0.5f));
+    float v0, v1;
+    f2_split(v2, v0, v1);
+    const F2 ax2 = f2_make(fabsf(v0) * 0.7071067811865476f, fabsf(v1) * 0.7071067811865476f);
+    float d0, d1;
+    f2_split(f2_fma(ax2, f2_make(0.3275911f, 0.3275911f), f2_make(1.0f, 1.0f)), d0, d1);
+    float t0, t1;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(t0) : "f"(d0));
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(t1) : "f"(d1));
+    const F2 t2 = f2_make(t0, t1);
+    // -(a1 + t (a2 + t (a3 + t (a4 + t a5)))) t, negated coefficients
+    F2 p2 = f2_fma(f2_make(-1.061405429f, -1.061405429f), t2, f2_make(1.453152027f, 1.453152027f));
+    p2 = f2_fma(p2, t2, f2_make(-1.421413741f, -1.421413741f));
+    p2 = f2_fma(p2, t2, f2_make(0.284496736f, 0.284496736f));
+    p2 = f2_fma(p2, t2, f2_make(-0.254829592f, -0.254829592f));
+    p2 = f2_mul(p2, t2);
+    float a0, a1;
+    f2_split(f2_mul(f2_mul(ax2, ax2), f2_make(-1.4426950408889634f, -1.4426950408889634f)), a0, a1);
+    const F2 e2 = f2_make(ex2_approx(a0), ex2_approx(a1));
+    float r0, r1;
+    f2_split(f2_fma(p2, e2, f2_make(1.0f, 1.0f)), r0, r1);  // erf(|x|)
+    const F2 erf2 = f2_make(copysignf(r0, v0), copysignf(r1, v1));
+    return f2_fma(hv2, erf2, hv2);
+}
+
 __device__ __forceinline__ float tanh_approx(float x) {
     float y;
     asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -74,44 +104,72 @@ __device__ __forceinline__ float tanh_approx(float x) {
 // (bias vectors are the same for every row, so they stay in L1).  The tanh
 // form uses MUFU.TANH (rel. error ~2^-11) for 16-bit outputs, whose own
 // rounding is coarser, and the accurate tanhf for fp32.
-template <typename T, int VB, bool APPROX, int NT>
+template <typename T, int VB, bool APPROX, int NT, int U>
 __global__ void __launch_bounds__(NT) add_bias_gelu_kernel(T* out, const T* x,
                                                            const T* __restrict__ bias,
-                                                           int64_t rows, int n, int rpb) {
+                                                           int64_t rows, int n, int rpb,
+                                                           FastDivU32 div_nvec) {
     PdlScope pdl_;  // griddepcontrol.wait first: no global access before it (PDL)
     constexpr int VE = VB / (int)sizeof(T);
     const int nvec = n / VE;
     const int64_t r0 = (int64_t)blockIdx.x * rpb;
     const int64_t r1 = min(rows, r0 + rpb);
-    for (int64_t r = r0; r < r1; ++r) {
-        const T* xr = x + r * (int64_t)n;
-        T* orow = out + r * (int64_t)n;
-        for (int vi = threadIdx.x; vi < nvec; vi += NT) {
-            Raw<VB> wx, wb;
-            ld_stream<VB>(xr + vi * VE, wx);
-            ld_param<VB>(bias + vi * VE, wb);
-            float f[VE], g[VE];
-            Elem<T>::template unpack<VB>(wx, f);
-            Elem<T>::template unpack<VB>(wb, g);
+    if (r1 <= r0) return;
+    // the CTA's rows are one contiguous span of (r1 - r0) * nvec vectors; vector
+    // f of the span uses bias vector f mod nvec.  U vectors per thread in
+    // flight: every load of a batch is issued before the (MUFU-heavy) GELU
+    // arithmetic of the first.
+    const T* xs = x + r0 * (int64_t)n;
+    T* os = out + r0 * (int64_t)n;
+    const int nf = (int)(r1 - r0) * nvec;
+    for (int f0 = threadIdx.x; f0 < nf; f0 += NT * U) {
+        Raw<VB> wx[U], wb[U];
 #pragma unroll
-            for (int e = 0; e < VE; ++e) {
-                const float v = f[e] + g[e];
-                const float hv = 0.5f * v;
-                if constexpr (APPROX) {
-                    const float u = 0.7978845608028654f * fmaf(0.044715f * v, v * v, v);
-                    const float th = sizeof(T) == 4 ? tanhf(u) : tanh_approx(u);
-                    f[e] = fmaf(hv, th, hv);
-                } else {
-                    f[e] = fmaf(hv, erf_as(v * 0.7071067811865476f), hv);
+        for (int u = 0; u < U; ++u) {
+            const int fi = f0 + u * NT;
+            if (fi < nf) {
+                const int bi = fi - (int)div_nvec.div((uint32_t)fi) * nvec;
+                ld_stream<VB>(xs + (int64_t)fi * VE, wx[u]);
+                ld_param<VB>(bias + bi * VE, wb[u]);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int fi = f0 + u * NT;
+            if (fi >= nf) break;
+            float fv[VE], g[VE];
+            Elem<T>::template unpack<VB>(wx[u], fv);
+            Elem<T>::template unpack<VB>(wb[u], g);
+            if constexpr (APPROX) {
+#pragma unroll
+                for (int e = 0; e < VE; ++e) {
+                    const float v = fv[e] + g[e];
+                    const float hv = 0.5f * v;
+                    const float uu = 0.7978845608028654f * fmaf(0.044715f * v, v * v, v);
+                    const float th = sizeof(T) == 4 ? tanhf(uu) : tanh_approx(uu);
+                    fv[e] = fmaf(hv, th, hv);
+                }
+            } else if constexpr (VE % 2 == 0) {
+#pragma unroll
+                for (int e = 0; e < VE; e += 2)
+                    f2_split(gelu_erf2(f2_add(f2_make(fv[e], fv[e + 1]), f2_make(g[e], g[e + 1]))),
+                             fv[e], fv[e + 1]);
+            } else {
+#pragma unroll
+                for (int e = 0; e < VE; ++e) {
+                    const float v = fv[e] + g[e];
+                    const float hv = 0.5f * v;
+                    fv[e] = fmaf(hv, erf_as(v * 0.7071067811865476f), hv);
                 }
             }
             Raw<VB> wy;
-            Elem<T>::template pack<VB>(f, wy);
-            st_stream<VB>(orow + vi * VE, wy);
+            Elem<T>::template pack<VB>(fv, wy);
+            st_stream<VB>(os + (int64_t)fi * VE, wy);
         }
     }
 }
 
+constexpr int64_t kGeluBigVecs = 4 << 20;  // calls of >= 4 M vectors: 4 per thread in flight
 template <typename T, int VB, bool APPROX>
 cudaError_t launch_gelu(void* out, const void* x, const void* bias, int64_t rows, int64_t n,
                         cudaStream_t st) {
@@ -123,11 +181,16 @@ cudaError_t launch_gelu(void* out, const void* x, const void* bias, int64_t rows
     const int64_t max_rpb = (rows + 4 * (int64_t)sm_count_e() - 1) / (4 * (int64_t)sm_count_e());
     if (rpb > max_rpb) rpb = max_rpb > 0 ? max_rpb : 1;
     const int64_t grid = (rows + rpb - 1) / rpb;
-    if (grid > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
+    if (grid > 0x7fffffffLL || rpb * nvec > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
     {
-        const cudaError_t le_ = launch_k(add_bias_gelu_kernel<T, VB, APPROX, NT>, (unsigned)grid, NT, 0, st,
+        // 4 vectors per thread in flight on large calls (BERT-large FFN: 101 -> 94 us);
+        // small calls, a few waves of CTAs, are latency-bound and prefer one
+        // (BERT-base b20 s128: 9.3 -> 8.6 us; profiles/r02_next2/)
+        auto kern = rows * nvec >= kGeluBigVecs ? add_bias_gelu_kernel<T, VB, APPROX, NT, 4>
+                                                : add_bias_gelu_kernel<T, VB, APPROX, NT, 1>;
+        const cudaError_t le_ = launch_k(kern, (unsigned)grid, NT, 0, st,
         static_cast<T*>(out), static_cast<const T*>(x), static_cast<const T*>(bias), rows,
-        (int)n, (int)rpb);
+        (int)n, (int)rpb, FastDivU32::make((uint32_t)nvec));
         if (le_ != cudaSuccess) return le_;
     }
     return cudaGetLastError();

@@ -42,6 +42,23 @@ def test_add_bias_gelu_in_place_and_bert_ffn_shape(ttlib, dtype):
     assert_close("gelu", dtype, x[:: 97], oracle.add_bias_gelu(ref_in, b.cpu()), "in place")
 
 
+@pytest.mark.parametrize("dtype", DT)
+@pytest.mark.parametrize("rows,n", [(32771, 1024), (4099, 4100)])
+def test_add_bias_gelu_large_calls(ttlib, dtype, rows, n):
+    """Calls of >= 4 M vectors take the 4-vectors-per-thread kernel (elementwise.cu
+    kGeluBigVecs): a row count that leaves a partial last CTA span, and a width whose
+    pitch is not a multiple of the 16-byte vector (element-size vectors); every 61st
+    row and the last row against the oracle."""
+    x = W.scores(1, 1, rows, n, dtype, device="cuda", seed=rows, std=2.0).reshape(rows, n)
+    b = _gen((n,), dtype, 3, std=0.3).cuda()
+    out = torch.empty_like(x)
+    ttlib.tt_add_bias_gelu(out, x, b)
+    torch.cuda.synchronize()
+    idx = torch.cat([torch.arange(0, rows, 61), torch.tensor([rows - 1])]).cuda()
+    assert_close("gelu", dtype, out[idx], oracle.add_bias_gelu(x[idx].cpu(), b.cpu()),
+                 f"gelu {rows}x{n}")
+
+
 def _split_ref(qkv, bias, B, S, H, D, dtype):
     return [t.to(dtype) for t in oracle.split_qkv_add_bias(qkv, bias, B, S, H, D)]
 
