@@ -415,8 +415,8 @@ def run_ours(args, rank, world, local_rank):
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
         "warmup": args.warmup, "ms_per_step": round(ms / K, 6), "higher_is_better": True,
-        "scaling": scaling, "vs_baseline": None, "dtype": W.DTYPE_NAMES[wl.dtype],
-        "arith": "fp32",
+        "scaling": scaling, "vs_baseline": None, "dtype": "f32",
+        "arith": "fp32", "storage": W.DTYPE_NAMES[wl.dtype],
         "data": "synthetic (seeded; logits N(0,8^2), LN inputs N(0,1); SURVEY §8(d) recipe)",
         "config": desc,
         "rows_per_s": rec["rows_per_s"],
