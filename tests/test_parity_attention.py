@@ -146,3 +146,32 @@ def test_attention_o_rescale_branch(ttlib, variant, dtype, S, lens):
         assert _rescale_fraction(q, k, lens, 0.125, bn) > 0.5, bn
     got = _run(ttlib, q, k, v, lens, 0.125)
     _check(dtype, got, oracle.attention(q, k, v, lens, 0.125), f"peaky S={S} lens={lens}")
+
+
+@pytest.mark.parametrize("case", ["C4", "C4 ragged", "C3"])
+def test_attention_full_size_sampled_heads(ttlib, case):
+    """The automatic schedule at the BASELINE sizes tools/attn_bench.py times (C4
+    BERT-large b64 s512 bf16, full and ragged lengths; C3 64 requests U{5..500}
+    fp16, S = their max): the whole [B, H, S, 64] output computed in one launch,
+    then every row of eight sampled (b, h) heads -- the longest and shortest
+    requests included -- against the fp64 oracle."""
+    if case.startswith("C4"):
+        B, H, S, dtype = 64, 16, 512, torch.bfloat16
+        lens = W.lengths_full(B, S) if case == "C4" else W.lengths_ragged(B, S, 4)
+    else:
+        lens = W.c3_lengths()
+        B, H, S, dtype = len(lens), 12, int(np.max(lens)), torch.float16
+    g = torch.Generator(device="cuda").manual_seed(11)
+    q, k, v = (torch.randn(B, H, S, 64, device="cuda", generator=g).to(dtype) for _ in range(3))
+    out = torch.empty_like(q)
+    ttlib.tt_attention_fwd(out, q, k, v, torch.as_tensor(np.asarray(lens, dtype=np.int32)).cuda(),
+                           0.125)
+    torch.cuda.synchronize()
+    order = np.argsort(np.asarray(lens), kind="stable")
+    rng = np.random.default_rng(5)
+    bs = [int(order[0]), int(order[-1])] + [int(x) for x in rng.choice(B, 6, replace=False)]
+    for i, b in enumerate(bs):
+        h = (7 * i + 3) % H
+        sl = (slice(b, b + 1), slice(h, h + 1))
+        ref = oracle.attention(q[sl].cpu(), k[sl].cpu(), v[sl].cpu(), [int(lens[b])], 0.125)
+        _check(dtype, out[sl].cpu(), ref, f"{case} b={b} h={h} L={int(lens[b])}")
