@@ -51,7 +51,7 @@ __device__ __forceinline__ void packed_rows(T* __restrict__ scores, uint32_t fir
     for (uint32_t b = first + (threadIdx.x >> 5) * GPW; b < row_end; b += step, row += step) {
         const bool live = row < row_end;
         T* p = scores + base + (int64_t)((live ? row : first) - row0) * L;
-        softmax_row_pass<T, VB, GC, NVC, false, false, UP>(p, live, L, L, c, q);
+        softmax_row_pass<T, VB, GC, NVC, false, false, UP, true>(p, live, L, L, c, q);
     }
 }
 
@@ -97,7 +97,7 @@ __device__ __forceinline__ void packed_body(T* __restrict__ scores, const int32_
         const int L = min(__ldg(cu + r + 1) - __ldg(cu + r), CAP);
         const uint32_t row0 = H * (uint32_t)__ldg(cu + r);
         T* p = scores + __ldg(blocks + r) + (int64_t)(row - row0) * L;
-        softmax_row_pass<T, VB, 32, NV, false, false, UP>(p, true, L, L, c, lane);
+        softmax_row_pass<T, VB, 32, NV, false, false, UP, true>(p, true, L, L, c, lane);
     }
 }
 

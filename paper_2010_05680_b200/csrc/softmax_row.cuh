@@ -81,7 +81,8 @@ __device__ __forceinline__ void row_load(const T* __restrict__ p, int L, int Sk,
 // remaining body vectors are written as zeros without any arithmetic.  UP:
 // c > 0, so the row max of c*x is c*max(x) (else c*min(x)); a template
 // parameter so that only one of the two reductions is compiled into each path.
-template <typename T, int VB, int GC, int NVC, bool ALIGNED, bool NARROW, bool UP, bool EF = false>
+template <typename T, int VB, int GC, int NVC, bool ALIGNED, bool NARROW, bool UP, bool EF = false,
+          bool FULLROW = false>
 __device__ __forceinline__ void row_finish(T* __restrict__ p, bool live, int L, int Sk, float c,
                                            int q, const RowRaw<T, VB, GC, NVC, ALIGNED>& r) {
     using RR = RowRaw<T, VB, GC, NVC, ALIGNED>;
@@ -93,9 +94,17 @@ __device__ __forceinline__ void row_finish(T* __restrict__ p, bool live, int L, 
     int hd, nv;
     row_split<T, VB, ALIGNED>(p, Sk, hd, nv);
     const int tl0 = hd + nv * VE;
-    // masking is needed unless every key is valid and every vector slot of
-    // the group maps onto the row (uniform within the group)
-    const bool masked = (L < Sk) || (nv != GC * NVC);
+    // FULLROW (the packed layout: every key of every row valid, L = Sk) with at
+    // least one body vector: no per-element mask.  Vector slots past the row
+    // (vi >= nv) then hold a re-read copy of the row's first body vector
+    // (row_load), which cannot change the max, and are left out of the sum by a
+    // 0 / 1 weight (the sum's FADD2 becomes an FFMA2) and never stored.
+    // Otherwise masking is needed unless every key is valid and every vector
+    // slot of the group maps onto the row.  (Uniform within the group.  Not
+    // compiled into the padded kernels: the extra path costs their 40-register
+    // unaligned 16-bit tiers a spill, C3 fp16 -2 %.)
+    const bool masked = FULLROW ? (L < Sk) || (nv == 0) : (L < Sk) || (nv != GC * NVC);
+    const bool dead_slots = FULLROW && !masked && (nv != GC * NVC);
 
     float v[NVC][VE];
 #pragma unroll
@@ -157,7 +166,10 @@ __device__ __forceinline__ void row_finish(T* __restrict__ p, bool live, int L, 
         const F2 c2 = f2_make(c, c), nm2 = f2_make(nm, nm);
         F2 s2 = f2_make(0.f, 0.f);
 #pragma unroll
-        for (int k = 0; k < NVC; ++k)
+        for (int k = 0; k < NVC; ++k) {
+            // a slot past the row (dead_slots) is summed with weight 0
+            const float w = (!dead_slots || q + k * GC < nv) ? 1.f : 0.f;
+            const F2 w2 = f2_make(w, w);
 #pragma unroll
             for (int e = 0; e < VE; e += 2) {
                 const F2 t = f2_fma(f2_make(v[k][e], v[k][e + 1]), c2, nm2);
@@ -165,8 +177,12 @@ __device__ __forceinline__ void row_finish(T* __restrict__ p, bool live, int L, 
                 f2_split(t, t0, t1);
                 v[k][e] = ex2_approx(t0);
                 v[k][e + 1] = ex2_approx(t1);
-                s2 = f2_add(s2, f2_make(v[k][e], v[k][e + 1]));
+                if constexpr (FULLROW)
+                    s2 = f2_fma(f2_make(v[k][e], v[k][e + 1]), w2, s2);
+                else
+                    s2 = f2_add(s2, f2_make(v[k][e], v[k][e + 1]));
             }
+        }
         float s0, s1;
         f2_split(s2, s0, s1);
         s[0] = s0 + s1;
@@ -221,13 +237,14 @@ __device__ __forceinline__ void row_finish(T* __restrict__ p, bool live, int L, 
 }
 
 // One row, load then finish (no prefetch).
-template <typename T, int VB, int GC, int NVC, bool ALIGNED, bool NARROW, bool UP>
+template <typename T, int VB, int GC, int NVC, bool ALIGNED, bool NARROW, bool UP,
+          bool FULLROW = false>
 __device__ __forceinline__ void softmax_row_pass(T* __restrict__ p, bool live, int L, int Sk,
                                                  float c, int q) {
     if (!live) L = 0;
     RowRaw<T, VB, GC, NVC, ALIGNED> r;
     row_load<T, VB, GC, NVC, ALIGNED>(p, L, Sk, q, r);
-    row_finish<T, VB, GC, NVC, ALIGNED, NARROW, UP>(p, live, L, Sk, c, q, r);
+    row_finish<T, VB, GC, NVC, ALIGNED, NARROW, UP, false, FULLROW>(p, live, L, Sk, c, q, r);
 }
 
 }  // namespace tt

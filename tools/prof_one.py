@@ -9,6 +9,7 @@ import argparse
 import os
 import sys
 
+import numpy as np
 import torch
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -43,6 +44,16 @@ def main():
             tt.attention_variant(int(a.tier))
         for _ in range(a.reps):
             tt.tt_attention_fwd(o, q, k, v, L, 0.125)
+    elif a.op == "packed":  # C3 lengths, dims = H: the padding-free layout (NEXT-1)
+        lens = W.c3_lengths()
+        H = a.dims[0]
+        cu = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
+        blk = np.concatenate([[0], np.cumsum(H * lens.astype(np.int64) ** 2)]).astype(np.int64)
+        x = W.scores(1, 1, 1, int(blk[-1]), dt, device="cuda").reshape(-1)
+        cu_d, blk_d = torch.as_tensor(cu).cuda(), torch.as_tensor(blk[:-1]).cuda()
+        print("tier:", tt.softmax_packed_plan(dt, int(lens.max())))
+        for _ in range(a.reps):
+            tt.tt_softmax_packed(x, cu_d, blk_d, H, int(cu[-1]), int(lens.max()), 0.125)
     elif a.op == "softmax":
         if a.c3:
             lens = W.c3_lengths()
