@@ -23,18 +23,28 @@ namespace {
 constexpr float kLog2eP = 1.4426950408889634f;
 }
 
-// largest r in [0, num_req) with H * cu[r] <= row (cu nondecreasing, cu[0] = 0)
-__device__ __forceinline__ int find_req(const int32_t* __restrict__ cu, int num_req, uint32_t H,
-                                        uint32_t row) {
-    int lo = 0, hi = num_req - 1;
-    while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if ((uint64_t)H * (uint32_t)__ldg(cu + mid) <= row)
-            lo = mid;
-        else
-            hi = mid - 1;
+// largest r in [0, num_req) with H * cu[r] <= row (cu nondecreasing, cu[0] = 0),
+// searched by one whole warp (every lane calls it with the same row; the
+// result is warp-uniform): 32 evenly spaced probes per round and a ballot,
+// so ceil(log32 num_req) dependent loads instead of log2 num_req, and no CTA
+// barrier -- the CTA-wide search by one thread behind a __syncthreads was 25 %
+// of the packed kernel's stall samples (profiles/r02_packed/).
+__device__ __forceinline__ int find_req_warp(const int32_t* __restrict__ cu, int num_req,
+                                             uint32_t H, uint32_t row) {
+    const int lane = threadIdx.x & 31;
+    int lo = 0, cnt = num_req;  // the answer lies in [lo, lo + cnt); cu[lo] qualifies
+    while (true) {
+        const int step = (cnt + 31) / 32;
+        const bool probe = lane * step < cnt;
+        const int idx = lo + (probe ? lane * step : 0);
+        const bool ok = probe && (uint64_t)H * (uint32_t)__ldg(cu + idx) <= row;
+        const unsigned bal = __ballot_sync(0xffffffffu, ok);  // lane 0 always set
+        const int k = 31 - __clz(bal);
+        if (step == 1) return lo + k;
+        const int hi = lo + cnt;
+        lo += k * step;
+        cnt = min(step, hi - lo);
     }
-    return lo;
 }
 
 // all rows of [first, row_end) belong to one request of length L whose block
@@ -62,17 +72,13 @@ __device__ __forceinline__ void packed_body(T* __restrict__ scores, const int32_
     constexpr int VE = VB / (int)sizeof(T);
     constexpr int GPB = NT / 32;
     constexpr int CAP = 32 * NV * VE;
-    __shared__ int req[2];
     const uint32_t dev_rows = H * (uint32_t)__ldg(cu + num_req);
     const uint32_t first = blockIdx.x * (uint32_t)(GPB * rpg);
     const uint32_t row_end = min(min(total_rows, dev_rows), first + (uint32_t)(GPB * rpg));
     if (first >= row_end) return;  // uniform per CTA
-    if (threadIdx.x == 0) {
-        req[0] = find_req(cu, num_req, H, first);
-        req[1] = find_req(cu, num_req, H, row_end - 1);
-    }
-    __syncthreads();
-    const int r0 = req[0], r1 = req[1];
+    // every warp finds the requests of the CTA's first and last rows itself
+    const int r0 = find_req_warp(cu, num_req, H, first);
+    const int r1 = find_req_warp(cu, num_req, H, row_end - 1);
     if (r0 == r1) {
         const int L = min(__ldg(cu + r0 + 1) - __ldg(cu + r0), CAP);
         const int64_t base = __ldg(blocks + r0);
@@ -93,7 +99,7 @@ __device__ __forceinline__ void packed_body(T* __restrict__ scores, const int32_
     // the CTA straddles requests: one row per warp, looked up per row
     const int lane = threadIdx.x & 31;
     for (uint32_t row = first + (threadIdx.x >> 5); row < row_end; row += GPB) {
-        const int r = find_req(cu, num_req, H, row);
+        const int r = find_req_warp(cu, num_req, H, row);
         const int L = min(__ldg(cu + r + 1) - __ldg(cu + r), CAP);
         const uint32_t row0 = H * (uint32_t)__ldg(cu + r);
         T* p = scores + __ldg(blocks + r) + (int64_t)(row - row0) * L;

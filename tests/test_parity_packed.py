@@ -56,6 +56,21 @@ def test_many_tiny_requests_straddle_ctas(ttlib, dtype):
     assert_close("softmax", dtype, y, oracle.softmax_packed(x, lens, 2, W.SCALE_BERT), "tiny")
 
 
+@pytest.mark.parametrize("num_req", [33, 1025, 40000])
+def test_many_requests_search_rounds(ttlib, num_req):
+    """The warp-parallel request search (32 probes per round, softmax_packed.cu
+    find_req_warp) over 2, 3 and 4 rounds: many short requests with empty ones
+    (equal cu_seqlens entries) mixed in, CTAs inside and across requests."""
+    rng = np.random.default_rng(num_req)
+    lens = rng.integers(0, 24, size=num_req)
+    lens[rng.choice(num_req, num_req // 7, replace=False)] = 0
+    lens[-1] = 17
+    x = _packed_input(lens, 2, torch.float16, seed=num_req)
+    y = _run(ttlib, x, lens, 2, W.SCALE_BERT)
+    assert_close("softmax", torch.float16, y, oracle.softmax_packed(x, lens, 2, W.SCALE_BERT),
+                 f"{num_req} requests")
+
+
 @pytest.mark.parametrize("dtype", DT)
 def test_length_boundaries_and_max(ttlib, dtype):
     cap = 1024 if dtype == torch.float32 else 2048
