@@ -180,7 +180,7 @@ const PackedTier kPk_f32[] = {TT_PK(float, "f32", 1, 6), TT_PK(float, "f32", 2, 
                               TT_PK(float, "f32", 3, 4), TT_PK(float, "f32", 4, 4)};
 const PackedTier kPk_f16[] = {TT_PK(__half, "f16", 1, 5), TT_PK(__half, "f16", 2, 4),
                               TT_PK(__half, "f16", 3, 2), TT_PK(__half, "f16", 4, 2)};
-const PackedTier kPk_bf16[] = {TT_PK(__nv_bfloat16, "bf16", 1, 6),
+const PackedTier kPk_bf16[] = {TT_PK(__nv_bfloat16, "bf16", 1, 5),
                                TT_PK(__nv_bfloat16, "bf16", 2, 4),
                                TT_PK(__nv_bfloat16, "bf16", 3, 2),
                                TT_PK(__nv_bfloat16, "bf16", 4, 2)};

@@ -3,9 +3,22 @@
 // kernel (softmax_packed.cu).  See softmax.cu for the design notes.
 #pragma once
 
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace tt {
+
+// f16 bit pattern of the small integer n (0 <= n < 2048), exact
+__host__ __device__ constexpr uint32_t f16_int_bits(int n) {
+    int e = 0;
+    while (n >> (e + 1)) ++e;
+    return n == 0 ? 0u : (uint32_t)(((e + 15) << 10) | ((n - (1 << e)) << (10 - e)));
+}
+// the key indices (2 i, 2 i + 1) of word i of a vector, as an f16x2 pair
+__host__ __device__ constexpr uint32_t f16_pair_index(int i) {
+    return f16_int_bits(2 * i) | (f16_int_bits(2 * i + 1) << 16);
+}
 
 __device__ __forceinline__ float rcp_approx(float x) {
     float y;
@@ -107,15 +120,46 @@ __device__ __forceinline__ void row_finish(T* __restrict__ p, bool live, int L, 
     const bool dead_slots = FULLROW && !masked && (nv != GC * NVC);
 
     float v[NVC][VE];
-#pragma unroll
-    for (int k = 0; k < NVC; ++k) Elem<T>::template unpack<VB>(r.raw[k], v[k]);
-    if (masked) {
+    // (not in the 16-bit G8 x NV5 tier: there the word masks made ptxas spill
+    // 36-48 bytes of the row at its 64-register cap)
+    constexpr bool kWordMask = sizeof(T) == 2 && !(GC == 8 && NVC == 5);
+    if constexpr (kWordMask) {
+        // 16-bit storage: the key mask on the packed words before unpacking --
+        // per pair of keys one HSET2 (key index < nvalid, both halves at once,
+        // indices as exact f16 constants) and one LOP3 that swaps the masked
+        // halves for the sentinel's bit pattern: 1 instruction per key instead
+        // of an ISETP + FSEL after the conversion
+        constexpr uint32_t kSentH =
+            std::is_same<T, __half>::value ? (UP ? 0xFC00u : 0x7C00u) : (UP ? 0xFF80u : 0x7F80u);
+        constexpr uint32_t kSent2 = kSentH | (kSentH << 16);
 #pragma unroll
         for (int k = 0; k < NVC; ++k) {
-            const int vi = q + k * GC;
-            const int nvalid = vi < nv ? min(max(L - (hd + vi * VE), 0), VE) : 0;
+            Raw<VB> w = r.raw[k];
+            if (masked) {
+                const int vi = q + k * GC;
+                const int nvalid = vi < nv ? min(max(L - (hd + vi * VE), 0), VE) : 0;
+                const uint32_t h = __half_as_ushort(__int2half_rn(nvalid));
+                const uint32_t h2 = h | (h << 16);
 #pragma unroll
-            for (int e = 0; e < VE; ++e) v[k][e] = e < nvalid ? v[k][e] : sent;
+                for (int i = 0; i < Raw<VB>::W; ++i) {
+                    uint32_t m;
+                    asm("set.lt.u32.f16x2 %0, %1, %2;" : "=r"(m) : "r"(f16_pair_index(i)), "r"(h2));
+                    w.w[i] = (w.w[i] & m) | (kSent2 & ~m);
+                }
+            }
+            Elem<T>::template unpack<VB>(w, v[k]);
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < NVC; ++k) Elem<T>::template unpack<VB>(r.raw[k], v[k]);
+        if (masked) {
+#pragma unroll
+            for (int k = 0; k < NVC; ++k) {
+                const int vi = q + k * GC;
+                const int nvalid = vi < nv ? min(max(L - (hd + vi * VE), 0), VE) : 0;
+#pragma unroll
+                for (int e = 0; e < VE; ++e) v[k][e] = e < nvalid ? v[k][e] : sent;
+            }
         }
     }
     float hv[HIA], tv[HIA];
