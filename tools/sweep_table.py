@@ -6,7 +6,8 @@ import sys
 
 print("# tools/sweep.py: device time per call (CUDA-graph replay), algorithmic GB/s, % of the "
       "measured copy peak, % of nominal 8 TB/s; ref = same-traffic torch SM kernel (neg / add) in "
-      "the same mode; err = max abs error vs the fp64 oracle on 256 sampled rows")
+      "the same mode, moving the op's algorithmic bytes, and (ref/ours) its time over ours; err = max "
+      "abs error vs the fp64 oracle on 256 sampled rows")
 for line in open(sys.argv[1]):
     d = json.loads(line)
     if "config" not in d:
@@ -18,4 +19,5 @@ for line in open(sys.argv[1]):
     print(f"{d['config']:<14} {d['op']:<19} {d['dtype']:<4} {str(d['shape']):<22} "
           f"{'ragged' if d['ragged'] else 'full':<10} {d['us']:>7.2f} us {d['GBps']:>9.1f} GB/s "
           f"{d['pct_peak']:>5.1f}% " + (f"({nom:>5.1f}% nom) " if nom is not None else "") +
-          f" ref {ref} us " + (f" err {err:.2e} " if err is not None else "") + f" {d['tier']}")
+          f" ref {ref} us ({100 * float(ref) / d['us']:.0f}%) " +
+          (f" err {err:.2e} " if err is not None else "") + f" {d['tier']}")
