@@ -217,7 +217,7 @@ struct LnTier {
     /* selected through the preference tables kLnPref* */                                    \
     TT_LN_TIER(false, T, TN, 32, 32, 3, 1, 256, 1), TT_LN_TIER(false, T, TN, 32, 32, 4, 1, 256, 1), \
     TT_LN_TIER(false, T, TN, 32, 32, 4, 1, 128, 1), TT_LN_TIER(false, T, TN, 32, 32, 2, 1, 256, 1), \
-    TT_LN_TIER(false, T, TN, 16, 32, 3, 1, 256, 1),                                        \
+    TT_LN_TIER(false, T, TN, 16, 32, 3, 1, 256, 1), TT_LN_TIER(false, T, TN, 32, 16, 3, 1, 256, 1), \
     TT_LN_EARLY(false, T, TN, 16, 32, 3, 128), TT_LN_EARLY(false, T, TN, 16, 32, 3, 256),        \
     TT_LN_EARLY(false, T, TN, 32, 32, 2, 128), TT_LN_EARLY(false, T, TN, 32, 32, 2, 256),        \
     TT_LN_EARLY(false, T, TN, 32, 32, 3, 256), TT_LN_EARLY(false, T, TN, 32, 32, 4, 256),        \
@@ -246,7 +246,7 @@ struct LnTier {
     TT_LN_WARP(false, T, TN, 16, 32, 3, 128, 6), TT_LN_WARP(false, T, TN, 16, 32, 4, 128, 6),   \
     TT_LN_WARP(false, T, TN, 32, 32, 2, 128, 6), TT_LN_WARP(false, T, TN, 32, 32, 3, 128, 6),   \
     TT_LN_TIER(false, T, TN, 32, 32, 3, 2, 256, 1), TT_LN_TIER(false, T, TN, 32, 32, 4, 2, 256, 1), \
-    TT_LN_TIER(false, T, TN, 32, 16, 3, 1, 256, 1), TT_LN_TIER(false, T, TN, 32, 16, 4, 1, 256, 1), \
+    TT_LN_TIER(false, T, TN, 32, 16, 4, 1, 256, 1),                                        \
     TT_LN_TIER(false, T, TN, 16, 32, 4, 1, 256, 1), TT_LN_TIER(false, T, TN, 16, 32, 6, 1, 256, 1), \
     TT_LN_TIER(false, T, TN, 32, 32, 2, 2, 128, 4),                                        \
     TT_LN_TIER(false, T, TN, 32, 32, 2, 1, 256, 3), TT_LN_TIER(false, T, TN, 16, 32, 4, 1, 128, 6), \
@@ -306,6 +306,15 @@ const Pref kLnPrefSmall[] = {
     {1, 768, 1024, "ln_rows<f16,V32,G32,NV2,R1,T256,M1>"},
     {2, 512, 768, "ln_rows<bf16,V16,G32,NV3,R1,T128,M1>"},
     {2, 768, 1024, "ln_rows<bf16,V32,G32,NV2,R1,T256,M1>"},
+};
+// Just past one full wave of the 128-thread tier (4 rows per CTA; at hidden 768
+// fp16 one wave holds ~5 300 rows): half-warp rows in 256-thread CTAs (16 rows
+// per CTA) take the whole call in one wave.  tools/tune.py (profiles/r02_ln_wave/):
+// 6000 rows 8.46 -> 7.34 us, while 5120 (6.39 vs 6.92) and 8000 rows (9.56 vs
+// 10.88) stay on the 128-thread tier.
+constexpr int64_t kWaveLo = 5400, kWaveHi = 7000;
+const Pref kLnPrefWave[] = {
+    {1, 512, 768, "ln_rows<f16,V32,G16,NV3,R1,T256,M1>"},
 };
 // Very few rows: one CTA (four warps) per row, so the rows spread over as many
 // SMs as there are rows and every thread issues only a few loads (re-tuned on
@@ -382,6 +391,9 @@ const LnTier* pick_dtype(int dtype, int64_t hidden, int vec_bytes, int64_t rows)
         rows <= kMicroRows  ? from_prefs(kLnPrefMicro, idx_micro, dtype, hidden, vec_bytes)
         : rows <= kMiniRows ? from_prefs(kLnPrefMini, idx_mini, dtype, hidden, vec_bytes)
                             : nullptr;
+    static std::atomic<int> idx_wave[sizeof(kLnPrefWave) / sizeof(Pref)];
+    if (!pbest && rows > kWaveLo && rows <= kWaveHi)
+        pbest = from_prefs(kLnPrefWave, idx_wave, dtype, hidden, vec_bytes);
     if (!pbest)
         pbest = rows <= kTinyRows    ? from_prefs(kLnPrefTiny, idx_tiny, dtype, hidden, vec_bytes)
                 : rows <= kSmallRows ? from_prefs(kLnPrefSmall, idx_small, dtype, hidden, vec_bytes)
