@@ -308,13 +308,14 @@ const Pref kLnPrefSmall[] = {
     {2, 768, 1024, "ln_rows<bf16,V32,G32,NV2,R1,T256,M1>"},
 };
 // Just past one full wave of the 128-thread tier (4 rows per CTA; at hidden 768
-// fp16 one wave holds ~5 300 rows): half-warp rows in 256-thread CTAs (16 rows
+// 16-bit one wave holds ~5 300 rows): half-warp rows in 256-thread CTAs (16 rows
 // per CTA) take the whole call in one wave.  tools/tune.py (profiles/r02_ln_wave/):
 // 6000 rows 8.46 -> 7.34 us, while 5120 (6.39 vs 6.92) and 8000 rows (9.56 vs
 // 10.88) stay on the 128-thread tier.
 constexpr int64_t kWaveLo = 5400, kWaveHi = 7000;
 const Pref kLnPrefWave[] = {
     {1, 512, 768, "ln_rows<f16,V32,G16,NV3,R1,T256,M1>"},
+    {2, 512, 768, "ln_rows<bf16,V32,G16,NV3,R1,T256,M1>"},  // 6000 / 7000 rows: 7.1 / 7.6 us
 };
 // Very few rows: one CTA (four warps) per row, so the rows spread over as many
 // SMs as there are rows and every thread issues only a few loads (re-tuned on
