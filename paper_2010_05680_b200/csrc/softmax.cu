@@ -132,22 +132,23 @@ cudaError_t launch_softmax_warp(void* scores, const int32_t* lengths, int64_t nr
     // RPG > 0: fixed rows per group; RPG = 0: one persistent wave (rows spread
     // evenly over SMs x resident CTAs).
     int rpg = RPG;
+    static std::atomic<int> occ_cache[3] = {{0}, {0}, {0}};
+    int occ = occ_cache[kv].load(std::memory_order_relaxed);
+    if (!occ) {
+        cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT, 0);
+        if (e != cudaSuccess) return e;
+        occ = occ > 0 ? occ : 1;
+        occ_cache[kv].store(occ);
+    }
     if (RPG == 0) {
-        static std::atomic<int> occ_cache[3] = {{0}, {0}, {0}};
-        int occ = occ_cache[kv].load(std::memory_order_relaxed);
-        if (!occ) {
-            cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT, 0);
-            if (e != cudaSuccess) return e;
-            occ = occ > 0 ? occ : 1;
-            occ_cache[kv].store(occ);
-        }
         const int64_t slots = (int64_t)sm_count() * occ * GPB;
         rpg = (int)((nrows + slots - 1) / slots);
     } else {
-        // small problems are latency-bound: give every group a single row
-        // rather than a few CTAs walking RPG rows each (at least 2 CTAs of
-        // work per SM before rows are chained)
-        const int64_t spread = (int64_t)sm_count() * 2 * GPB;
+        // problems that fit a wave are latency-bound: the shortest chain of
+        // rows per group that still keeps the call in one wave of resident
+        // CTAs (every slot of every SM), rather than RPG rows per group on a
+        // part-empty wave (round 1 used 2 CTAs per SM here)
+        const int64_t spread = (int64_t)sm_count() * occ * GPB;
         const int64_t need = (nrows + spread - 1) / spread;
         if (need < rpg) rpg = need > 0 ? (int)need : 1;
     }
