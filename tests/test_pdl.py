@@ -178,3 +178,45 @@ def test_attention_block_chain_pdl_on_off_identical(ttlib, variant):
         ttlib.attention_variant(0)
     assert torch.isfinite(outs[True].float()).all()
     assert torch.equal(outs[False].view(torch.int16), outs[True].view(torch.int16))
+
+
+_FRESH_CAPTURE = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+import paper_2010_05680_b200 as tt, workloads as W, oracle
+# the library's first calls happen INSIDE a stream capture: the per-kernel
+# occupancy query (rows per group, softmax.cu) and the dynamic-smem opt-in
+# must be legal there
+lens = np.array([100, 37, 64, 1], dtype=np.int32)
+x = W.scores(4, 12, 100, 100, torch.float16, seed=3)
+y = x.cuda()
+L = torch.as_tensor(lens).cuda()
+d = W.ln_inputs(4000, 768, torch.float16, seed=4)
+dd = {k: v.cuda() for k, v in d.items()}
+out = torch.empty_like(dd["x"])
+s = torch.cuda.Stream()
+g = torch.cuda.CUDAGraph()
+with torch.cuda.graph(g, stream=s):
+    tt.tt_softmax_masked(y, L, 0.125)
+    tt.tt_add_bias_layernorm(out, dd["x"], dd["residual"], dd["bias"], dd["gamma"], dd["beta"], 1e-12)
+y.copy_(x.cuda())
+g.replay()
+torch.cuda.synchronize()
+ref = oracle.softmax_masked(x, lens, 0.125)
+assert (y.cpu().double() - ref).abs().max().item() < 2e-3
+refl = oracle.add_bias_layernorm(d["x"], d["residual"], d["bias"], d["gamma"], d["beta"], 1e-12)
+assert (out.cpu().double() - refl).abs().max().item() < 2e-2
+print("ok")
+"""
+
+
+@pytest.mark.gpu
+def test_first_calls_inside_graph_capture():
+    """A fresh process whose first library calls are captured into a CUDA graph."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", _FRESH_CAPTURE, root], capture_output=True,
+                       text=True, timeout=600)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr
