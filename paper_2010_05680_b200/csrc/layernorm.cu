@@ -298,7 +298,12 @@ struct Pref {
 // (profiles/r02_ln/): at hidden 768 the 128-thread ln_rows tiers win from
 // 5120 to 10000 rows (fp16 10.9 us vs 11.7 for the persistent warp tier at
 // 10000 rows; fp32 16.8 vs 17.9 us).
-constexpr int64_t kTinyRows = 2048, kSmallRows = 16384;
+// kSmallRows re-measured on the final round-2 build (profiles/r02_ln_band/): from 12 000
+// rows the large-call tiers win -- 16-bit hidden 768 persistent ln_warp (16 384 rows 15.5 vs
+// 16.8 us, 12 000 rows 12.8 vs 13.1), bf16 hidden 1024 T64 (12 000 rows 14.9 vs 15.2), fp32
+// hidden 1024 T128 (26.7 vs 27.1) -- while at 11 000 rows (fp16 hidden 768) the 128-thread
+// tier still does (12.4 vs 12.6 us).
+constexpr int64_t kTinyRows = 2048, kSmallRows = 11500;
 const Pref kLnPrefSmall[] = {
     {0, 512, 768, "ln_rows<f32,V32,G32,NV3,R1,T128,M1>"},
     {0, 768, 1024, "ln_rows<f32,V32,G32,NV4,R1,T256,M1>"},

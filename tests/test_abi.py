@@ -144,6 +144,10 @@ def test_softmax_tier_plan(ttlib, dtype, Sk, tier):
     (torch.float16, 800, 768, "ln_rows<f16,V16,G128,NV4,R1,T128,M1>"),
     (torch.float16, 2000, 768, "ln_rows<f16,V32,G32,NV2,R1,T128,M1,E>"),
     (torch.float16, 30000, 768, "ln_warp<f16,V16,G32,NV3,T256,M3,PF0>"),
+    (torch.float16, 6000, 768, "ln_rows<f16,V32,G16,NV3,R1,T256,M1>"),   # one-wave band
+    (torch.bfloat16, 7000, 768, "ln_rows<bf16,V32,G16,NV3,R1,T256,M1>"),
+    (torch.float16, 11000, 768, "ln_rows<f16,V16,G32,NV3,R1,T128,M1>"),
+    (torch.float16, 12000, 768, "ln_warp<f16,V16,G32,NV3,T256,M3,PF0>"),  # kSmallRows = 11500
     (torch.bfloat16, 31808, 768, "ln_warp<bf16,V16,G32,NV3,T256,M3,PF0>"),
     (torch.bfloat16, 10, 1024, "ln_rows<bf16,V32,G32,NV2,R1,T256,M1,E>"),
     (torch.bfloat16, 32768, 1024, "ln_rows<bf16,V32,G32,NV2,R1,T64,M12>"),
